@@ -1,0 +1,444 @@
+"""Benchmark: per-gate HBM bandwidth of the state-vector engine (BASELINE cfg2)
+plus random-circuit sec/layer (cfg4), with a roofline and a CPU baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N=1, BASELINE.json configs[1]): the 28-qubit per-gate sweep --
+H, RX(theta_t), RZ(theta_t), CNOT((t+1)%n, t), CZ(t, (t+1)%n) on every target
+t = 0..27 of a random complex128 state; one step = the full 140-gate sweep.
+``value`` = algorithmic HBM bytes of the sweep / device time (GB/s), bytes per
+gate from SURVEY.md 8(d): 32*2^n for H/RX/RZ, 32*2^(n-1) for CNOT (only the
+control-1 half moves), 32*2^(n-2) for CZ (only |11> changes).  The state
+(4 GiB) is 32x the 126 MB L2, so no flush is needed between timed steps.
+
+``random_circuit`` (extra object): cfg4, cz-ladder(30, depth 20, seed 1)
+compiled by the native planner, sec/layer = circuit time / 21 layers.
+
+``--impl reference``: the reference's algorithm on the host CPU (the numpy
+port in oracle/, all host threads through the reference's own chunking),
+same metric on a bounded sample of the same sweep.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GATE_KINDS = ("H", "RX", "RZ", "CNOT", "CZ")
+
+
+def gate_bytes(kind: str, n: int) -> float:
+    if kind == "CNOT":
+        return 32.0 * 2 ** (n - 1)
+    if kind == "CZ":
+        return 32.0 * 2 ** (n - 2)
+    return 32.0 * 2 ** n
+
+
+def sweep_spec(n):
+    """(kind, target, angle) for the cfg2 sweep in execution order."""
+    out = []
+    for t in range(n):
+        theta = float(np.random.default_rng(t).uniform(0, 2 * np.pi))
+        for k in GATE_KINDS:
+            out.append((k, t, theta))
+    return out
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (numpy port in oracle/) on host cores
+def cpu_sweep_sample(n, num_gates, threads, start=0, amps=None):
+    """Time ``num_gates`` gates of the cfg2 sweep at width n with the oracle
+    port; returns (bytes, seconds, description)."""
+    from oracle import qsim_oracle as orc
+    orc.set_threads(threads)
+    if amps is None:
+        amps = np.full(1 << n, (1.0 + 0.0j) / math.sqrt(1 << n), dtype=np.complex128)
+    spec = sweep_spec(n)
+    # spread the sample over kinds and targets
+    picks = [spec[(start + i * 37) % len(spec)] for i in range(num_gates)]
+    tot_b = tot_s = 0.0
+    for kind, t, theta in picks:
+        rec = _oracle_record(kind, t, theta, n)
+        t0 = time.perf_counter()
+        orc.apply_record(amps, n, rec)
+        tot_s += time.perf_counter() - t0
+        tot_b += gate_bytes(kind, n)
+    desc = ", ".join(f"{k}@{t}" for k, t, _ in picks)
+    return tot_b, tot_s, desc
+
+
+def _oracle_record(kind, t, theta, n):
+    h = np.array([[1, 1], [1, -1]], dtype=np.complex128) / np.sqrt(2)
+    if kind == "H":
+        return ("dense", (t,), h, ())
+    if kind == "RX":
+        return ("pauli_rot", (t,), (1,), theta, ())
+    if kind == "RZ":
+        return ("pauli_rot", (t,), (3,), theta, ())
+    if kind == "CNOT":
+        return ("pauli", (t,), (1,), (((t + 1) % n, 1),))
+    return ("diag", ((t + 1) % n,), np.array([1, -1], dtype=np.complex128), ((t, 1),))
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU algorithm, rank 0 only."""
+    if rank != 0:
+        return
+    n = args.qubits
+    threads = os.cpu_count() or 1
+    steps, warm = args.steps, args.warmup
+    # each step = a bounded sample of the sweep (1 gate at 28 qubits)
+    per_step = max(1, args.ref_gates_per_step)
+    amps = np.full(1 << n, (1.0 + 0.0j) / math.sqrt(1 << n), dtype=np.complex128)
+    for w in range(warm):
+        cpu_sweep_sample(min(n, 20), per_step, threads, start=w)
+    tb = ts = 0.0
+    descs = []
+    for s in range(steps):
+        b, t, d = cpu_sweep_sample(n, per_step, threads, start=s * per_step, amps=amps)
+        tb += b
+        ts += t
+        descs.append(d)
+    value = tb / ts / 1e9
+    line = {
+        "impl": "reference",
+        "metric": "per-gate HBM GB/s vs 8 TB/s peak (cfg2 28-qubit H/RX/RZ/CNOT/CZ sweep)",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": ts / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (uniform superposition)",
+        "config": {"workload": f"cfg2 per-gate sweep, n={n}", "qubits": n,
+                   "sample": f"{per_step} gate(s)/step: " + "; ".join(descs)},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} steps x {per_step} gate(s) at n={n}, "
+                                   "numpy port of qsimcore kernels (oracle/qsim_oracle.py), "
+                                   "reference thread chunking with QSIM_NUM_THREADS=nproc"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def build_gates(n):
+    from paper_2011_13524_b200 import gate as qg
+    out = []
+    for kind, t, theta in sweep_spec(n):
+        if kind == "H":
+            g = qg.H(t)
+        elif kind == "RX":
+            g = qg.RX(t, theta)
+        elif kind == "RZ":
+            g = qg.RZ(t, theta)
+        elif kind == "CNOT":
+            g = qg.CNOT((t + 1) % n, t)
+        else:
+            g = qg.CZ(t, (t + 1) % n)
+        out.append((kind, t, g))
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2011_13524_b200 as qs
+    from paper_2011_13524_b200 import workloads
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    n = args.qubits
+    gates = build_gates(n)
+    st = qs.QuantumState(n, device=dev)
+    st.set_stream(stream.cuda_stream)
+    st.set_random_state_device(1234 + rank)
+    bytes_step = sum(gate_bytes(k, n) for k, _, _ in gates)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(args.warmup):
+        for _, _, g in gates:
+            g.update_quantum_state(st)
+    torch.cuda.synchronize(dev)
+
+    # timed region: device events around the whole sweep and around each gate
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps * len(gates))]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clk:
+        start.record(stream)
+        i = 0
+        for _ in range(args.steps):
+            for _, _, g in gates:
+                ev[i][0].record(stream)
+                g.update_quantum_state(st)
+                ev[i][1].record(stream)
+                i += 1
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    if dist is not None:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = bytes_step * args.steps * world / (elapsed_ms / 1e3) / 1e9
+
+    # per-kind kernel durations (the dominant kernel for the roofline)
+    per_kind = {k: [0.0, 0.0, 0] for k in GATE_KINDS}
+    i = 0
+    for _ in range(args.steps):
+        for kind, _, _ in gates:
+            ms = ev[i][0].elapsed_time(ev[i][1])
+            per_kind[kind][0] += ms
+            per_kind[kind][1] += gate_bytes(kind, n)
+            per_kind[kind][2] += 1
+            i += 1
+    peak, peak_kind = measured_peaks()
+    kinds_out = {k: {"gbs": v[1] / (v[0] / 1e3) / 1e9, "ms_avg": v[0] / v[2],
+                     "frac_of_peak": v[1] / (v[0] / 1e3) / 1e9 / peak}
+                 for k, v in per_kind.items() if v[2]}
+    # dominant kernel: k_pair2x2 (1-qubit dense; H and RX, the largest share)
+    dom_ms = per_kind["H"][0] + per_kind["RX"][0]
+    dom_b = per_kind["H"][1] + per_kind["RX"][1]
+    dom_n = per_kind["H"][2] + per_kind["RX"][2]
+    achieved = dom_b / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                traffic = json.load(fh).get("k_pair2x2_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if rank == 0 or world > 1:
+        host = torch.empty(2 << n, dtype=torch.float64).pin_memory()
+        hv = host.numpy().view(np.complex128)
+        st.get_vector(out=hv)
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            st.load(hv)
+            for _, _, g in gates:
+                g.update_quantum_state(st)
+            st.get_vector(out=hv)
+        torch.cuda.synchronize(dev)
+        e2e_s = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": bytes_step * e2e_steps * world / e2e_s / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 16 << n, "d2h_bytes_per_step": 16 << n,
+               "steps": e2e_steps}
+        del host, hv
+
+    extra = {}
+    if rank == 0 and not args.skip_circuit:
+        extra["random_circuit"] = run_random_circuit(args, dev, stream, qs, workloads, torch)
+        del st
+        torch.cuda.empty_cache()
+    if rank == 0 and not args.skip_cpu:
+        b, s, desc = cpu_sweep_sample(n, args.cpu_gates, os.cpu_count() or 1)
+        cpu = {"value": b / s / 1e9, "unit": "GB/s", "cores": os.cpu_count() or 1,
+               "kind": "port",
+               "sample": f"{args.cpu_gates} gates of the n={n} sweep ({desc}); numpy port "
+                         "of the qsimcore kernels (oracle/qsim_oracle.py), reference "
+                         "thread chunking with nproc threads"}
+    else:
+        cpu = None
+
+    if rank != 0:
+        return
+    launches = args.steps * sum(1 for _ in gates)
+    line = {
+        "metric": "per-gate HBM GB/s vs 8 TB/s peak (cfg2 28-qubit H/RX/RZ/CNOT/CZ sweep)",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (device-generated random state)",
+        "config": {"workload": f"cfg2 per-gate sweep: 5 gates x {n} targets, n={n} qubits "
+                               "per GPU", "qubits": n, "gates_per_step": len(gates),
+                   "bytes_per_step": bytes_step,
+                   "l2": "state 16*2^n B >> 126 MB L2, no flush needed",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_pair2x2 (1-qubit dense: H, RX)", "launches": dom_n,
+                     "bytes_per_launch": dom_b / max(1, dom_n), "peak_source": peak_kind,
+                     "frac_of_8TBs": achieved / 8000.0},
+        "per_gate": kinds_out,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    line.update(extra)
+    print(json.dumps(line), flush=True)
+
+
+def run_random_circuit(args, dev, stream, qs, workloads, torch):
+    """cfg4: cz-ladder(n=30, depth 20, seed 1) through the native planner."""
+    n, depth = args.circuit_qubits, 20
+    circ = workloads.generate_cz_ladder(n, depth, seed=1)
+    gates_in = circ.get_gate_count()
+    t0 = time.perf_counter()
+    stats = circ.program_stats()
+    plan_s = time.perf_counter() - t0
+    st = qs.QuantumState(n, device=dev)
+    st.set_stream(stream.cuda_stream)
+    st.set_random_state_device(99)
+    circ.update_quantum_state(st)  # warm (graph capture)
+    torch.cuda.synchronize(dev)
+    times = []
+    for _ in range(args.circuit_reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        circ.update_quantum_state(st)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        times.append(a.elapsed_time(b) / 1e3)
+    best = min(times)
+    out = {"metric": "random-circuit sec/layer", "unit": "s/layer",
+           "value": best / (depth + 1), "higher_is_better": False,
+           "workload": f"cz-ladder n={n} depth={depth} seed=1 ({gates_in} gates), "
+                       "native planner (fusion + tile passes)",
+           "circuit_s_best": best, "circuit_s_all": times, "plan_s": plan_s,
+           "program": stats,
+           "hbm_gbs_effective": stats.get("hbm_bytes", 0.0) / best / 1e9}
+    del st
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--qubits", type=int, default=28)
+    ap.add_argument("--circuit-qubits", type=int, default=30)
+    ap.add_argument("--circuit-reps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-gates", type=int, default=3)
+    ap.add_argument("--ref-gates-per-step", type=int, default=1)
+    ap.add_argument("--skip-circuit", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

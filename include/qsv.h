@@ -1,0 +1,171 @@
+/*
+ * qsv.h -- C ABI of the B200 state-vector engine (libqsv.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (qsimcore, /root/reference/pkg/src/qsimcore) has no C ABI; its seam is the
+ * Python kernel layer `kernels.apply_*(amps, num_qubits, targets, payload,
+ * controls)` reached only through `BasicGate._apply_kernel`
+ * (gates.py:98-100).  Each entry point below replaces one function of that
+ * layer (or of the state container) and says which.  The Python package
+ * `paper_2011_13524_b200` binds these through ctypes;
+ * argument validation that raises ValueError in the reference stays in that
+ * Python layer, the library re-checks and returns QSV_EINVAL.
+ *
+ * Conventions
+ *   - amplitudes are complex128 = two little-endian float64 (re, im);
+ *     qubit i is bit i of the amplitude index (state.py:1-6);
+ *   - matrices are row-major 2^m x 2^m interleaved complex; bit j of a
+ *     row/column index refers to targets[j] (kernels.py:42-52);
+ *   - controls are (qubit, value) pairs, value 0 or 1 (gates.py:108-123);
+ *   - every call returns QSV_OK (0) or a negative code; qsv_last_error()
+ *     returns a thread-local message for the last failing call;
+ *   - work is enqueued on the state's stream (default: the legacy default
+ *     stream, so torch.cuda events see it); calls that return host data
+ *     (qsv_get, qsv_norm2, qsv_inner, qsv_expect) synchronise that stream;
+ *   - a handle is not thread-safe (same contract as the reference,
+ *     SPEC.md:177 / _handles.py:1-7).
+ */
+#ifndef QSV_H
+#define QSV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSV_OK 0
+#define QSV_EINVAL (-1)      /* bad argument  -> Python ValueError   */
+#define QSV_ENOMEM (-2)      /* cudaMalloc    -> Python MemoryError  */
+#define QSV_ECUDA (-3)       /* CUDA failure  -> Python RuntimeError */
+#define QSV_EUNSUPPORTED (-4)
+
+#define QSV_MAX_TARGETS 12   /* largest dense / diagonal target count */
+#define QSV_MAX_CONTROLS 16
+
+typedef struct qsv_state qsv_state;
+typedef struct qsv_program qsv_program;
+
+/* ------------------------------------------------------------ library */
+const char* qsv_last_error(void);
+int qsv_version(void);
+int qsv_device_count(int* out);
+
+/* --------------------------------------------------------------- state
+ * qsv_state_create        <- StateVector.__init__ (state.py:25-30):
+ *                            2^n amplitudes set to |0...0>.
+ * qsv_set_zero            <- set_zero_state (state.py:32-34)
+ * qsv_set_basis           <- set_computational_basis (state.py:36-44)
+ * qsv_load / qsv_get      <- load / get_vector (state.py:63-73); the host
+ *                            buffer may be pageable or pinned.
+ * qsv_load_range/get_range   partial transfers (shards, chunked I/O).
+ * qsv_copy                <- copy (state.py:56-61), device to device.
+ * qsv_set_random_device   non-parity device-generated random state for
+ *                         benchmark inputs only (set_haar_random stays
+ *                         host-side numpy for bit-exact parity).
+ */
+int qsv_state_create(int num_qubits, int device, qsv_state** out);
+int qsv_state_destroy(qsv_state* st);
+int qsv_state_num_qubits(const qsv_state* st, int* out);
+int qsv_state_device_ptr(const qsv_state* st, void** out);
+int qsv_set_stream(qsv_state* st, void* cuda_stream);
+int qsv_get_stream(const qsv_state* st, void** cuda_stream);
+int qsv_sync(qsv_state* st);
+
+int qsv_set_zero(qsv_state* st);
+int qsv_set_basis(qsv_state* st, uint64_t index);
+int qsv_load(qsv_state* st, const double* interleaved, uint64_t n_amps);
+int qsv_get(const qsv_state* st, double* interleaved_out, uint64_t n_amps);
+int qsv_load_range(qsv_state* st, const double* interleaved, uint64_t offset, uint64_t count);
+int qsv_get_range(const qsv_state* st, double* interleaved_out, uint64_t offset, uint64_t count);
+int qsv_copy(const qsv_state* src, qsv_state* dst);
+int qsv_set_random_device(qsv_state* st, uint64_t seed);
+
+/* --------------------------------------------------------------- gates
+ * qsv_apply_dense      <- kernels.apply_dense (kernels.py:79-138), any m
+ *                         up to QSV_MAX_TARGETS, optional controls.
+ * qsv_apply_diag       <- kernels.apply_diagonal (kernels.py:155-173).
+ * qsv_apply_pauli      <- kernels.apply_pauli (kernels.py:216-220).
+ * qsv_apply_pauli_rot  <- kernels.apply_pauli_rotation
+ *                         (kernels.py:223-235): exp(+i angle P / 2).
+ * ids are Pauli ids 0=I 1=X 2=Y 3=Z (gates.py:23).
+ */
+int qsv_apply_dense(qsv_state* st, const int* targets, int m, const double* matrix,
+                    const int* control_qubits, const int* control_values, int nc);
+int qsv_apply_diag(qsv_state* st, const int* targets, int m, const double* diag,
+                   const int* control_qubits, const int* control_values, int nc);
+int qsv_apply_pauli(qsv_state* st, const int* targets, const int* ids, int m,
+                    const int* control_qubits, const int* control_values, int nc);
+int qsv_apply_pauli_rot(qsv_state* st, const int* targets, const int* ids, int m,
+                        double angle, const int* control_qubits,
+                        const int* control_values, int nc);
+
+/* ------------------------------------------------------- state algebra
+ * qsv_norm2   <- get_squared_norm (state.py:75-76)
+ * qsv_scale   <- normalize / multiply_coef (state.py:78-81, 108-109)
+ * qsv_add     <- add_state (state.py:111-114): dst += src
+ * qsv_inner   <- inner_product (state.py:136-139): <bra|ket>
+ * qsv_expect  <- GeneralOperator._accumulate (observable.py:99-104):
+ *                sum_t coef_t <bra| P_t |ket>.  Term t has term_len[t]
+ *                factors, listed consecutively in qubits[] / ids[];
+ *                coefs are interleaved complex.  bra may equal ket.
+ * All reductions are deterministic (fixed-order two-stage tree).
+ */
+int qsv_norm2(const qsv_state* st, double* out);
+int qsv_scale(qsv_state* st, double re, double im);
+int qsv_add(qsv_state* dst, const qsv_state* src);
+int qsv_inner(const qsv_state* bra, const qsv_state* ket, double out_re_im[2]);
+int qsv_expect(const qsv_state* bra, const qsv_state* ket, int nterms,
+               const int* term_len, const int* qubits, const int* ids,
+               const double* coefs, double out_re_im[2]);
+
+/* ------------------------------------------------------------ programs
+ * A program is a compiled gate list: the replacement for the per-gate loop
+ * of Circuit.update_state (circuit.py:48-55).  qsv_program_create copies the
+ * payloads to the device once, fuses runs of gates with the same support and
+ * packs the rest into tile passes (several gates per HBM sweep); run replays
+ * it on a state of the same width.
+ */
+#define QSV_OP_DENSE 1
+#define QSV_OP_DIAG 2
+#define QSV_OP_PAULI 3
+#define QSV_OP_PAULI_ROT 4
+
+typedef struct qsv_op {
+  int32_t kind;                            /* QSV_OP_*                     */
+  int32_t m;                               /* target count                 */
+  int32_t targets[QSV_MAX_TARGETS];
+  int32_t ids[QSV_MAX_TARGETS];            /* Pauli ids (PAULI, PAULI_ROT) */
+  int32_t nc;                              /* control count                */
+  int32_t control_qubits[QSV_MAX_CONTROLS];
+  int32_t control_values[QSV_MAX_CONTROLS];
+  double angle;                            /* PAULI_ROT                    */
+  const double* data;                      /* DENSE: 4^m, DIAG: 2^m complex */
+} qsv_op;
+
+typedef struct qsv_plan_opts {
+  int32_t use_tiles;      /* 1: pack gates into tile passes (default)     */
+  int32_t tile_qubits;    /* qubits per tile, 0 = engine default           */
+  int32_t fuse;           /* 1: fuse same-support runs on the host (def.)  */
+  int32_t use_graph;      /* 1: replay through a CUDA graph                */
+} qsv_plan_opts;
+
+typedef struct qsv_program_stats {
+  int32_t num_ops_in;     /* gates given to qsv_program_create             */
+  int32_t num_steps;      /* kernels launched per run                      */
+  int32_t num_tile_passes;/* of which tile passes                          */
+  int32_t num_gate_kernels;
+  double hbm_bytes;       /* algorithmic HBM bytes per run                 */
+} qsv_program_stats;
+
+int qsv_program_create(int num_qubits, const qsv_op* ops, int nops,
+                       const qsv_plan_opts* opts, qsv_program** out);
+int qsv_program_run(qsv_program* prog, qsv_state* st);
+int qsv_program_stats_get(const qsv_program* prog, qsv_program_stats* out);
+int qsv_program_destroy(qsv_program* prog);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSV_H */

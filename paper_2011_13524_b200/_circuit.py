@@ -1,0 +1,274 @@
+"""Circuits: ordered gate lists compiled into libqsv programs.
+
+Core semantics follow the reference ``Circuit`` / ``ParametricCircuit``
+(circuit.py:11-125) and the Qulacs-named handles ``QuantumCircuit`` /
+``ParametricQuantumCircuit`` (bindings __init__.py:91-149).  The reference
+runs ``for gate in gates: gate.apply(state)`` (circuit.py:54-55); here the
+gate list is lowered once into a ``qsv_program`` (fused + tiled + replayed as
+a CUDA graph by the native planner) and re-lowered only when the list or a
+rotation angle changes.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _lib
+from ._gates import BasicGate, PauliRotationGate, QuantumGate
+from ._handles import QuantumGateBase, unwrap
+from ._lib import check, lib
+
+
+class _Program:
+    """Owner of one native program handle."""
+
+    __slots__ = ("h", "stats")
+
+    def __init__(self, n, gates, opts):
+        ops = (_lib.QsvOp * max(1, len(gates)))()
+        keep = []
+        for i, g in enumerate(gates):
+            g.fill_op(ops[i], keep)
+        h = C.c_void_p()
+        check(lib.qsv_program_create(n, ops, len(gates), C.byref(opts), C.byref(h)))
+        self.h = h
+        st = _lib.QsvProgramStats()
+        check(lib.qsv_program_stats_get(h, C.byref(st)))
+        self.stats = {f: getattr(st, f) for f, _ in _lib.QsvProgramStats._fields_}
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            lib.qsv_program_destroy(h)
+            self.h = None
+
+    def run(self, state):
+        check(lib.qsv_program_run(self.h, state._handle()))
+
+
+def default_plan_opts(**kw) -> _lib.QsvPlanOpts:
+    o = _lib.QsvPlanOpts()
+    o.use_tiles = int(kw.get("use_tiles", 1))
+    o.tile_qubits = int(kw.get("tile_qubits", 0))
+    o.fuse = int(kw.get("fuse", 1))
+    o.use_graph = int(kw.get("use_graph", 1))
+    return o
+
+
+class Circuit:
+    """Ordered gate list over a fixed qubit count (circuit.py:11-72)."""
+
+    def __init__(self, num_qubits: int):
+        if num_qubits < 1:
+            raise ValueError("qubit count must be positive")
+        self.num_qubits = int(num_qubits)
+        self.gates: list[QuantumGate] = []
+        self._prog = None
+        self._prog_key = None
+        self._plan = default_plan_opts()
+
+    # -- editing -------------------------------------------------------------
+    def _check_gate(self, gate) -> None:
+        if not isinstance(gate, QuantumGate):
+            raise TypeError(f"expected a gate, got {type(gate).__name__}")
+        if not isinstance(gate, BasicGate):
+            raise ValueError("only basic gates run on the B200 engine (quantum maps are "
+                             "outside the accelerated path)")
+        top = max(gate.touched_qubits(), default=-1)
+        if top >= self.num_qubits:
+            raise ValueError(f"gate touches qubit {top} but the circuit has "
+                             f"{self.num_qubits} qubits")
+
+    def add_gate(self, gate, position=None) -> None:
+        self._check_gate(gate)
+        if position is None:
+            self.gates.append(gate)
+            return
+        if not 0 <= position <= len(self.gates):
+            raise ValueError(f"insert position {position} out of range")
+        self.gates.insert(position, gate)
+
+    def remove_gate(self, position: int) -> None:
+        if not 0 <= position < len(self.gates):
+            raise ValueError(f"position {position} out of range")
+        del self.gates[position]
+
+    def get_gate(self, position: int):
+        if not 0 <= position < len(self.gates):
+            raise ValueError(f"position {position} out of range")
+        return self.gates[position].copy()
+
+    def get_gate_count(self) -> int:
+        return len(self.gates)
+
+    def calculate_depth(self) -> int:
+        """ASAP layering over touched qubits (circuit.py:57-67)."""
+        level = [0] * self.num_qubits
+        depth = 0
+        for g in self.gates:
+            qs = g.touched_qubits()
+            layer = max((level[q] for q in qs), default=0) + 1
+            for q in qs:
+                level[q] = layer
+            depth = max(depth, layer)
+        return depth
+
+    def copy(self):
+        out = type(self).__new__(type(self))
+        Circuit.__init__(out, self.num_qubits)
+        out.gates = [g.copy() for g in self.gates]
+        out._plan = self._plan
+        return out
+
+    # -- execution -------------------------------------------------------------
+    def set_plan_options(self, **kw) -> None:
+        """Engine knobs: use_tiles, tile_qubits, fuse, use_graph."""
+        self._plan = default_plan_opts(**kw)
+        self._prog = None
+
+    def _key(self):
+        # the gate objects themselves (identity compare, keeps ids alive)
+        return (tuple(self.gates),
+                tuple(g.angle for g in self.gates if isinstance(g, PauliRotationGate)),
+                bytes(self._plan))
+
+    def compile(self):
+        key = self._key()
+        if self._prog is None or self._prog_key != key:
+            self._prog = _Program(self.num_qubits, self.gates, self._plan)
+            self._prog_key = key
+        return self._prog
+
+    def program_stats(self) -> dict:
+        return dict(self.compile().stats)
+
+    def update_state(self, state, rng=None) -> None:
+        if state.get_qubit_count() != self.num_qubits:
+            raise ValueError("state and circuit qubit counts differ")
+        if not self.gates:
+            return
+        self.compile().run(state)
+
+
+class ParametricCircuit(Circuit):
+    """Circuit with a mutable angle table tracked by gate identity
+    (circuit.py:75-125)."""
+
+    def __init__(self, num_qubits: int):
+        super().__init__(num_qubits)
+        self._params: list[QuantumGate] = []
+
+    def add_parametric_gate(self, gate, position=None) -> None:
+        if not gate.is_parametric:
+            raise ValueError("gate is not parametric")
+        super().add_gate(gate, position)
+        self._params.append(gate)
+
+    def remove_gate(self, position: int) -> None:
+        if 0 <= position < len(self.gates):
+            victim = self.gates[position]
+            self._params = [g for g in self._params if g is not victim]
+        super().remove_gate(position)
+
+    def get_parameter_count(self) -> int:
+        return len(self._params)
+
+    def _param(self, index: int):
+        if not 0 <= index < len(self._params):
+            raise ValueError(f"parameter index {index} out of range")
+        return self._params[index]
+
+    def get_parameter(self, index: int) -> float:
+        return self._param(index).angle
+
+    def set_parameter(self, index: int, angle: float) -> None:
+        self._param(index).angle = float(angle)
+
+    def get_parametric_gate_position(self, index: int) -> int:
+        g = self._param(index)
+        for pos, other in enumerate(self.gates):
+            if other is g:
+                return pos
+        raise RuntimeError("parametric gate missing from the gate list")
+
+    def copy(self):
+        out = ParametricCircuit(self.num_qubits)
+        out.gates = [g.copy() for g in self.gates]
+        twin = {id(a): b for a, b in zip(self.gates, out.gates)}
+        out._params = [twin[id(g)] for g in self._params]
+        out._plan = self._plan
+        return out
+
+
+# ------------------------------------------------------------------ handles
+class QuantumCircuit:
+    """Qulacs-named handle (bindings __init__.py:91-128)."""
+
+    __slots__ = ("_core",)
+    _core_cls = Circuit
+
+    def __init__(self, qubit_count: int):
+        self._core = self._core_cls(qubit_count)
+
+    def get_qubit_count(self) -> int:
+        return self._core.num_qubits
+
+    def add_gate(self, gate, position=None) -> None:
+        self._core.add_gate(unwrap(gate), position)
+
+    def remove_gate(self, position: int) -> None:
+        self._core.remove_gate(position)
+
+    def get_gate(self, position: int) -> QuantumGateBase:
+        return QuantumGateBase(self._core.get_gate(position))
+
+    def get_gate_count(self) -> int:
+        return self._core.get_gate_count()
+
+    def calculate_depth(self) -> int:
+        return self._core.calculate_depth()
+
+    def update_quantum_state(self, state, seed=None) -> None:
+        self._core.update_state(state, rng=seed)
+
+    def add_observable_rotation_gate(self, observable, angle, num_slices) -> None:
+        from ._observable import add_observable_rotation
+        add_observable_rotation(self._core, unwrap(observable), angle, num_slices)
+
+    def set_plan_options(self, **kw) -> None:
+        self._core.set_plan_options(**kw)
+
+    def program_stats(self) -> dict:
+        return self._core.program_stats()
+
+    def copy(self):
+        out = type(self).__new__(type(self))
+        out._core = self._core.copy()
+        return out
+
+
+class ParametricQuantumCircuit(QuantumCircuit):
+    """Bindings __init__.py:131-149."""
+
+    _core_cls = ParametricCircuit
+
+    def add_parametric_gate(self, gate, position=None) -> None:
+        self._core.add_parametric_gate(unwrap(gate), position)
+
+    def get_parameter_count(self) -> int:
+        return self._core.get_parameter_count()
+
+    def get_parameter(self, index: int) -> float:
+        return self._core.get_parameter(index)
+
+    def set_parameter(self, index: int, angle: float) -> None:
+        self._core.set_parameter(index, angle)
+
+    def get_parametric_gate_position(self, index: int) -> int:
+        return self._core.get_parametric_gate_position(index)
+
+
+def circuit_records(circuit) -> list:
+    """Neutral records of every gate (fed to the test oracle)."""
+    return [g.record() for g in unwrap(circuit).gates]
+

@@ -1,0 +1,145 @@
+"""ctypes binding of libqsv.so (the C ABI declared in include/qsv.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+sm_100a).  There is no fallback: if the shared object is missing the import
+fails, and every call that needs a GPU raises when none is present.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqsv.so")
+
+QSV_OK = 0
+QSV_EINVAL = -1
+QSV_ENOMEM = -2
+QSV_ECUDA = -3
+QSV_EUNSUPPORTED = -4
+
+MAX_TARGETS = 12
+MAX_CONTROLS = 16
+
+OP_DENSE = 1
+OP_DIAG = 2
+OP_PAULI = 3
+OP_PAULI_ROT = 4
+
+
+class QsvOp(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("m", C.c_int32),
+        ("targets", C.c_int32 * MAX_TARGETS),
+        ("ids", C.c_int32 * MAX_TARGETS),
+        ("nc", C.c_int32),
+        ("control_qubits", C.c_int32 * MAX_CONTROLS),
+        ("control_values", C.c_int32 * MAX_CONTROLS),
+        ("angle", C.c_double),
+        ("data", C.c_void_p),
+    ]
+
+
+class QsvPlanOpts(C.Structure):
+    _fields_ = [
+        ("use_tiles", C.c_int32),
+        ("tile_qubits", C.c_int32),
+        ("fuse", C.c_int32),
+        ("use_graph", C.c_int32),
+    ]
+
+
+class QsvProgramStats(C.Structure):
+    _fields_ = [
+        ("num_ops_in", C.c_int32),
+        ("num_steps", C.c_int32),
+        ("num_tile_passes", C.c_int32),
+        ("num_gate_kernels", C.c_int32),
+        ("hbm_bytes", C.c_double),
+    ]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA engine first "
+        "(python -c 'import __graft_entry__ as g; g.build()')")
+
+lib = C.CDLL(LIB_PATH)
+
+_P = C.c_void_p
+_I = C.c_int
+_IP = C.POINTER(C.c_int)
+_DP = C.c_void_p
+_U64 = C.c_uint64
+
+_SIGS = {
+    "qsv_last_error": ([], C.c_char_p),
+    "qsv_version": ([], _I),
+    "qsv_device_count": ([_IP], _I),
+    "qsv_state_create": ([_I, _I, C.POINTER(_P)], _I),
+    "qsv_state_destroy": ([_P], _I),
+    "qsv_state_num_qubits": ([_P, _IP], _I),
+    "qsv_state_device_ptr": ([_P, C.POINTER(_P)], _I),
+    "qsv_set_stream": ([_P, _P], _I),
+    "qsv_get_stream": ([_P, C.POINTER(_P)], _I),
+    "qsv_sync": ([_P], _I),
+    "qsv_set_zero": ([_P], _I),
+    "qsv_set_basis": ([_P, _U64], _I),
+    "qsv_load": ([_P, _DP, _U64], _I),
+    "qsv_get": ([_P, _DP, _U64], _I),
+    "qsv_load_range": ([_P, _DP, _U64, _U64], _I),
+    "qsv_get_range": ([_P, _DP, _U64, _U64], _I),
+    "qsv_copy": ([_P, _P], _I),
+    "qsv_set_random_device": ([_P, _U64], _I),
+    "qsv_apply_dense": ([_P, _IP, _I, _DP, _IP, _IP, _I], _I),
+    "qsv_apply_diag": ([_P, _IP, _I, _DP, _IP, _IP, _I], _I),
+    "qsv_apply_pauli": ([_P, _IP, _IP, _I, _IP, _IP, _I], _I),
+    "qsv_apply_pauli_rot": ([_P, _IP, _IP, _I, C.c_double, _IP, _IP, _I], _I),
+    "qsv_norm2": ([_P, C.POINTER(C.c_double)], _I),
+    "qsv_scale": ([_P, C.c_double, C.c_double], _I),
+    "qsv_add": ([_P, _P], _I),
+    "qsv_inner": ([_P, _P, C.POINTER(C.c_double)], _I),
+    "qsv_expect": ([_P, _P, _I, _IP, _IP, _IP, _DP, C.POINTER(C.c_double)], _I),
+    "qsv_program_create": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts), C.POINTER(_P)], _I),
+    "qsv_program_run": ([_P, _P], _I),
+    "qsv_program_stats_get": ([_P, C.POINTER(QsvProgramStats)], _I),
+    "qsv_program_destroy": ([_P], _I),
+}
+
+EXPORTED = tuple(_SIGS)
+
+for _name, (_args, _res) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+
+
+def check(rc: int) -> None:
+    """Map a libqsv return code onto the reference's exception types
+    (ValueError for bad arguments, MemoryError for allocation failure)."""
+    if rc == QSV_OK:
+        return
+    msg = lib.qsv_last_error().decode(errors="replace")
+    if rc == QSV_EINVAL:
+        raise ValueError(msg)
+    if rc == QSV_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"libqsv error {rc}: {msg}")
+
+
+def int_array(values):
+    values = list(values)
+    arr = (C.c_int * max(1, len(values)))()
+    for i, v in enumerate(values):
+        arr[i] = int(v)
+    return arr
+
+
+def device_count() -> int:
+    out = C.c_int(0)
+    rc = lib.qsv_device_count(C.byref(out))
+    if rc != QSV_OK:
+        return 0
+    return out.value

@@ -1,0 +1,181 @@
+"""Device-resident state vector (``QuantumState`` / ``StateVector``).
+
+Mirrors the reference container (``qsimcore.StateVector``, state.py:22-133)
+and its Qulacs-named handle (``qsimbind.StateVector``, _handles.py:55-112),
+but the 2^n complex128 amplitudes live in HBM, owned by a libqsv handle that
+is released deterministically with the Python object.  Host copies happen
+only in ``load`` / ``get_vector`` / ``set_Haar_random_state``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import check, lib
+
+WILDCARD = 2
+
+
+def _check_count(n) -> int:
+    if isinstance(n, bool) or not isinstance(n, (int, np.integer)) or n < 1:
+        raise ValueError(f"qubit count must be a positive integer, got {n!r}")
+    return int(n)
+
+
+class StateVector:
+    """2^n amplitudes on a GPU plus the classical register list."""
+
+    __slots__ = ("_h", "_n", "_device", "_cregs", "__weakref__")
+
+    def __init__(self, qubit_count: int, device: int = 0):
+        n = _check_count(qubit_count)
+        self._h = None
+        self._n = n
+        self._device = int(device)
+        self._cregs: list[int] = []
+        h = C.c_void_p()
+        check(lib.qsv_state_create(n, self._device, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.qsv_state_destroy(h)
+            self._h = None
+
+    def _handle(self):
+        return self._h
+
+    # -- shape -------------------------------------------------------------
+    def get_qubit_count(self) -> int:
+        return self._n
+
+    @property
+    def num_qubits(self) -> int:
+        return self._n
+
+    @property
+    def dim(self) -> int:
+        return 1 << self._n
+
+    def get_device(self) -> int:
+        return self._device
+
+    # -- initialisation (state.py:32-54) ------------------------------------
+    def set_zero_state(self) -> None:
+        check(lib.qsv_set_zero(self._h))
+
+    def set_computational_basis(self, index: int) -> None:
+        index = int(index)
+        if not 0 <= index < self.dim:
+            raise ValueError(f"basis index {index} out of range for {self._n} qubits")
+        check(lib.qsv_set_basis(self._h, index))
+
+    def set_Haar_random_state(self, seed=None) -> None:
+        """Complex Gaussian (real block, then imaginary block, PCG64) divided
+        by its norm -- drawn on the host with numpy so that a seed gives the
+        bit-identical state of the reference (state.py:46-54)."""
+        gen = np.random.default_rng(seed)
+        raw = gen.standard_normal(self.dim) + 1j * gen.standard_normal(self.dim)
+        raw /= np.linalg.norm(raw)
+        self._upload(raw)
+
+    set_haar_random = set_Haar_random_state
+
+    def set_random_state_device(self, seed: int = 0) -> None:
+        """Benchmark-only initialiser: Gaussian amplitudes generated on the
+        GPU from a counter hash, normalised.  NOT bit-compatible with
+        ``set_Haar_random_state``; used where only the timing matters."""
+        check(lib.qsv_set_random_device(self._h, int(seed) & ((1 << 64) - 1)))
+
+    # -- transfer (state.py:56-73) -----------------------------------------
+    def _upload(self, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr, dtype=np.complex128)
+        check(lib.qsv_load(self._h, arr.ctypes.data, arr.size))
+
+    def load(self, state) -> None:
+        if isinstance(state, StateVector):
+            if state._n != self._n:
+                raise ValueError(f"expected {self.dim} amplitudes, got {state.dim}")
+            check(lib.qsv_copy(state._h, self._h))
+            self._cregs = list(state._cregs)
+            return
+        data = np.asarray(state, dtype=np.complex128)
+        if data.shape != (self.dim,):
+            raise ValueError(f"expected {self.dim} amplitudes, got shape {data.shape}")
+        self._upload(data)
+
+    def get_vector(self, out: np.ndarray | None = None) -> np.ndarray:
+        """A host copy (mutating it never touches the device state).  ``out``
+        may supply a contiguous complex128 buffer, e.g. pinned memory."""
+        if out is None:
+            out = np.empty(self.dim, dtype=np.complex128)
+        elif out.dtype != np.complex128 or out.shape != (self.dim,) or \
+                not out.flags.c_contiguous:
+            raise ValueError(f"out must be a contiguous complex128 array of {self.dim}")
+        check(lib.qsv_get(self._h, out.ctypes.data, out.size))
+        return out
+
+    def copy(self) -> "StateVector":
+        out = StateVector(self._n, self._device)
+        check(lib.qsv_copy(self._h, out._h))
+        out._cregs = list(self._cregs)
+        return out
+
+    # -- algebra (state.py:75-81, 108-114) --------------------------------
+    def get_squared_norm(self) -> float:
+        out = C.c_double()
+        check(lib.qsv_norm2(self._h, C.byref(out)))
+        return float(out.value)
+
+    def normalize(self, squared_norm: float) -> None:
+        if squared_norm <= 0:
+            raise ValueError("squared norm must be positive")
+        check(lib.qsv_scale(self._h, 1.0 / float(np.sqrt(squared_norm)), 0.0))
+
+    def multiply_coef(self, coef) -> None:
+        c = complex(coef)
+        check(lib.qsv_scale(self._h, c.real, c.imag))
+
+    def add_state(self, other: "StateVector") -> None:
+        if other._n != self._n:
+            raise ValueError("qubit counts differ")
+        check(lib.qsv_add(self._h, other._h))
+
+    # -- classical registers (state.py:116-127) ----------------------------
+    def get_classical_value(self, index: int) -> int:
+        if index < 0:
+            raise ValueError("register address must be non-negative")
+        return self._cregs[index] if index < len(self._cregs) else 0
+
+    def set_classical_value(self, index: int, value: int) -> None:
+        if index < 0:
+            raise ValueError("register address must be non-negative")
+        if index >= len(self._cregs):
+            self._cregs.extend([0] * (index + 1 - len(self._cregs)))
+        self._cregs[index] = int(value)
+
+    def synchronize(self) -> None:
+        check(lib.qsv_sync(self._h))
+
+    def set_stream(self, cuda_stream_ptr: int) -> None:
+        """Enqueue this state's work on an external CUDA stream (e.g.
+        ``torch.cuda.current_stream().cuda_stream``)."""
+        check(lib.qsv_set_stream(self._h, C.c_void_p(int(cuda_stream_ptr))))
+
+    def __repr__(self) -> str:
+        return f"QuantumState(qubits={self._n}, device={self._device})"
+
+
+QuantumState = StateVector
+
+
+def inner_product(bra: StateVector, ket: StateVector) -> complex:
+    """<bra|ket> (state.py:136-139)."""
+    if bra.get_qubit_count() != ket.get_qubit_count():
+        raise ValueError("qubit counts differ")
+    out = (C.c_double * 2)()
+    check(lib.qsv_inner(bra._h, ket._h, out))
+    return complex(out[0], out[1])

@@ -1,0 +1,558 @@
+// extern "C" entry points of libqsv (declared in include/qsv.h).
+#include <cstdarg>
+#include <cstring>
+#include <cmath>
+#include <string>
+#include <vector>
+#include <map>
+#include <algorithm>
+
+#include "qsv_internal.cuh"
+#include "qsv_program.cuh"
+
+namespace qsv {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  cudaGetLastError();  // clear sticky-free errors
+  return e == cudaErrorMemoryAllocation ? QSV_ENOMEM : QSV_ECUDA;
+}
+
+int launch_expect_sweep(const double2* bra, const double2* ket, int n, uint64_t xm,
+                        const uint64_t* zm, int nt, double* partials, double* dev_out,
+                        cudaStream_t s);
+
+__global__ void k_set1(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
+
+// Device scratch owned by a state: payloads of direct gate calls and
+// reduction results.  Grown on demand, reused in stream order.
+struct Scratch {
+  void* ptr = nullptr;
+  size_t cap = 0;
+};
+static std::map<const qsv_state*, Scratch> g_payload;
+static std::map<const qsv_state*, Scratch> g_results;
+
+static int ensure(Scratch& s, size_t bytes, cudaStream_t stream) {
+  if (s.cap >= bytes) return QSV_OK;
+  if (s.ptr) {
+    QSV_TRY(cudaStreamSynchronize(stream));
+    QSV_TRY(cudaFree(s.ptr));
+    s.ptr = nullptr;
+    s.cap = 0;
+  }
+  size_t cap = std::max<size_t>(bytes, 4096);
+  QSV_TRY(cudaMalloc(&s.ptr, cap));
+  s.cap = cap;
+  return QSV_OK;
+}
+
+std::vector<char> make_payload(const GateDesc& g) {
+  std::vector<char> out;
+  if (g.kind == QSV_OP_DENSE && g.m >= 5) {
+    const size_t D = (size_t)1 << g.m;
+    out.resize(D * D * sizeof(double2) + D * sizeof(uint64_t));
+    memcpy(out.data(), g.data.data(), D * D * sizeof(double2));
+    uint64_t* offs = reinterpret_cast<uint64_t*>(out.data() + D * D * sizeof(double2));
+    for (size_t z = 0; z < D; ++z) {
+      uint64_t o = 0;
+      for (int j = 0; j < g.m; ++j)
+        if ((z >> j) & 1) o |= 1ULL << g.targets[j];
+      offs[z] = o;
+    }
+  } else if (g.kind == QSV_OP_DIAG && g.m > 5) {
+    out.resize(((size_t)1 << g.m) * sizeof(double2));
+    memcpy(out.data(), g.data.data(), out.size());
+  }
+  return out;
+}
+
+static int apply_desc(qsv_state* st, const GateDesc& g0) {
+  int rc = validate_gate(st->n, g0);
+  if (rc) return rc;
+  DeviceGuard dg(st->device);
+  GateDesc g = canonicalize(g0);
+  std::vector<char> payload = make_payload(g);
+  const Cplx* dev = nullptr;
+  if (!payload.empty()) {
+    Scratch& s = g_payload[st];
+    rc = ensure(s, payload.size(), st->stream);
+    if (rc) return rc;
+    QSV_TRY(cudaMemcpyAsync(s.ptr, payload.data(), payload.size(), cudaMemcpyHostToDevice,
+                            st->stream));
+    dev = reinterpret_cast<const Cplx*>(s.ptr);
+    // pageable source: the copy is staged before return, so the host vector
+    // may be freed; the kernel below is ordered after the copy.
+  }
+  return launch_gate(st->amps, st->n, g, dev, st->stream);
+}
+
+static GateDesc make_desc(int kind, const int* targets, const int* ids, int m, const int* cq,
+                          const int* cv, int nc) {
+  GateDesc g;
+  memset(g.targets, 0, sizeof(g.targets));
+  memset(g.ids, 0, sizeof(g.ids));
+  memset(g.cq, 0, sizeof(g.cq));
+  memset(g.cv, 0, sizeof(g.cv));
+  g.kind = kind;
+  g.m = m;
+  g.nc = nc;
+  g.angle = 0;
+  if (m > 0 && m <= QSV_MAX_TARGETS)
+    for (int j = 0; j < m; ++j) {
+      g.targets[j] = targets[j];
+      g.ids[j] = ids ? ids[j] : 0;
+    }
+  if (nc > 0 && nc <= QSV_MAX_CONTROLS)
+    for (int j = 0; j < nc; ++j) {
+      g.cq[j] = cq[j];
+      g.cv[j] = cv[j];
+    }
+  return g;
+}
+
+static bool bad_state(const qsv_state* st) {
+  if (!st) {
+    set_error("null state handle");
+    return true;
+  }
+  return false;
+}
+
+}  // namespace qsv
+
+using namespace qsv;
+
+extern "C" {
+
+const char* qsv_last_error(void) { return g_err.c_str(); }
+
+int qsv_version(void) { return 1; }
+
+int qsv_device_count(int* out) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *out = c;
+  return QSV_OK;
+}
+
+int qsv_state_create(int num_qubits, int device, qsv_state** out) {
+  if (!out) {
+    set_error("null output pointer");
+    return QSV_EINVAL;
+  }
+  *out = nullptr;
+  if (num_qubits < 1 || num_qubits > 40) {
+    set_error("qubit count must be in [1, 40], got %d", num_qubits);
+    return QSV_EINVAL;
+  }
+  int ndev = 0;
+  QSV_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    set_error("device %d out of range (%d devices)", device, ndev);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(device);
+  qsv_state* st = new qsv_state();
+  st->n = num_qubits;
+  st->device = device;
+  st->dim = 1ULL << num_qubits;
+  st->stream = 0;
+  st->amps = nullptr;
+  st->partials = nullptr;
+  st->host_res = nullptr;
+  const size_t bytes = st->dim * sizeof(double2);
+  cudaError_t e = cudaMalloc(&st->amps, std::max<size_t>(bytes, 32));
+  if (e != cudaSuccess) {
+    delete st;
+    set_error("cannot allocate %zu bytes for a %d-qubit state: %s", bytes, num_qubits,
+              cudaGetErrorString(e));
+    cudaGetLastError();
+    return QSV_ENOMEM;
+  }
+  e = cudaMalloc(&st->partials, sizeof(double) * 2 * kRedBlocks * kMaxTerms);
+  if (e != cudaSuccess) {
+    cudaFree(st->amps);
+    delete st;
+    return cuda_fail(e, "cudaMalloc(partials)");
+  }
+  *out = st;
+  return qsv_set_zero(st);
+}
+
+int qsv_state_destroy(qsv_state* st) {
+  if (!st) return QSV_OK;
+  DeviceGuard dg(st->device);
+  cudaStreamSynchronize(st->stream);
+  cudaFree(st->amps);
+  cudaFree(st->partials);
+  for (auto* mp : {&g_payload, &g_results}) {
+    auto it = mp->find(st);
+    if (it != mp->end()) {
+      cudaFree(it->second.ptr);
+      mp->erase(it);
+    }
+  }
+  delete st;
+  return QSV_OK;
+}
+
+int qsv_state_num_qubits(const qsv_state* st, int* out) {
+  if (bad_state(st)) return QSV_EINVAL;
+  *out = st->n;
+  return QSV_OK;
+}
+
+int qsv_state_device_ptr(const qsv_state* st, void** out) {
+  if (bad_state(st)) return QSV_EINVAL;
+  *out = st->amps;
+  return QSV_OK;
+}
+
+int qsv_set_stream(qsv_state* st, void* stream) {
+  if (bad_state(st)) return QSV_EINVAL;
+  st->stream = reinterpret_cast<cudaStream_t>(stream);
+  return QSV_OK;
+}
+
+int qsv_get_stream(const qsv_state* st, void** stream) {
+  if (bad_state(st)) return QSV_EINVAL;
+  *stream = reinterpret_cast<void*>(st->stream);
+  return QSV_OK;
+}
+
+int qsv_sync(qsv_state* st) {
+  if (bad_state(st)) return QSV_EINVAL;
+  DeviceGuard dg(st->device);
+  QSV_TRY(cudaStreamSynchronize(st->stream));
+  return QSV_OK;
+}
+
+int qsv_set_zero(qsv_state* st) { return qsv_set_basis(st, 0); }
+
+int qsv_set_basis(qsv_state* st, uint64_t index) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (index >= st->dim) {
+    set_error("basis index %llu out of range for %d qubits", (unsigned long long)index, st->n);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(st->device);
+  QSV_TRY(cudaMemsetAsync(st->amps, 0, st->dim * sizeof(double2), st->stream));
+  k_set1<<<1, 1, 0, st->stream>>>(st->amps, index);
+  QSV_CHECK_LAUNCH("k_set1");
+  return QSV_OK;
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+int qsv_load_range(qsv_state* st, const double* src, uint64_t offset, uint64_t count) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (offset > st->dim || count > st->dim - offset) {
+    set_error("range [%llu, +%llu) outside a state of %llu amplitudes",
+              (unsigned long long)offset, (unsigned long long)count, (unsigned long long)st->dim);
+    return QSV_EINVAL;
+  }
+  if (count == 0) return QSV_OK;
+  DeviceGuard dg(st->device);
+  QSV_TRY(cudaMemcpyAsync(st->amps + offset, src, count * sizeof(double2), cudaMemcpyHostToDevice,
+                          st->stream));
+  if (!is_pinned(src)) QSV_TRY(cudaStreamSynchronize(st->stream));
+  return QSV_OK;
+}
+
+int qsv_load(qsv_state* st, const double* src, uint64_t n_amps) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (n_amps != st->dim) {
+    set_error("expected %llu amplitudes, got %llu", (unsigned long long)st->dim,
+              (unsigned long long)n_amps);
+    return QSV_EINVAL;
+  }
+  return qsv_load_range(st, src, 0, n_amps);
+}
+
+int qsv_get_range(const qsv_state* st, double* dst, uint64_t offset, uint64_t count) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (offset > st->dim || count > st->dim - offset) {
+    set_error("range [%llu, +%llu) outside a state of %llu amplitudes",
+              (unsigned long long)offset, (unsigned long long)count, (unsigned long long)st->dim);
+    return QSV_EINVAL;
+  }
+  if (count == 0) return QSV_OK;
+  DeviceGuard dg(st->device);
+  QSV_TRY(cudaMemcpyAsync(dst, st->amps + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                          st->stream));
+  QSV_TRY(cudaStreamSynchronize(st->stream));
+  return QSV_OK;
+}
+
+int qsv_get(const qsv_state* st, double* dst, uint64_t n_amps) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (n_amps != st->dim) {
+    set_error("expected a buffer of %llu amplitudes, got %llu", (unsigned long long)st->dim,
+              (unsigned long long)n_amps);
+    return QSV_EINVAL;
+  }
+  return qsv_get_range(st, dst, 0, n_amps);
+}
+
+int qsv_copy(const qsv_state* src, qsv_state* dst) {
+  if (bad_state(src) || bad_state(dst)) return QSV_EINVAL;
+  if (src->n != dst->n) {
+    set_error("qubit counts differ (%d vs %d)", src->n, dst->n);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(dst->device);
+  if (src->stream != dst->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
+  if (src->device == dst->device) {
+    QSV_TRY(cudaMemcpyAsync(dst->amps, src->amps, src->dim * sizeof(double2),
+                            cudaMemcpyDeviceToDevice, dst->stream));
+  } else {
+    QSV_TRY(cudaMemcpyPeerAsync(dst->amps, dst->device, src->amps, src->device,
+                                src->dim * sizeof(double2), dst->stream));
+  }
+  return QSV_OK;
+}
+
+int qsv_set_random_device(qsv_state* st, uint64_t seed) {
+  if (bad_state(st)) return QSV_EINVAL;
+  DeviceGuard dg(st->device);
+  int rc = launch_random(st->amps, st->dim, seed, st->stream);
+  if (rc) return rc;
+  double s = 0;
+  rc = qsv_norm2(st, &s);
+  if (rc) return rc;
+  return qsv_scale(st, 1.0 / std::sqrt(s), 0.0);
+}
+
+// ------------------------------------------------------------------ gates
+int qsv_apply_dense(qsv_state* st, const int* targets, int m, const double* matrix, const int* cq,
+                    const int* cv, int nc) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (m < 0 || m > QSV_MAX_TARGETS || nc < 0 || nc > QSV_MAX_CONTROLS) {
+    set_error("unsupported target/control count (%d, %d)", m, nc);
+    return QSV_EINVAL;
+  }
+  GateDesc g = make_desc(QSV_OP_DENSE, targets, nullptr, m, cq, cv, nc);
+  const size_t D = (size_t)1 << m;
+  g.data.resize(D * D);
+  memcpy(g.data.data(), matrix, D * D * sizeof(Cplx));
+  return apply_desc(st, g);
+}
+
+int qsv_apply_diag(qsv_state* st, const int* targets, int m, const double* diag, const int* cq,
+                   const int* cv, int nc) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (m < 0 || m > QSV_MAX_TARGETS || nc < 0 || nc > QSV_MAX_CONTROLS) {
+    set_error("unsupported target/control count (%d, %d)", m, nc);
+    return QSV_EINVAL;
+  }
+  GateDesc g = make_desc(QSV_OP_DIAG, targets, nullptr, m, cq, cv, nc);
+  g.data.resize((size_t)1 << m);
+  memcpy(g.data.data(), diag, g.data.size() * sizeof(Cplx));
+  return apply_desc(st, g);
+}
+
+int qsv_apply_pauli(qsv_state* st, const int* targets, const int* ids, int m, const int* cq,
+                    const int* cv, int nc) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (m < 0 || m > QSV_MAX_TARGETS || nc < 0 || nc > QSV_MAX_CONTROLS) {
+    set_error("unsupported target/control count (%d, %d)", m, nc);
+    return QSV_EINVAL;
+  }
+  GateDesc g = make_desc(QSV_OP_PAULI, targets, ids, m, cq, cv, nc);
+  return apply_desc(st, g);
+}
+
+int qsv_apply_pauli_rot(qsv_state* st, const int* targets, const int* ids, int m, double angle,
+                        const int* cq, const int* cv, int nc) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (m < 0 || m > QSV_MAX_TARGETS || nc < 0 || nc > QSV_MAX_CONTROLS) {
+    set_error("unsupported target/control count (%d, %d)", m, nc);
+    return QSV_EINVAL;
+  }
+  GateDesc g = make_desc(QSV_OP_PAULI_ROT, targets, ids, m, cq, cv, nc);
+  g.angle = angle;
+  return apply_desc(st, g);
+}
+
+// ---------------------------------------------------------- reductions
+struct Sweep {
+  uint64_t xm;
+  std::vector<uint64_t> zm;
+  std::vector<int> term;  // term index per slot
+};
+
+static int run_sweeps(const qsv_state* bra, const qsv_state* ket,
+                      const std::vector<Sweep>& sweeps, std::vector<double>& res) {
+  DeviceGuard dg(ket->device);
+  cudaStream_t s = ket->stream;
+  if (bra->stream != ket->stream) QSV_TRY(cudaStreamSynchronize(bra->stream));
+  const size_t need = sizeof(double) * 2 * kMaxTerms * std::max<size_t>(1, sweeps.size());
+  Scratch& sc = g_results[ket];
+  int rc = ensure(sc, need, s);
+  if (rc) return rc;
+  double* dout = reinterpret_cast<double*>(sc.ptr);
+  for (size_t i = 0; i < sweeps.size(); ++i) {
+    rc = launch_expect_sweep(bra->amps, ket->amps, ket->n, sweeps[i].xm, sweeps[i].zm.data(),
+                             (int)sweeps[i].zm.size(), ket->partials,
+                             dout + 2 * kMaxTerms * i, s);
+    if (rc) return rc;
+  }
+  res.assign(2 * kMaxTerms * sweeps.size(), 0.0);
+  if (!sweeps.empty()) {
+    QSV_TRY(cudaMemcpyAsync(res.data(), dout, res.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            s));
+  }
+  QSV_TRY(cudaStreamSynchronize(s));
+  return QSV_OK;
+}
+
+int qsv_norm2(const qsv_state* st, double* out) {
+  if (bad_state(st)) return QSV_EINVAL;
+  std::vector<Sweep> sw(1);
+  sw[0].xm = 0;
+  sw[0].zm = {0};
+  sw[0].term = {0};
+  std::vector<double> res;
+  int rc = run_sweeps(st, st, sw, res);
+  if (rc) return rc;
+  *out = res[0];
+  return QSV_OK;
+}
+
+int qsv_inner(const qsv_state* bra, const qsv_state* ket, double out[2]) {
+  if (bad_state(bra) || bad_state(ket)) return QSV_EINVAL;
+  if (bra->n != ket->n) {
+    set_error("qubit counts differ (%d vs %d)", bra->n, ket->n);
+    return QSV_EINVAL;
+  }
+  if (bra->device != ket->device) {
+    set_error("states live on different devices");
+    return QSV_EINVAL;
+  }
+  std::vector<Sweep> sw(1);
+  sw[0].xm = 0;
+  sw[0].zm = {0};
+  sw[0].term = {0};
+  std::vector<double> res;
+  int rc = run_sweeps(bra, ket, sw, res);
+  if (rc) return rc;
+  out[0] = res[0];
+  out[1] = res[1];
+  return QSV_OK;
+}
+
+int qsv_expect(const qsv_state* bra, const qsv_state* ket, int nterms, const int* term_len,
+               const int* qubits, const int* ids, const double* coefs, double out[2]) {
+  if (bad_state(bra) || bad_state(ket)) return QSV_EINVAL;
+  if (bra->n != ket->n || bra->device != ket->device) {
+    set_error("bra and ket differ in width or device");
+    return QSV_EINVAL;
+  }
+  // group terms by flip mask (one sweep per <= kMaxTerms terms of a group)
+  std::map<uint64_t, std::vector<int>> groups;
+  std::vector<uint64_t> zms(nterms);
+  std::vector<int> nys(nterms);
+  size_t pos = 0;
+  for (int t = 0; t < nterms; ++t) {
+    uint64_t xm = 0, zm = 0, used = 0;
+    int ny = 0;
+    for (int f = 0; f < term_len[t]; ++f, ++pos) {
+      const int q = qubits[pos], id = ids[pos];
+      if (q < 0 || q >= ket->n) {
+        set_error("term touches qubit %d but the operator has %d qubits", q, ket->n);
+        return QSV_EINVAL;
+      }
+      if (used & (1ULL << q)) {
+        set_error("qubit indices in a Pauli product must be distinct");
+        return QSV_EINVAL;
+      }
+      used |= 1ULL << q;
+      if (id < 0 || id > 3) {
+        set_error("Pauli ids must be in {0, 1, 2, 3}");
+        return QSV_EINVAL;
+      }
+      if (id == 1 || id == 2) xm |= 1ULL << q;
+      if (id == 2 || id == 3) zm |= 1ULL << q;
+      if (id == 2) ++ny;
+    }
+    zms[t] = zm;
+    nys[t] = ny;
+    groups[xm].push_back(t);
+  }
+  std::vector<Sweep> sweeps;
+  for (auto& kv : groups) {
+    for (size_t i = 0; i < kv.second.size(); i += kMaxTerms) {
+      Sweep s;
+      s.xm = kv.first;
+      for (size_t j = i; j < std::min(kv.second.size(), i + kMaxTerms); ++j) {
+        s.term.push_back(kv.second[j]);
+        s.zm.push_back(zms[kv.second[j]]);
+      }
+      sweeps.push_back(s);
+    }
+  }
+  std::vector<double> res;
+  int rc = run_sweeps(bra, ket, sweeps, res);
+  if (rc) return rc;
+  // sum_t coef_t * i^ny_t * S_t, accumulated in term order
+  std::vector<Cplx> per_term(nterms, Cplx{0, 0});
+  for (size_t i = 0; i < sweeps.size(); ++i)
+    for (size_t j = 0; j < sweeps[i].term.size(); ++j)
+      per_term[sweeps[i].term[j]] = {res[2 * kMaxTerms * i + 2 * j],
+                                     res[2 * kMaxTerms * i + 2 * j + 1]};
+  static const Cplx ip[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+  double re = 0, im = 0;
+  for (int t = 0; t < nterms; ++t) {
+    const Cplx p = ip[nys[t] & 3];
+    const Cplx S = per_term[t];
+    const Cplx v{p.re * S.re - p.im * S.im, p.re * S.im + p.im * S.re};
+    const double cr = coefs[2 * t], ci = coefs[2 * t + 1];
+    re += cr * v.re - ci * v.im;
+    im += cr * v.im + ci * v.re;
+  }
+  out[0] = re;
+  out[1] = im;
+  return QSV_OK;
+}
+
+int qsv_scale(qsv_state* st, double re, double im) {
+  if (bad_state(st)) return QSV_EINVAL;
+  DeviceGuard dg(st->device);
+  return launch_scale(st->amps, st->dim, make_double2(re, im), st->stream);
+}
+
+int qsv_add(qsv_state* dst, const qsv_state* src) {
+  if (bad_state(dst) || bad_state(src)) return QSV_EINVAL;
+  if (dst->n != src->n || dst->device != src->device) {
+    set_error("qubit counts differ");
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(dst->device);
+  if (src->stream != dst->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
+  return launch_add(dst->amps, src->amps, dst->dim, dst->stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,224 @@
+// qsv_program: the compiled replacement of Circuit.update_state's per-gate
+// loop (reference circuit.py:48-55).  Creation canonicalises every gate,
+// copies all payloads to the device once and plans the steps; run replays the
+// steps on the state's stream (optionally through a CUDA graph, which removes
+// the per-launch CPU cost for small states).
+#include <cstring>
+#include <string>
+#include <cmath>
+#include <vector>
+#include <algorithm>
+
+#include "qsv_internal.cuh"
+#include "qsv_program.cuh"
+#include "qsv_tile.cuh"
+
+using namespace qsv;
+
+struct qsv_program {
+  int n;
+  std::vector<Step> steps;
+  std::vector<TilePlan> tiles;
+  void* dev_payload = nullptr;
+  size_t payload_bytes = 0;
+  qsv_program_stats stats;
+  qsv_plan_opts opts;
+  // CUDA graph cache (valid for one amps pointer / stream / device)
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t graph = nullptr;
+  double2* graph_amps = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  int device = -1;
+};
+
+namespace {
+
+int launch_steps(qsv_program* p, double2* amps, cudaStream_t s) {
+  for (const Step& st : p->steps) {
+    int rc;
+    if (st.type == 0) {
+      const Cplx* dev =
+          st.has_payload ? reinterpret_cast<const Cplx*>((char*)p->dev_payload + st.payload_off)
+                         : nullptr;
+      rc = launch_gate(amps, p->n, st.gate, dev, s);
+    } else {
+      rc = launch_tile_pass(amps, p->n, p->tiles[st.tile], p->dev_payload, s);
+    }
+    if (rc) return rc;
+  }
+  return QSV_OK;
+}
+
+void drop_graph(qsv_program* p) {
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  p->gexec = nullptr;
+  p->graph = nullptr;
+  p->graph_amps = nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* opts,
+                       qsv_program** out) {
+  if (!out) {
+    set_error("null output pointer");
+    return QSV_EINVAL;
+  }
+  *out = nullptr;
+  if (n < 1 || n > 40 || nops < 0 || (nops > 0 && !ops)) {
+    set_error("bad program arguments");
+    return QSV_EINVAL;
+  }
+  qsv_plan_opts o{1, 0, 1, 1};
+  if (opts) o = *opts;
+  std::vector<GateDesc> gates;
+  gates.reserve(nops);
+  for (int i = 0; i < nops; ++i) {
+    const qsv_op& op = ops[i];
+    GateDesc g;
+    memset(g.targets, 0, sizeof(g.targets));
+    memset(g.ids, 0, sizeof(g.ids));
+    memset(g.cq, 0, sizeof(g.cq));
+    memset(g.cv, 0, sizeof(g.cv));
+    g.kind = op.kind;
+    g.m = op.m;
+    g.nc = op.nc;
+    g.angle = op.angle;
+    if (op.m < 0 || op.m > QSV_MAX_TARGETS || op.nc < 0 || op.nc > QSV_MAX_CONTROLS) {
+      set_error("op %d: unsupported target/control count", i);
+      return QSV_EINVAL;
+    }
+    for (int j = 0; j < op.m; ++j) {
+      g.targets[j] = op.targets[j];
+      g.ids[j] = op.ids[j];
+    }
+    for (int j = 0; j < op.nc; ++j) {
+      g.cq[j] = op.control_qubits[j];
+      g.cv[j] = op.control_values[j];
+    }
+    if (op.kind == QSV_OP_DENSE) {
+      const size_t D = (size_t)1 << op.m;
+      if (!op.data) {
+        set_error("op %d: dense gate without a matrix", i);
+        return QSV_EINVAL;
+      }
+      g.data.resize(D * D);
+      memcpy(g.data.data(), op.data, D * D * sizeof(Cplx));
+    } else if (op.kind == QSV_OP_DIAG) {
+      const size_t D = (size_t)1 << op.m;
+      if (!op.data) {
+        set_error("op %d: diagonal gate without entries", i);
+        return QSV_EINVAL;
+      }
+      g.data.resize(D);
+      memcpy(g.data.data(), op.data, D * sizeof(Cplx));
+    }
+    int rc = validate_gate(n, g);
+    if (rc) {
+      std::string msg = qsv_last_error();
+      set_error("op %d: %s", i, msg.c_str());
+      return rc;
+    }
+    g = canonicalize(g);
+    if (g.nc < 0) continue;  // identity
+    gates.push_back(g);
+  }
+
+  qsv_program* p = new qsv_program();
+  p->n = n;
+  p->opts = o;
+  memset(&p->stats, 0, sizeof(p->stats));
+  p->stats.num_ops_in = nops;
+
+  std::vector<char> host_payload;
+  int rc = plan_program(n, gates, o, p->steps, p->tiles, host_payload, &p->stats);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  p->payload_bytes = host_payload.size();
+  if (!host_payload.empty()) {
+    cudaError_t e = cudaMalloc(&p->dev_payload, host_payload.size());
+    if (e != cudaSuccess) {
+      delete p;
+      return cuda_fail(e, "cudaMalloc(program payload)");
+    }
+    e = cudaMemcpy(p->dev_payload, host_payload.data(), host_payload.size(),
+                   cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(p->dev_payload);
+      delete p;
+      return cuda_fail(e, "cudaMemcpy(program payload)");
+    }
+  }
+  cudaGetDevice(&p->device);
+  *out = p;
+  return QSV_OK;
+}
+
+int qsv_program_run(qsv_program* p, qsv_state* st) {
+  if (!p || !st) {
+    set_error("null handle");
+    return QSV_EINVAL;
+  }
+  if (p->n != st->n) {
+    set_error("state and circuit qubit counts differ (%d vs %d)", st->n, p->n);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(st->device);
+  if (!p->opts.use_graph || p->steps.empty()) return launch_steps(p, st->amps, st->stream);
+  if (!(p->gexec && p->graph_amps == st->amps && p->graph_stream == st->stream &&
+        p->device == st->device)) {
+    drop_graph(p);
+    // capture on a private stream (the legacy stream cannot be captured)
+    cudaStream_t cap;
+    QSV_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      cudaStreamDestroy(cap);
+      return cuda_fail(e, "cudaStreamBeginCapture");
+    }
+    int rc = launch_steps(p, st->amps, cap);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(cap, &g);
+    cudaStreamDestroy(cap);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&p->gexec, g, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g);
+      return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    p->graph = g;
+    p->graph_amps = st->amps;
+    p->graph_stream = st->stream;
+    p->device = st->device;
+  }
+  QSV_TRY(cudaGraphLaunch(p->gexec, st->stream));
+  return QSV_OK;
+}
+
+int qsv_program_stats_get(const qsv_program* p, qsv_program_stats* out) {
+  if (!p || !out) {
+    set_error("null handle");
+    return QSV_EINVAL;
+  }
+  *out = p->stats;
+  return QSV_OK;
+}
+
+int qsv_program_destroy(qsv_program* p) {
+  if (!p) return QSV_OK;
+  drop_graph(p);
+  if (p->dev_payload) cudaFree(p->dev_payload);
+  delete p;
+  return QSV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,382 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the reference's
+golden outputs and the CPU oracle.
+
+Bars (north star): <= 1e-12 max |amplitude error|, <= 1e-10 relative error
+on expectation values with an absolute floor of 1e-10 * sum|coef| (SURVEY.md
+8(c) "near-zero expectations").
+"""
+
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import paper_2011_13524_b200 as qs
+from paper_2011_13524_b200 import gate as qg
+from paper_2011_13524_b200 import workloads
+from paper_2011_13524_b200 import _optimizer
+from paper_2011_13524_b200._circuit import circuit_records
+from paper_2011_13524_b200.circuit import QuantumCircuitOptimizer
+from paper_2011_13524_b200.quantum_operator import create_quantum_operator_from_openfermion_text
+from paper_2011_13524_b200.state import inner_product
+
+from oracle import qsim_oracle as orc
+from golden_util import build_gate, load_circuits, load_gate_cases, load_haar, load_observables
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-12
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def haar(n, seed):
+    s = qs.QuantumState(n)
+    s.set_Haar_random_state(seed)
+    return s
+
+
+def close_expect(got, ref, scale):
+    return abs(got - ref) <= 1e-10 * max(abs(ref), scale)
+
+
+# ----------------------------------------------------------------- golden
+def test_haar_bit_exact():
+    for key, vec in load_haar().items():
+        n, seed = key[1:].split("_s")
+        got = haar(int(n), int(seed)).get_vector()
+        assert np.array_equal(got.view(np.uint64), vec.view(np.uint64)), key
+
+
+def test_golden_gate_cases():
+    cases, outs = load_gate_cases()
+    worst = 0.0
+    bad = []
+    for case in cases:
+        st = haar(case["n"], case["seed"])
+        build_gate(case, qg).update_quantum_state(st)
+        err = float(np.max(np.abs(st.get_vector() - outs[case["id"]])))
+        worst = max(worst, err)
+        if err > AMP_TOL:
+            bad.append((case["factory"], case["args"], case["controls"], err))
+    assert not bad, bad[:10]
+    print(f"golden gate cases: {len(cases)}, worst {worst:.2e}")
+
+
+@pytest.mark.parametrize("plan", [dict(), dict(use_graph=0), dict(use_tiles=0),
+                                  dict(use_tiles=1, tile_qubits=8)])
+def test_golden_circuits(plan):
+    meta, outs = load_circuits()
+    for e in meta["circuits"]:
+        n = e["n"]
+        if e["name"] == "cnot-ring":
+            circ = workloads.generate_cnot_ring(n, seed=e["seed"])
+        else:
+            circ = workloads.generate_cz_ladder(n, e["depth"], seed=e["seed"],
+                                                commuting=e["name"].endswith("commuting"))
+        if "opt" in e:
+            if e["opt"] == "light":
+                QuantumCircuitOptimizer().optimize_light(circ)
+            else:
+                QuantumCircuitOptimizer().optimize(circ, e["opt"])
+        assert circ.get_gate_count() == e["gate_count"], e
+        circ.set_plan_options(**plan)
+        st = qs.QuantumState(n)
+        if e["start_seed"] is not None:
+            st.set_Haar_random_state(e["start_seed"])
+        circ.update_quantum_state(st)
+        err = np.max(np.abs(st.get_vector() - outs[e["id"]]))
+        assert err <= AMP_TOL, (e, err)
+
+
+def test_golden_observables():
+    data = load_observables()
+    for case in data["random"]:
+        n = case["n"]
+        op = qs.GeneralQuantumOperator(n)
+        scale = 0.0
+        for t in case["terms"]:
+            coef = complex(*t["coef"])
+            scale += abs(coef)
+            s = " ".join(f"{'IXYZ'[a]} {q}" for q, a in t["ops"])
+            op.add_operator(qs.PauliOperator(s, coef))
+        ket = haar(n, case["seed"])
+        bra = haar(n, case["seed"] + 1)
+        assert close_expect(op.get_expectation_value(ket), complex(*case["value"]), scale)
+        assert close_expect(op.get_transition_amplitude(bra, ket), complex(*case["transition"]),
+                            scale)
+    for case in data["tfim"]:
+        n = case["n"]
+        v = workloads.tfim_observable(n).get_expectation_value(haar(n, case["seed"]))
+        assert isinstance(v, float)
+        assert close_expect(v, case["value"], 1.5 * n)
+    op = create_quantum_operator_from_openfermion_text(data["hamiltonian_text"])
+    assert abs(op.get_expectation_value(qs.QuantumState(4))) <= 1e-9
+    assert close_expect(op.get_expectation_value(haar(4, 5)),
+                        complex(*data["hamiltonian_haar5"]), 2.0)
+
+
+@pytest.mark.parametrize("n", [8, 12, 24])
+def test_golden_vqe(n):
+    ref = {e["n"]: e for e in load_observables()["vqe"]}
+    if n not in ref:
+        pytest.skip("fixture generated without --with-cfg3")
+    circ = workloads.vqe_ansatz(n)
+    assert circ.get_gate_count() == ref[n]["gates"]
+    st = qs.QuantumState(n)
+    circ.update_quantum_state(st)
+    v = workloads.tfim_observable(n).get_expectation_value(st)
+    assert close_expect(v, ref[n]["value"], 1.5 * n), (v, ref[n]["value"])
+    # parameter update invalidates the compiled program
+    circ.set_parameter(0, circ.get_parameter(0) + 0.1)
+    st2 = qs.QuantumState(n)
+    circ.update_quantum_state(st2)
+    assert abs(workloads.tfim_observable(n).get_expectation_value(st2) - v) > 1e-8
+
+
+# ------------------------------------------------------------ oracle, larger n
+def _c_oracle():
+    lib = C.CDLL(os.path.join(ROOT, "oracle", "liboracle_c.so"))
+    return lib
+
+
+def _ip(v):
+    return (C.c_int * max(1, len(v)))(*v)
+
+
+def _oracle_apply(lib, psi, n, rec):
+    kind = rec[0]
+    if kind == "dense":
+        _, t, mat, ctl = rec
+        mat = np.ascontiguousarray(mat, dtype=np.complex128)
+        lib.oracle_apply_dense(psi.ctypes.data, n, _ip(t), len(t), mat.ctypes.data,
+                               _ip([q for q, _ in ctl]), _ip([v for _, v in ctl]), len(ctl))
+    elif kind == "diag":
+        _, t, d, ctl = rec
+        d = np.ascontiguousarray(d, dtype=np.complex128)
+        lib.oracle_apply_diag(psi.ctypes.data, n, _ip(t), len(t), d.ctypes.data,
+                              _ip([q for q, _ in ctl]), _ip([v for _, v in ctl]), len(ctl))
+    elif kind == "pauli" and not rec[3]:
+        lib.oracle_apply_pauli(psi.ctypes.data, n, _ip(rec[1]), _ip(rec[2]), len(rec[1]))
+    elif kind == "pauli_rot" and not rec[4]:
+        lib.oracle_apply_pauli_rot(psi.ctypes.data, n, _ip(rec[1]), _ip(rec[2]), len(rec[1]),
+                                   C.c_double(rec[3]))
+    elif kind == "pauli":
+        _, t, ids, ctl = rec
+        _oracle_apply(lib, psi, n, ("dense", t, orc.pauli_matrix(ids), ctl))
+    else:
+        _, t, ids, ang, ctl = rec
+        mat = np.cos(ang / 2) * np.eye(1 << len(t)) + 1j * np.sin(ang / 2) * orc.pauli_matrix(ids)
+        _oracle_apply(lib, psi, n, ("dense", t, mat, ctl))
+
+
+def cfg2_gates(n):
+    """cfg2 sweep: H, RX, RZ, CNOT((t+1)%n, t), CZ(t, (t+1)%n) on every t."""
+    out = []
+    for t in range(n):
+        theta = float(np.random.default_rng(t).uniform(0, 2 * np.pi))
+        out += [qg.H(t), qg.RX(t, theta), qg.RZ(t, theta),
+                qg.CNOT((t + 1) % n, t), qg.CZ(t, (t + 1) % n)]
+    return out
+
+
+@pytest.mark.parametrize("n", [2, 5, 20])
+def test_cfg2_sweep_vs_oracle(n):
+    """Every (gate, target) of the per-gate sweep, applied one by one with
+    single-gate calls, vs the C oracle."""
+    lib = _c_oracle()
+    st = haar(n, 0)
+    ref = orc.haar_state(n, 0)
+    for g in cfg2_gates(n):
+        g.update_quantum_state(st)
+        _oracle_apply(lib, ref, n, g._core.record())
+    err = np.max(np.abs(st.get_vector() - ref))
+    assert err <= AMP_TOL, err
+
+
+@pytest.mark.slow
+def test_cfg2_n28_sampled_vs_oracle():
+    """10 sampled (gate, target) pairs at the benchmark width n=28 vs the C
+    oracle (4 GiB state)."""
+    n = 28
+    lib = _c_oracle()
+    ref = orc.haar_state(n, 0)
+    st = qs.QuantumState(n)
+    st.load(ref)
+    gates = cfg2_gates(n)
+    pick = np.random.default_rng(1).choice(len(gates), size=10, replace=False)
+    for i in sorted(pick):
+        gates[i].update_quantum_state(st)
+        _oracle_apply(lib, ref, n, gates[i]._core.record())
+    got = st.get_vector()
+    assert np.max(np.abs(got - ref)) <= AMP_TOL
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6, 8])
+def test_dense_k_with_controls_vs_oracle(k):
+    n = 12
+    lib = _c_oracle()
+    rng = np.random.default_rng(100 + k)
+    for trial in range(4):
+        qsel = [int(v) for v in rng.permutation(n)]
+        t, rest = qsel[:k], qsel[k:]
+        ctl = [(rest[i], int(rng.integers(2))) for i in range(trial % 3)]
+        g = qg.RandomUnitary(t, seed=int(rng.integers(1 << 30)))
+        for q, v in ctl:
+            g.add_control_qubit(q, v)
+        st = haar(n, trial)
+        ref = orc.haar_state(n, trial)
+        g.update_quantum_state(st)
+        _oracle_apply(lib, ref, n, g._core.record())
+        assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (k, trial)
+
+
+def test_low_qubit_layouts():
+    """Controls / targets on bit 0 and 1 exercise the scalar and 256-bit
+    pair paths."""
+    n = 10
+    lib = _c_oracle()
+    combos = [(0, 1), (1, 0), (0, 9), (9, 0), (1, 2), (2, 1), (5, 0)]
+    for c, t in combos:
+        for mk in (lambda: qg.CNOT(c, t), lambda: qg.CZ(c, t),
+                   lambda: qg.RandomUnitary([t], seed=c * 10 + t)):
+            g = mk()
+            if len(g.get_control_index_list()) == 0:
+                g.add_control_qubit(c, 1)
+            st = haar(n, c + 17 * t)
+            ref = orc.haar_state(n, c + 17 * t)
+            g.update_quantum_state(st)
+            _oracle_apply(lib, ref, n, g._core.record())
+            assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (c, t)
+
+
+def test_big_diagonal_and_pauli_products():
+    n = 11
+    lib = _c_oracle()
+    rng = np.random.default_rng(3)
+    for m in (2, 5, 7):
+        t = [int(v) for v in rng.permutation(n)[:m]]
+        d = np.exp(1j * rng.uniform(0, 6, 1 << m))
+        g = qg.DiagonalMatrix(t, d)
+        g.add_control_qubit([q for q in range(n) if q not in t][0], 1)
+        st, ref = haar(n, m), orc.haar_state(n, m)
+        g.update_quantum_state(st)
+        _oracle_apply(lib, ref, n, g._core.record())
+        assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL
+    for trial in range(12):
+        k = int(rng.integers(1, 6))
+        t = [int(v) for v in rng.permutation(n)[:k]]
+        ids = [int(v) for v in rng.integers(1, 4, k)]
+        for g in (qg.Pauli(t, ids), qg.PauliRotation(t, ids, float(rng.uniform(-7, 7)))):
+            st, ref = haar(n, trial), orc.haar_state(n, trial)
+            g.update_quantum_state(st)
+            _oracle_apply(lib, ref, n, g._core.record())
+            assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (t, ids)
+
+
+def test_cz_ladder_fused_n20_vs_oracle():
+    """cfg4 code path (heavy(5) fusion + engine planner) at n=20."""
+    n = 20
+    lib = _c_oracle()
+    circ = workloads.generate_cz_ladder(n, 6, seed=1)
+    QuantumCircuitOptimizer().optimize(circ, 5)
+    st = haar(n, 4)
+    ref = orc.haar_state(n, 4)
+    circ.update_quantum_state(st)
+    for rec in circuit_records(circ):
+        _oracle_apply(lib, ref, n, rec)
+    assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL
+
+
+def test_unfused_cz_ladder_n22_vs_oracle():
+    n = 22
+    lib = _c_oracle()
+    circ = workloads.generate_cz_ladder(n, 4, seed=2)
+    st = haar(n, 5)
+    ref = orc.haar_state(n, 5)
+    circ.update_quantum_state(st)
+    for rec in circuit_records(circ):
+        _oracle_apply(lib, ref, n, rec)
+    assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL
+    # mirror check: U then U^dagger returns the start state
+    inv = qs.QuantumCircuit(n)
+    for g in reversed(circ._core.gates):
+        inv.add_gate(qg.DenseMatrix(list(g.targets), g.gate_matrix().conj().T)
+                     if not g.controls else g.copy())
+    inv.update_quantum_state(st)
+    assert np.max(np.abs(st.get_vector() - orc.haar_state(n, 5))) <= 1e-11
+
+
+# ------------------------------------------------------------- state algebra
+def test_state_algebra():
+    n = 13
+    a, b = haar(n, 1), haar(n, 2)
+    va, vb = a.get_vector(), b.get_vector()
+    assert a.get_squared_norm() == pytest.approx(1.0, abs=1e-13)
+    assert abs(inner_product(a, b) - np.vdot(va, vb)) <= 1e-13
+    a.multiply_coef(0.5 - 2j)
+    assert np.max(np.abs(a.get_vector() - (0.5 - 2j) * va)) <= 1e-15
+    a.add_state(b)
+    assert np.max(np.abs(a.get_vector() - ((0.5 - 2j) * va + vb))) <= 1e-14
+    s = a.get_squared_norm()
+    a.normalize(s)
+    assert a.get_squared_norm() == pytest.approx(1.0, abs=1e-12)
+    c = a.copy()
+    assert np.array_equal(c.get_vector(), a.get_vector())
+    c.set_computational_basis(5)
+    v = c.get_vector()
+    assert v[5] == 1 and np.count_nonzero(v) == 1
+    c.set_zero_state()
+    assert c.get_vector()[0] == 1
+    with pytest.raises(ValueError):
+        c.set_computational_basis(1 << n)
+    with pytest.raises(ValueError):
+        inner_product(qs.QuantumState(2), qs.QuantumState(3))
+
+
+def test_roundtrip_and_copy_semantics():
+    s = haar(3, 0)
+    vec = s.get_vector()
+    vec[0] = 123.0
+    assert s.get_vector()[0] != 123.0
+    t = qs.QuantumState(3)
+    t.load(s.get_vector())
+    assert np.array_equal(t.get_vector().view(np.uint64), s.get_vector().view(np.uint64))
+    with pytest.raises(ValueError):
+        qs.QuantumState(2).load([1, 0, 0])
+
+
+def test_errors_and_memory():
+    with pytest.raises(ValueError):
+        qg.H(5).update_quantum_state(qs.QuantumState(2))
+    with pytest.raises(MemoryError):
+        qs.QuantumState(40)
+    with pytest.raises(ValueError):
+        qs.QuantumState(0)
+
+
+def test_deterministic_release():
+    import weakref
+    refs = []
+    for i in range(2000):
+        s = qs.QuantumState(4)
+        if i % 500 == 0:
+            refs.append(weakref.ref(s))
+        del s
+    assert all(r() is None for r in refs)
+
+
+def test_device_random_state_is_normalised():
+    s = qs.QuantumState(16)
+    s.set_random_state_device(7)
+    assert s.get_squared_norm() == pytest.approx(1.0, abs=1e-12)
+
+
+def test_program_stats_and_reuse():
+    circ = workloads.generate_cnot_ring(12, seed=1)
+    stats = circ.program_stats()
+    assert stats["num_ops_in"] == circ.get_gate_count()
+    a, b = qs.QuantumState(12), qs.QuantumState(12)
+    circ.update_quantum_state(a)
+    circ.update_quantum_state(b)
+    assert np.array_equal(a.get_vector(), b.get_vector())
