@@ -6,7 +6,6 @@ on expectation values with an absolute floor of 1e-10 * sum|coef| (SURVEY.md
 8(c) "near-zero expectations").
 """
 
-import ctypes as C
 import os
 
 import numpy as np
@@ -21,7 +20,7 @@ from paper_2011_13524_b200.circuit import QuantumCircuitOptimizer
 from paper_2011_13524_b200.quantum_operator import create_quantum_operator_from_openfermion_text
 from paper_2011_13524_b200.state import inner_product
 
-from oracle import qsim_oracle as orc
+from oracle import c_oracle, qsim_oracle as orc
 from golden_util import build_gate, load_circuits, load_gate_cases, load_haar, load_observables
 
 pytestmark = pytest.mark.gpu
@@ -135,41 +134,6 @@ def test_golden_vqe(n):
 
 
 # ------------------------------------------------------------ oracle, larger n
-def _c_oracle():
-    lib = C.CDLL(os.path.join(ROOT, "oracle", "liboracle_c.so"))
-    return lib
-
-
-def _ip(v):
-    return (C.c_int * max(1, len(v)))(*v)
-
-
-def _oracle_apply(lib, psi, n, rec):
-    kind = rec[0]
-    if kind == "dense":
-        _, t, mat, ctl = rec
-        mat = np.ascontiguousarray(mat, dtype=np.complex128)
-        lib.oracle_apply_dense(psi.ctypes.data, n, _ip(t), len(t), mat.ctypes.data,
-                               _ip([q for q, _ in ctl]), _ip([v for _, v in ctl]), len(ctl))
-    elif kind == "diag":
-        _, t, d, ctl = rec
-        d = np.ascontiguousarray(d, dtype=np.complex128)
-        lib.oracle_apply_diag(psi.ctypes.data, n, _ip(t), len(t), d.ctypes.data,
-                              _ip([q for q, _ in ctl]), _ip([v for _, v in ctl]), len(ctl))
-    elif kind == "pauli" and not rec[3]:
-        lib.oracle_apply_pauli(psi.ctypes.data, n, _ip(rec[1]), _ip(rec[2]), len(rec[1]))
-    elif kind == "pauli_rot" and not rec[4]:
-        lib.oracle_apply_pauli_rot(psi.ctypes.data, n, _ip(rec[1]), _ip(rec[2]), len(rec[1]),
-                                   C.c_double(rec[3]))
-    elif kind == "pauli":
-        _, t, ids, ctl = rec
-        _oracle_apply(lib, psi, n, ("dense", t, orc.pauli_matrix(ids), ctl))
-    else:
-        _, t, ids, ang, ctl = rec
-        mat = np.cos(ang / 2) * np.eye(1 << len(t)) + 1j * np.sin(ang / 2) * orc.pauli_matrix(ids)
-        _oracle_apply(lib, psi, n, ("dense", t, mat, ctl))
-
-
 def cfg2_gates(n):
     """cfg2 sweep: H, RX, RZ, CNOT((t+1)%n, t), CZ(t, (t+1)%n) on every t."""
     out = []
@@ -184,12 +148,11 @@ def cfg2_gates(n):
 def test_cfg2_sweep_vs_oracle(n):
     """Every (gate, target) of the per-gate sweep, applied one by one with
     single-gate calls, vs the C oracle."""
-    lib = _c_oracle()
     st = haar(n, 0)
     ref = orc.haar_state(n, 0)
     for g in cfg2_gates(n):
         g.update_quantum_state(st)
-        _oracle_apply(lib, ref, n, g._core.record())
+        c_oracle.apply_record(ref, n, g._core.record())
     err = np.max(np.abs(st.get_vector() - ref))
     assert err <= AMP_TOL, err
 
@@ -199,7 +162,6 @@ def test_cfg2_n28_sampled_vs_oracle():
     """10 sampled (gate, target) pairs at the benchmark width n=28 vs the C
     oracle (4 GiB state)."""
     n = 28
-    lib = _c_oracle()
     ref = orc.haar_state(n, 0)
     st = qs.QuantumState(n)
     st.load(ref)
@@ -207,7 +169,7 @@ def test_cfg2_n28_sampled_vs_oracle():
     pick = np.random.default_rng(1).choice(len(gates), size=10, replace=False)
     for i in sorted(pick):
         gates[i].update_quantum_state(st)
-        _oracle_apply(lib, ref, n, gates[i]._core.record())
+        c_oracle.apply_record(ref, n, gates[i]._core.record())
     got = st.get_vector()
     assert np.max(np.abs(got - ref)) <= AMP_TOL
 
@@ -215,7 +177,6 @@ def test_cfg2_n28_sampled_vs_oracle():
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6, 8])
 def test_dense_k_with_controls_vs_oracle(k):
     n = 12
-    lib = _c_oracle()
     rng = np.random.default_rng(100 + k)
     for trial in range(4):
         qsel = [int(v) for v in rng.permutation(n)]
@@ -227,7 +188,7 @@ def test_dense_k_with_controls_vs_oracle(k):
         st = haar(n, trial)
         ref = orc.haar_state(n, trial)
         g.update_quantum_state(st)
-        _oracle_apply(lib, ref, n, g._core.record())
+        c_oracle.apply_record(ref, n, g._core.record())
         assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (k, trial)
 
 
@@ -235,7 +196,6 @@ def test_low_qubit_layouts():
     """Controls / targets on bit 0 and 1 exercise the scalar and 256-bit
     pair paths."""
     n = 10
-    lib = _c_oracle()
     combos = [(0, 1), (1, 0), (0, 9), (9, 0), (1, 2), (2, 1), (5, 0)]
     for c, t in combos:
         for mk in (lambda: qg.CNOT(c, t), lambda: qg.CZ(c, t),
@@ -246,13 +206,12 @@ def test_low_qubit_layouts():
             st = haar(n, c + 17 * t)
             ref = orc.haar_state(n, c + 17 * t)
             g.update_quantum_state(st)
-            _oracle_apply(lib, ref, n, g._core.record())
+            c_oracle.apply_record(ref, n, g._core.record())
             assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (c, t)
 
 
 def test_big_diagonal_and_pauli_products():
     n = 11
-    lib = _c_oracle()
     rng = np.random.default_rng(3)
     for m in (2, 5, 7):
         t = [int(v) for v in rng.permutation(n)[:m]]
@@ -261,7 +220,7 @@ def test_big_diagonal_and_pauli_products():
         g.add_control_qubit([q for q in range(n) if q not in t][0], 1)
         st, ref = haar(n, m), orc.haar_state(n, m)
         g.update_quantum_state(st)
-        _oracle_apply(lib, ref, n, g._core.record())
+        c_oracle.apply_record(ref, n, g._core.record())
         assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL
     for trial in range(12):
         k = int(rng.integers(1, 6))
@@ -270,33 +229,31 @@ def test_big_diagonal_and_pauli_products():
         for g in (qg.Pauli(t, ids), qg.PauliRotation(t, ids, float(rng.uniform(-7, 7)))):
             st, ref = haar(n, trial), orc.haar_state(n, trial)
             g.update_quantum_state(st)
-            _oracle_apply(lib, ref, n, g._core.record())
+            c_oracle.apply_record(ref, n, g._core.record())
             assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (t, ids)
 
 
 def test_cz_ladder_fused_n20_vs_oracle():
     """cfg4 code path (heavy(5) fusion + engine planner) at n=20."""
     n = 20
-    lib = _c_oracle()
     circ = workloads.generate_cz_ladder(n, 6, seed=1)
     QuantumCircuitOptimizer().optimize(circ, 5)
     st = haar(n, 4)
     ref = orc.haar_state(n, 4)
     circ.update_quantum_state(st)
     for rec in circuit_records(circ):
-        _oracle_apply(lib, ref, n, rec)
+        c_oracle.apply_record(ref, n, rec)
     assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL
 
 
 def test_unfused_cz_ladder_n22_vs_oracle():
     n = 22
-    lib = _c_oracle()
     circ = workloads.generate_cz_ladder(n, 4, seed=2)
     st = haar(n, 5)
     ref = orc.haar_state(n, 5)
     circ.update_quantum_state(st)
     for rec in circuit_records(circ):
-        _oracle_apply(lib, ref, n, rec)
+        c_oracle.apply_record(ref, n, rec)
     assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL
     # mirror check: U then U^dagger returns the start state
     inv = qs.QuantumCircuit(n)

@@ -6,13 +6,12 @@ reference and can be trusted as the checker for the GPU path at sizes the
 fixtures do not cover.  CPU only.
 """
 
-import ctypes as C
 import os
 
 import numpy as np
 import pytest
 
-from oracle import qsim_oracle as orc
+from oracle import c_oracle, qsim_oracle as orc
 from golden_util import load_circuits, load_gate_cases, load_haar, load_observables, \
     record_from_json
 
@@ -68,49 +67,40 @@ def test_observables_match_reference():
 
 
 def test_c_oracle_matches_numpy_oracle():
-    lib = C.CDLL(os.path.join(ROOT, "oracle", "liboracle_c.so"))
     rng = np.random.default_rng(5)
-    n = 9
-    ip = lambda v: (C.c_int * max(1, len(v)))(*v)  # noqa: E731
-    for trial in range(40):
-        psi = orc.haar_state(n, trial)
-        ref = psi.copy()
-        k = int(rng.integers(1, 4))
-        qs = [int(v) for v in rng.permutation(n)]
-        t, rest = qs[:k], qs[k:]
-        nc = int(rng.integers(0, 3))
-        ctl = [(rest[i], int(rng.integers(2))) for i in range(nc)]
-        kind = trial % 4
-        if kind == 0:
-            mat = orc.pauli_matrix([1] * k) * 0.3 + np.eye(1 << k)
-            lib.oracle_apply_dense(psi.ctypes.data, n, ip(t), k, mat.ctypes.data,
-                                   ip([q for q, _ in ctl]), ip([v for _, v in ctl]), nc)
-            orc.apply_dense(ref, n, t, mat, ctl)
-        elif kind == 1:
-            d = np.exp(1j * rng.uniform(0, 6, 1 << k))
-            lib.oracle_apply_diag(psi.ctypes.data, n, ip(t), k, d.ctypes.data,
-                                  ip([q for q, _ in ctl]), ip([v for _, v in ctl]), nc)
-            orc.apply_diagonal(ref, n, t, d, ctl)
-        elif kind == 2:
-            ids = [int(v) for v in rng.integers(1, 4, k)]
-            ang = float(rng.uniform(-7, 7))
-            lib.oracle_apply_pauli_rot(psi.ctypes.data, n, ip(t), ip(ids), k, C.c_double(ang))
-            orc.apply_pauli_rotation(ref, n, t, ids, ang)
-        else:
-            ids = [int(v) for v in rng.integers(1, 4, k)]
-            lib.oracle_apply_pauli(psi.ctypes.data, n, ip(t), ip(ids), k)
-            orc.apply_pauli(ref, n, t, ids)
-        assert np.max(np.abs(psi - ref)) <= 1e-14, trial
+    for n in (9, 17):
+        for trial in range(40):
+            psi = orc.haar_state(n, trial)
+            ref = psi.copy()
+            k = int(rng.integers(1, 4))
+            qs = [int(v) for v in rng.permutation(n)]
+            t, rest = qs[:k], qs[k:]
+            nc = int(rng.integers(0, 3))
+            ctl = tuple((rest[i], int(rng.integers(2))) for i in range(nc))
+            kind = trial % 4
+            if kind == 0:
+                rec = ("dense", t, orc.pauli_matrix([1] * k) * 0.3 + np.eye(1 << k), ctl)
+            elif kind == 1:
+                rec = ("diag", t, np.exp(1j * rng.uniform(0, 6, 1 << k)), ctl)
+            elif kind == 2:
+                rec = ("pauli_rot", t, [int(v) for v in rng.integers(1, 4, k)],
+                       float(rng.uniform(-7, 7)), ctl)
+            else:
+                rec = ("pauli", t, [int(v) for v in rng.integers(1, 4, k)], ctl)
+            c_oracle.apply_record(psi, n, rec)
+            orc.apply_record(ref, n, rec)
+            assert np.max(np.abs(psi - ref)) <= 1e-14, trial
     # rotations and Paulis are bit-identical by construction
+    n = 9
     psi = orc.haar_state(n, 99)
     ref = psi.copy()
-    lib.oracle_apply_pauli_rot(psi.ctypes.data, n, ip([3]), ip([1]), 1, C.c_double(0.37))
+    c_oracle.apply_record(psi, n, ("pauli_rot", (3,), (1,), 0.37, ()))
     orc.apply_pauli_rotation(ref, n, [3], [1], 0.37)
     assert np.array_equal(psi, ref)
-    out = (C.c_double * 2)()
-    lib.oracle_pauli_term(psi.ctypes.data, psi.ctypes.data, n, ip([0, 4]), ip([1, 2]), 2, out)
+    got = c_oracle.pauli_term(psi, psi, n, [(0, 1), (4, 2)])
     v = orc.expectation(psi, psi, n, [(1.0, [(0, 1), (4, 2)])])
-    assert abs(complex(out[0], out[1]) - v) <= 1e-14
+    assert abs(got - v) <= 1e-14
+    assert abs(c_oracle.norm2(psi, n) - orc.squared_norm(psi)) <= 1e-14
 
 
 def test_cfg3_reference_value_recorded():
