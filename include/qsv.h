@@ -163,6 +163,9 @@ int qsv_program_create(int num_qubits, const qsv_op* ops, int nops,
 int qsv_program_run(qsv_program* prog, qsv_state* st);
 int qsv_program_stats_get(const qsv_program* prog, qsv_program_stats* out);
 int qsv_program_destroy(qsv_program* prog);
+/* Host-only: plan without touching a device (stats only). */
+int qsv_plan_stats(int num_qubits, const qsv_op* ops, int nops, const qsv_plan_opts* opts,
+                   qsv_program_stats* out);
 
 #ifdef __cplusplus
 }

@@ -142,6 +142,18 @@ class Circuit:
     def program_stats(self) -> dict:
         return dict(self.compile().stats)
 
+    def plan_stats(self, **kw) -> dict:
+        """Host-only planning statistics (no GPU needed)."""
+        opts = default_plan_opts(**kw) if kw else self._plan
+        ops = (_lib.QsvOp * max(1, len(self.gates)))()
+        keep = []
+        for i, g in enumerate(self.gates):
+            g.fill_op(ops[i], keep)
+        st = _lib.QsvProgramStats()
+        check(lib.qsv_plan_stats(self.num_qubits, ops, len(self.gates), C.byref(opts),
+                                 C.byref(st)))
+        return {f: getattr(st, f) for f, _ in _lib.QsvProgramStats._fields_}
+
     def update_state(self, state, rng=None) -> None:
         if state.get_qubit_count() != self.num_qubits:
             raise ValueError("state and circuit qubit counts differ")
@@ -240,6 +252,9 @@ class QuantumCircuit:
 
     def program_stats(self) -> dict:
         return self._core.program_stats()
+
+    def plan_stats(self, **kw) -> dict:
+        return self._core.plan_stats(**kw)
 
     def copy(self):
         out = type(self).__new__(type(self))

@@ -106,6 +106,8 @@ _SIGS = {
     "qsv_program_run": ([_P, _P], _I),
     "qsv_program_stats_get": ([_P, C.POINTER(QsvProgramStats)], _I),
     "qsv_program_destroy": ([_P], _I),
+    "qsv_plan_stats": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts),
+                        C.POINTER(QsvProgramStats)], _I),
 }
 
 EXPORTED = tuple(_SIGS)

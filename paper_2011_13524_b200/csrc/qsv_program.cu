@@ -59,22 +59,7 @@ void drop_graph(qsv_program* p) {
 
 }  // namespace
 
-extern "C" {
-
-int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* opts,
-                       qsv_program** out) {
-  if (!out) {
-    set_error("null output pointer");
-    return QSV_EINVAL;
-  }
-  *out = nullptr;
-  if (n < 1 || n > 40 || nops < 0 || (nops > 0 && !ops)) {
-    set_error("bad program arguments");
-    return QSV_EINVAL;
-  }
-  qsv_plan_opts o{1, 0, 1, 1};
-  if (opts) o = *opts;
-  std::vector<GateDesc> gates;
+static int convert_ops(int n, const qsv_op* ops, int nops, std::vector<GateDesc>& gates) {
   gates.reserve(nops);
   for (int i = 0; i < nops; ++i) {
     const qsv_op& op = ops[i];
@@ -126,6 +111,46 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
     if (g.nc < 0) continue;  // identity
     gates.push_back(g);
   }
+  return QSV_OK;
+}
+
+extern "C" {
+
+int qsv_plan_stats(int n, const qsv_op* ops, int nops, const qsv_plan_opts* opts,
+                   qsv_program_stats* out) {
+  if (!out || n < 1 || n > 40 || nops < 0 || (nops > 0 && !ops)) {
+    set_error("bad plan arguments");
+    return QSV_EINVAL;
+  }
+  qsv_plan_opts o{1, 0, 1, 1};
+  if (opts) o = *opts;
+  std::vector<GateDesc> gates;
+  int rc = convert_ops(n, ops, nops, gates);
+  if (rc) return rc;
+  std::vector<Step> steps;
+  std::vector<TilePlan> tiles;
+  std::vector<char> payload;
+  memset(out, 0, sizeof(*out));
+  out->num_ops_in = nops;
+  return plan_program(n, gates, o, steps, tiles, payload, out);
+}
+
+int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* opts,
+                       qsv_program** out) {
+  if (!out) {
+    set_error("null output pointer");
+    return QSV_EINVAL;
+  }
+  *out = nullptr;
+  if (n < 1 || n > 40 || nops < 0 || (nops > 0 && !ops)) {
+    set_error("bad program arguments");
+    return QSV_EINVAL;
+  }
+  qsv_plan_opts o{1, 0, 1, 1};
+  if (opts) o = *opts;
+  std::vector<GateDesc> gates;
+  int rc0 = convert_ops(n, ops, nops, gates);
+  if (rc0) return rc0;
 
   qsv_program* p = new qsv_program();
   p->n = n;

@@ -1,44 +1,832 @@
-// Tile passes and the program planner.
+// Tile passes: several gates per HBM sweep, plus the program planner.
+//
+// The reference applies a circuit gate by gate, each gate one full sweep of
+// the 2^n array (circuit.py:54-55 -> kernels.apply_*).  Here the planner
+// packs consecutive gates into passes.  A pass fixes a set S of L "tile"
+// qubits (always including qubits 0..3, so HBM runs are >= 256 B); one CTA
+// loads the 2^L amplitudes that share the values of all other qubits into
+// shared memory, applies every gate of the pass, and writes the tile back.
+// A gate can join a pass when its NON-diagonal targets lie in S: diagonal
+// factors and controls on qubits outside S are constants of the tile.
+//
+// Inside a tile the gates run in "phases": each thread holds 2^kRegBits
+// amplitudes whose local indices differ in kRegBits register bits, so every
+// gate acting on register bits is pure register arithmetic; a phase boundary
+// is one shared-memory round trip (XOR-swizzled, bank-conflict free).
+//
+// HBM bytes per pass: 32 * 2^n (read + write once), independent of the number
+// of gates in it; FP64 work: 8 FMA per amplitude per 1-qubit dense gate.
 #include <algorithm>
-#include <cstring>
 #include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
 
 #include "qsv_tile.cuh"
 
 namespace qsv {
 
-int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts& opts,
+// ===================================================================== device
+
+__device__ __forceinline__ uint32_t swz(uint32_t l) {
+  return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
+}
+
+struct TileCtx {
+  uint64_t base;       // global bits of this tile
+  uint32_t lt;         // thread's local base (thread bits placed)
+  uint32_t rb[kRegBits];  // local bit mask of each register slot
+};
+
+__device__ __forceinline__ uint32_t lidx(const TileCtx& c, int j) {
+  uint32_t l = c.lt;
+#pragma unroll
+  for (int i = 0; i < kRegBits; ++i)
+    if ((j >> i) & 1) l |= c.rb[i];
+  return l;
+}
+
+__device__ __forceinline__ bool lcond(const TileOp& op, uint32_t l) {
+  return (l & op.lmask) == op.lval;
+}
+
+template <int I, bool CTRL>
+__device__ __forceinline__ void t_dense1_body(double2 (&v)[16], const TileCtx& c,
+                                              const TileOp& op, double2 m00, double2 m01,
+                                              double2 m10, double2 m11) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if ((j >> I) & 1) continue;
+    const int q = j | (1 << I);
+    const double2 x = v[j], y = v[q];
+    double2 nx = cfma(m01, y, cmul(m00, x));
+    double2 ny = cfma(m11, y, cmul(m10, x));
+    if (CTRL) {
+      const bool ok = lcond(op, lidx(c, j));
+      nx = ok ? nx : x;
+      ny = ok ? ny : y;
+    }
+    v[j] = nx;
+    v[q] = ny;
+  }
+}
+
+template <int I>
+__device__ __forceinline__ void t_dense1(double2 (&v)[16], const TileCtx& c, const TileOp& op,
+                                         const double2* __restrict__ data) {
+  const double2 m00 = __ldg(data + op.data + 0), m01 = __ldg(data + op.data + 1);
+  const double2 m10 = __ldg(data + op.data + 2), m11 = __ldg(data + op.data + 3);
+  if (op.lmask)
+    t_dense1_body<I, true>(v, c, op, m00, m01, m10, m11);
+  else
+    t_dense1_body<I, false>(v, c, op, m00, m01, m10, m11);
+}
+
+__device__ __forceinline__ void t_apply(double2 (&v)[16], const TileCtx& c, const TileOp& op,
+                                        const double2* __restrict__ data) {
+  // tile-constant part of the op
+  if (op.gmask && ((c.base & op.gmask) != op.gval)) return;
+  switch (op.kind) {
+    case T_DENSE1:
+      switch (op.slots) {
+        case 1: t_dense1<0>(v, c, op, data); break;
+        case 2: t_dense1<1>(v, c, op, data); break;
+        case 4: t_dense1<2>(v, c, op, data); break;
+        case 8: t_dense1<3>(v, c, op, data); break;
+      }
+      break;
+    case T_DIAG: {
+      int gsub = 0;
+      for (int t = 0; t < op.m; ++t)
+        if (op.tpos[t] < 0) gsub |= (int)((c.base >> (-op.tpos[t] - 1)) & 1ULL) << t;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t l = lidx(c, j);
+        if (op.lmask && !lcond(op, l)) continue;
+        int sub = gsub;
+        for (int t = 0; t < op.m; ++t)
+          if (op.tpos[t] >= 0) sub |= (int)((l >> op.tpos[t]) & 1u) << t;
+        v[j] = cmul(v[j], __ldg(data + op.data + sub));
+      }
+      break;
+    }
+    case T_PHASE: {
+      const double2 f = __ldg(data + op.data);
+      const bool neg = (op.flags & 2);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (!lcond(op, lidx(c, j))) continue;
+        v[j] = neg ? make_double2(-v[j].x, -v[j].y) : cmul(v[j], f);
+      }
+      break;
+    }
+    case T_PARITY: {
+      const double2 f0 = __ldg(data + op.data), f1 = __ldg(data + op.data + 1);
+      const int gpar = __popcll(c.base & op.zg) & 1;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int p = (__popc(lidx(c, j) & op.zl) ^ gpar) & 1;
+        v[j] = cmul(v[j], p ? f1 : f0);
+      }
+      break;
+    }
+  }
+}
+
+// ---- shared-memory ops: a phase of their own, all threads over cosets
+template <int K>
+__device__ __forceinline__ void s_dense(double2* sm, int L, const TileOp& op,
+                                        const double2* __restrict__ data, int tid) {
+  constexpr int D = 1 << K;
+  int sorted[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) sorted[j] = op.tpos[j];
+#pragma unroll
+  for (int i = 1; i < K; ++i)
+#pragma unroll
+    for (int j = K - 1; j >= i; --j)
+      if (sorted[j - 1] > sorted[j]) {
+        const int t = sorted[j];
+        sorted[j] = sorted[j - 1];
+        sorted[j - 1] = t;
+      }
+  const uint32_t ncos = 1u << (L - K);
+  for (uint32_t cidx = tid; cidx < ncos; cidx += kTileThreads) {
+    uint32_t l0 = cidx;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t lo = l0 & ((1u << sorted[j]) - 1u);
+      l0 = ((l0 ^ lo) << 1) | lo;
+    }
+    if (op.lmask && !lcond(op, l0)) continue;
+    double2 in[D];
+#pragma unroll
+    for (int w = 0; w < D; ++w) {
+      uint32_t l = l0;
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if ((w >> j) & 1) l |= 1u << op.tpos[j];
+      in[w] = sm[swz(l)];
+    }
+#pragma unroll
+    for (int z = 0; z < D; ++z) {
+      double2 acc = cmul(__ldg(data + op.data + z * D), in[0]);
+#pragma unroll
+      for (int w = 1; w < D; ++w) acc = cfma(__ldg(data + op.data + z * D + w), in[w], acc);
+      uint32_t l = l0;
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if ((z >> j) & 1) l |= 1u << op.tpos[j];
+      sm[swz(l)] = acc;
+    }
+  }
+}
+
+__device__ __forceinline__ void s_pauli(double2* sm, int L, const TileOp& op,
+                                        const double2* __restrict__ data, int tid, int gpar) {
+  const uint32_t xml = (uint32_t)op.slots;
+  const int pivot = 31 - __clz(xml);
+  const double2 alpha = __ldg(data + op.data), bph = __ldg(data + op.data + 1);
+  const uint32_t np = 1u << (L - 1);
+  for (uint32_t p = tid; p < np; p += kTileThreads) {
+    const uint32_t lo = p & ((1u << pivot) - 1u);
+    const uint32_t l = ((p ^ lo) << 1) | lo;
+    const uint32_t q = l ^ xml;
+    const double2 x = sm[swz(l)], y = sm[swz(q)];
+    const int pl = (__popc(l & op.zl) ^ gpar) & 1;
+    const int pq = (__popc(q & op.zl) ^ gpar) & 1;
+    const double2 sy = pq ? make_double2(-y.x, -y.y) : y;
+    const double2 sx = pl ? make_double2(-x.x, -x.y) : x;
+    sm[swz(l)] = cfma(bph, sy, cmul(alpha, x));
+    sm[swz(q)] = cfma(bph, sx, cmul(alpha, y));
+  }
+}
+
+__device__ __noinline__ void s_apply(double2* sm, int L, const TileOp& op,
+                                     const double2* __restrict__ data, uint64_t base, int tid) {
+  if (op.gmask && ((base & op.gmask) != op.gval)) return;
+  if (op.kind == S_PAULI) {
+    s_pauli(sm, L, op, data, tid, __popcll(base & op.zg) & 1);
+    return;
+  }
+  switch (op.m) {
+    case 1: s_dense<1>(sm, L, op, data, tid); break;
+    case 2: s_dense<2>(sm, L, op, data, tid); break;
+    case 3: s_dense<3>(sm, L, op, data, tid); break;
+    case 4: s_dense<4>(sm, L, op, data, tid); break;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// global offset of local index bits 8..11 (the loop index k of the copies)
+__device__ __forceinline__ uint64_t hi_part(const TilePassDev* pd, int L, int k) {
+  uint64_t g = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (8 + b < L && ((k >> b) & 1)) g |= 1ULL << pd->spos[8 + b];
+  return g;
+}
+
+// Persistent tile kernel: one CTA per SM walks tiles blockIdx.x, +gridDim.x,
+// ...; two shared-memory buffers, the next tile's HBM->smem copy (cp.async,
+// XOR-swizzled 16-byte slots) in flight while the current tile computes.
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_tile(double2* __restrict__ a, const TilePassDev* __restrict__ pd,
+           const TilePhase* __restrict__ phases, const TileOp* __restrict__ ops,
+           const double2* __restrict__ data, FixedBits tb, uint64_t ntiles) {
+  extern __shared__ double2 smem_all[];
+  const int L = pd->L;
+  const uint32_t tile_amps = 1u << L;
+  const int tid = threadIdx.x;
+  // local bits 0..7 of the copy index l = k * 256 + tid come from tid
+  uint64_t lo_part = 0;
+  for (int b = 0; b < 8 && b < L; ++b)
+    if ((tid >> b) & 1) lo_part |= 1ULL << pd->spos[b];
+  const int nk = (int)((tile_amps + kTileThreads - 1) / kTileThreads);
+  const bool copy_thread = (uint32_t)tid < tile_amps;
+
+  auto issue_load = [&](uint64_t tile, double2* buf) {
+    const uint64_t base = widen(tile, tb);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
+    if (copy_thread) {
+      for (int k = 0; k < nk; ++k) {
+        const uint32_t l = (uint32_t)k * kTileThreads + tid;
+        const uint64_t g = base | lo_part | hi_part(pd, L, k);
+        cp_async16(sbase + swz(l) * 16u, a + g);
+      }
+    }
+    cp_async_commit();
+  };
+
+  uint64_t tile = blockIdx.x;
+  int cur = 0;
+  if (tile < ntiles) issue_load(tile, smem_all);
+  const int nthr = pd->nthrbits;
+  const bool active = tid < (1 << nthr);
+  for (; tile < ntiles; tile += gridDim.x, cur ^= 1) {
+    double2* sm = smem_all + (size_t)cur * tile_amps;
+    const uint64_t next = tile + gridDim.x;
+    if (next < ntiles) issue_load(next, smem_all + (size_t)(cur ^ 1) * tile_amps);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const uint64_t base = widen(tile, tb);
+
+    for (int ph = 0; ph < pd->nphases; ++ph) {
+      const TilePhase& P = phases[ph];
+      if (P.type != 0) {
+        for (int o = P.op_begin; o < P.op_end; ++o) {
+          s_apply(sm, L, ops[o], data, base, tid);
+          __syncthreads();
+        }
+        continue;
+      }
+      TileCtx c;
+      c.base = base;
+      c.lt = 0;
+      for (int j = 0; j < nthr; ++j)
+        if ((tid >> j) & 1) c.lt |= 1u << P.thrpos[j];
+#pragma unroll
+      for (int i = 0; i < kRegBits; ++i) c.rb[i] = 1u << P.regpos[i];
+      if (active) {
+        double2 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = sm[swz(lidx(c, j))];
+        for (int o = P.op_begin; o < P.op_end; ++o) t_apply(v, c, ops[o], data);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sm[swz(lidx(c, j))] = v[j];
+      }
+      __syncthreads();
+    }
+
+    // shared -> HBM (same mapping as the load)
+    if (copy_thread) {
+      for (int k = 0; k < nk; ++k) {
+        const uint32_t l = (uint32_t)k * kTileThreads + tid;
+        const uint64_t g = base | lo_part | hi_part(pd, L, k);
+        st1(a + g, sm[swz(l)]);
+      }
+    }
+    __syncthreads();  // buffer `cur` is refilled two tiles later
+  }
+  cp_async_wait<0>();
+}
+
+// ======================================================================= host
+
+namespace {
+
+struct M2 {
+  Cplx m[4];
+};
+
+M2 mat_of_1q(const GateDesc& g) {
+  // canonical 1-qubit uncontrolled gate -> 2x2
+  M2 r;
+  if (g.kind == QSV_OP_DENSE) {
+    for (int i = 0; i < 4; ++i) r.m[i] = g.data[i];
+  } else if (g.kind == QSV_OP_DIAG) {
+    r.m[0] = g.data[0];
+    r.m[1] = {0, 0};
+    r.m[2] = {0, 0};
+    r.m[3] = g.data[1];
+  } else {  // PAULI, one target
+    const int id = g.ids[0];
+    Cplx z{0, 0}, one{1, 0};
+    if (id == 1) r = {{z, one, one, z}};
+    else if (id == 2) r = {{z, {0, -1}, {0, 1}, z}};
+    else if (id == 3) r = {{one, z, z, {-1, 0}}};
+    else r = {{one, z, z, one}};
+  }
+  return r;
+}
+
+Cplx cm(Cplx a, Cplx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+Cplx ca(Cplx a, Cplx b) { return {a.re + b.re, a.im + b.im}; }
+
+M2 mul(const M2& A, const M2& B) {  // A * B
+  M2 r;
+  r.m[0] = ca(cm(A.m[0], B.m[0]), cm(A.m[1], B.m[2]));
+  r.m[1] = ca(cm(A.m[0], B.m[1]), cm(A.m[1], B.m[3]));
+  r.m[2] = ca(cm(A.m[2], B.m[0]), cm(A.m[3], B.m[2]));
+  r.m[3] = ca(cm(A.m[2], B.m[1]), cm(A.m[3], B.m[3]));
+  return r;
+}
+
+bool is_zero(Cplx c) { return c.re == 0.0 && c.im == 0.0; }
+
+bool is_1q(const GateDesc& g) {
+  if (g.m != 1 || g.nc != 0) return false;
+  return g.kind == QSV_OP_DENSE || g.kind == QSV_OP_DIAG || g.kind == QSV_OP_PAULI;
+}
+
+bool is_diagonal_gate(const GateDesc& g) {
+  if (g.kind == QSV_OP_DIAG) return true;
+  if (g.kind == QSV_OP_PAULI || g.kind == QSV_OP_PAULI_ROT) {
+    for (int j = 0; j < g.m; ++j)
+      if (g.ids[j] == 1 || g.ids[j] == 2) return false;
+    return true;
+  }
+  return false;
+}
+
+GateDesc desc_from_m2(int q, const M2& M) {
+  GateDesc g;
+  memset(g.targets, 0, sizeof(g.targets));
+  memset(g.ids, 0, sizeof(g.ids));
+  memset(g.cq, 0, sizeof(g.cq));
+  memset(g.cv, 0, sizeof(g.cv));
+  g.m = 1;
+  g.nc = 0;
+  g.angle = 0;
+  g.targets[0] = q;
+  if (is_zero(M.m[1]) && is_zero(M.m[2])) {
+    g.kind = QSV_OP_DIAG;
+    g.data = {M.m[0], M.m[3]};
+  } else {
+    g.kind = QSV_OP_DENSE;
+    g.data = {M.m[0], M.m[1], M.m[2], M.m[3]};
+  }
+  return g;
+}
+
+// Merge runs of uncontrolled 1-qubit gates on the same qubit into one 2x2
+// (a pending product per qubit, flushed before the next gate that does not
+// commute with it).  Diagonal pendings commute with diagonal gates.
+std::vector<GateDesc> fuse_1q(int n, const std::vector<GateDesc>& in) {
+  std::vector<GateDesc> out;
+  std::vector<int> has(n, 0);
+  std::vector<M2> pend(n);
+  std::vector<int> pend_cnt(n, 0);
+  auto pend_diag = [&](int q) { return is_zero(pend[q].m[1]) && is_zero(pend[q].m[2]); };
+  auto flush = [&](int q) {
+    if (!has[q]) return;
+    out.push_back(canonicalize(desc_from_m2(q, pend[q])));
+    if (out.back().nc < 0) out.pop_back();  // identity
+    has[q] = 0;
+    pend_cnt[q] = 0;
+  };
+  for (const GateDesc& g : in) {
+    if (is_1q(g)) {
+      const int q = g.targets[0];
+      const M2 M = mat_of_1q(g);
+      pend[q] = has[q] ? mul(M, pend[q]) : M;
+      has[q] = 1;
+      ++pend_cnt[q];
+      continue;
+    }
+    const bool gdiag = is_diagonal_gate(g);
+    auto touch = [&](int q) {
+      if (has[q] && !(gdiag && pend_diag(q))) flush(q);
+    };
+    for (int j = 0; j < g.m; ++j) touch(g.targets[j]);
+    for (int j = 0; j < g.nc; ++j) touch(g.cq[j]);
+    out.push_back(g);
+  }
+  for (int q = 0; q < n; ++q) flush(q);
+  return out;
+}
+
+// qubits that must be tile (local) qubits for the gate to run in a tile;
+// returns false if the gate cannot run inside a tile at all
+bool active_qubits(const GateDesc& g, uint64_t* act) {
+  *act = 0;
+  if (g.kind == QSV_OP_DENSE) {
+    if (g.m > 4) return false;
+    for (int j = 0; j < g.m; ++j) *act |= 1ULL << g.targets[j];
+    return true;
+  }
+  if (g.kind == QSV_OP_DIAG) return g.m <= 4;
+  if (g.kind == QSV_OP_PAULI || g.kind == QSV_OP_PAULI_ROT) {
+    if (g.nc) return false;  // canonical controlled Paulis are dense
+    for (int j = 0; j < g.m; ++j)
+      if (g.ids[j] == 1 || g.ids[j] == 2) *act |= 1ULL << g.targets[j];
+    return true;
+  }
+  return false;
+}
+
+uint64_t touched_mask(const GateDesc& g) {
+  uint64_t m = 0;
+  for (int j = 0; j < g.m; ++j) m |= 1ULL << g.targets[j];
+  for (int j = 0; j < g.nc; ++j) m |= 1ULL << g.cq[j];
+  return m;
+}
+
+int popc64(uint64_t x) { return __builtin_popcountll(x); }
+
+struct PassSel {
+  uint64_t S;                 // tile qubits
+  std::vector<int> taken;     // indices into the gate list, in order
+};
+
+// Greedy pass: scan gates in order; take a gate when no deferred gate shares
+// a qubit with it and its active qubits fit in S (growing S up to L).
+PassSel select_pass(int n, int L, const std::vector<GateDesc>& gates,
+                    const std::vector<uint64_t>& act, const std::vector<char>& ok,
+                    const std::vector<char>& done, size_t first) {
+  PassSel ps;
+  const int c = std::min(kLowQubits, n);
+  ps.S = (c >= 64) ? ~0ULL : ((1ULL << c) - 1);
+  uint64_t blocked = 0;
+  const uint64_t all = (n >= 64) ? ~0ULL : ((1ULL << n) - 1);
+  for (size_t i = first; i < gates.size(); ++i) {
+    if (done[i]) continue;
+    const uint64_t T = touched_mask(gates[i]);
+    if (!ok[i] || (T & blocked)) {
+      blocked |= T;
+      if ((blocked & all) == all) break;
+      continue;
+    }
+    const uint64_t A = act[i];
+    if ((A & ~ps.S) == 0) {
+      ps.taken.push_back((int)i);
+    } else if (popc64(ps.S | A) <= L) {
+      ps.S |= A;
+      ps.taken.push_back((int)i);
+    } else {
+      blocked |= T;
+      if ((blocked & all) == all) break;
+    }
+  }
+  // pad S to exactly L qubits with the lowest unused qubits
+  for (int q = 0; q < n && popc64(ps.S) < L; ++q) ps.S |= 1ULL << q;
+  return ps;
+}
+
+void put(std::vector<char>& buf, size_t off, const void* src, size_t bytes) {
+  if (buf.size() < off + bytes) buf.resize(off + bytes);
+  memcpy(buf.data() + off, src, bytes);
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// choose thread-bit order: the first three lane bits should have distinct
+// residues mod 3 so the XOR swizzle keeps 16-byte smem accesses conflict free
+void order_thread_bits(std::vector<int>& tb) {
+  for (size_t k = 0; k < 3 && k < tb.size(); ++k) {
+    for (size_t j = k; j < tb.size(); ++j) {
+      bool clash = false;
+      for (size_t p = 0; p < k; ++p)
+        if (tb[p] % 3 == tb[j] % 3) clash = true;
+      if (!clash) {
+        std::swap(tb[k], tb[j]);
+        break;
+      }
+    }
+  }
+}
+
+struct Encoded {
+  TilePassDev pd;
+  std::vector<TilePhase> phases;
+  std::vector<TileOp> ops;
+  std::vector<Cplx> data;
+};
+
+// Build phases and ops of one pass.
+Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>& pg) {
+  Encoded e;
+  memset(&e.pd, 0, sizeof(e.pd));
+  e.pd.L = L;
+  e.pd.nthrbits = L - kRegBits;
+  e.pd.smask = S;
+  int local_of[64];
+  for (int q = 0; q < 64; ++q) local_of[q] = -1;
+  {
+    int j = 0;
+    for (int q = 0; q < n; ++q)
+      if ((S >> q) & 1ULL) {
+        e.pd.spos[j] = q;
+        local_of[q] = j++;
+      }
+  }
+  // current register phase
+  bool open = false;
+  uint32_t R = 0;
+  size_t op_begin = 0;
+  std::vector<std::pair<size_t, int>> d1;  // (op index, local bit) of T_DENSE1 ops
+  auto close = [&]() {
+    if (!open) return;
+    for (int b = L - 1; b >= 0 && __builtin_popcount(R) < kRegBits; --b) R |= 1u << b;
+    TilePhase ph;
+    memset(&ph, 0, sizeof(ph));
+    ph.type = 0;
+    int slot_of[32];
+    for (int b = 0; b < 32; ++b) slot_of[b] = -1;
+    int sidx = 0;
+    std::vector<int> tb;
+    for (int b = 0; b < L; ++b) {
+      if ((R >> b) & 1u) {
+        ph.regpos[sidx] = b;
+        slot_of[b] = sidx++;
+      } else {
+        tb.push_back(b);
+      }
+    }
+    order_thread_bits(tb);
+    for (size_t k = 0; k < tb.size(); ++k) ph.thrpos[k] = tb[k];
+    for (auto& pr : d1) e.ops[pr.first].slots = 1 << slot_of[pr.second];
+    ph.op_begin = (int)op_begin;
+    ph.op_end = (int)e.ops.size();
+    e.phases.push_back(ph);
+    open = false;
+    R = 0;
+    d1.clear();
+  };
+  auto open_reg = [&]() {
+    if (open) return;
+    open = true;
+    R = 0;
+    op_begin = e.ops.size();
+  };
+  for (const GateDesc* gp : pg) {
+    const GateDesc& g = *gp;
+    TileOp op;
+    memset(&op, 0, sizeof(op));
+    for (int c = 0; c < g.nc; ++c) {
+      const int q = g.cq[c];
+      if (local_of[q] >= 0) {
+        op.lmask |= 1u << local_of[q];
+        if (g.cv[c]) op.lval |= 1u << local_of[q];
+      } else {
+        op.gmask |= 1ULL << q;
+        if (g.cv[c]) op.gval |= 1ULL << q;
+      }
+    }
+    op.data = (uint32_t)e.data.size();
+    if (g.kind == QSV_OP_DENSE && g.m == 1) {
+      const int b = local_of[g.targets[0]];
+      open_reg();
+      if (!((R >> b) & 1u) && __builtin_popcount(R) >= kRegBits) {
+        close();
+        open_reg();
+      }
+      R |= 1u << b;
+      op.kind = T_DENSE1;
+      const Cplx* M = g.data.data();
+      if (is_zero(M[0]) && is_zero(M[3]) && M[1].re == 1.0 && M[1].im == 0.0 &&
+          M[2].re == 1.0 && M[2].im == 0.0)
+        op.flags |= 1;
+      e.data.insert(e.data.end(), g.data.begin(), g.data.end());
+      d1.push_back({e.ops.size(), b});
+      e.ops.push_back(op);
+      continue;
+    }
+    if (g.kind == QSV_OP_DENSE) {  // m = 2..4: shared-memory op
+      close();
+      op.kind = S_DENSE;
+      op.m = g.m;
+      for (int t = 0; t < g.m; ++t) op.tpos[t] = local_of[g.targets[t]];
+      e.data.insert(e.data.end(), g.data.begin(), g.data.end());
+      TilePhase ph;
+      memset(&ph, 0, sizeof(ph));
+      ph.type = 1;
+      ph.op_begin = (int)e.ops.size();
+      e.ops.push_back(op);
+      ph.op_end = (int)e.ops.size();
+      e.phases.push_back(ph);
+      continue;
+    }
+    if (g.kind == QSV_OP_DIAG) {
+      open_reg();
+      if (g.m == 0) {
+        op.kind = T_PHASE;
+        const Cplx f = g.data[0];
+        if (f.re == -1.0 && f.im == 0.0) op.flags |= 2;
+        e.data.push_back(f);
+      } else {
+        op.kind = T_DIAG;
+        op.m = g.m;
+        for (int t = 0; t < g.m; ++t) {
+          const int q = g.targets[t];
+          op.tpos[t] = local_of[q] >= 0 ? local_of[q] : -(q + 1);
+        }
+        e.data.insert(e.data.end(), g.data.begin(), g.data.end());
+      }
+      e.ops.push_back(op);
+      continue;
+    }
+    // PAULI / PAULI_ROT, uncontrolled
+    uint64_t xm = 0, zm = 0;
+    int ny = 0;
+    for (int t = 0; t < g.m; ++t) {
+      const int id = g.ids[t];
+      if (id == 1 || id == 2) xm |= 1ULL << g.targets[t];
+      if (id == 2 || id == 3) zm |= 1ULL << g.targets[t];
+      if (id == 2) ++ny;
+    }
+    Cplx alpha{0, 0}, beta{1, 0};
+    if (g.kind == QSV_OP_PAULI_ROT) {
+      alpha = {std::cos(g.angle / 2), 0};
+      beta = {0, std::sin(g.angle / 2)};
+    }
+    static const Cplx ip[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+    const Cplx bph = cm(beta, ip[ny & 3]);
+    for (int q = 0; q < n; ++q)
+      if ((zm >> q) & 1ULL) {
+        if (local_of[q] >= 0) op.zl |= 1u << local_of[q];
+        else op.zg |= 1ULL << q;
+      }
+    if (xm == 0) {
+      open_reg();
+      op.kind = T_PARITY;
+      e.data.push_back(ca(alpha, bph));
+      e.data.push_back({alpha.re - bph.re, alpha.im - bph.im});
+      e.ops.push_back(op);
+      continue;
+    }
+    close();
+    op.kind = S_PAULI;
+    uint32_t xl = 0;
+    for (int q = 0; q < n; ++q)
+      if ((xm >> q) & 1ULL) xl |= 1u << local_of[q];
+    op.slots = (int32_t)xl;
+    e.data.push_back(alpha);
+    e.data.push_back(bph);
+    TilePhase ph;
+    memset(&ph, 0, sizeof(ph));
+    ph.type = 1;
+    ph.op_begin = (int)e.ops.size();
+    e.ops.push_back(op);
+    ph.op_end = (int)e.ops.size();
+    e.phases.push_back(ph);
+  }
+  close();
+  e.pd.nphases = (int)e.phases.size();
+  return e;
+}
+
+void add_gate_step(int n, const GateDesc& g, std::vector<Step>& steps, std::vector<char>& payload,
+                   qsv_program_stats* stats) {
+  Step st;
+  st.type = 0;
+  st.gate = g;
+  st.tile = -1;
+  std::vector<char> pl = make_payload(g);
+  st.has_payload = !pl.empty();
+  st.payload_off = 0;
+  if (st.has_payload) {
+    const size_t off = align_up(payload.size(), 256);
+    put(payload, off, pl.data(), pl.size());
+    st.payload_off = off;
+  }
+  steps.push_back(st);
+  stats->num_gate_kernels += 1;
+  stats->num_steps += 1;
+  stats->hbm_bytes += gate_hbm_bytes(n, g);
+}
+
+}  // namespace
+
+int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_opts& opts,
                  std::vector<Step>& steps, std::vector<TilePlan>& tiles,
                  std::vector<char>& payload, qsv_program_stats* stats) {
-  (void)opts;
-  (void)tiles;
-  for (const GateDesc& g : gates) {
-    Step st;
-    st.type = 0;
-    st.gate = g;
-    st.tile = -1;
-    std::vector<char> pl = make_payload(g);
-    st.has_payload = !pl.empty();
-    st.payload_off = 0;
-    if (st.has_payload) {
-      size_t off = (payload.size() + 255) & ~(size_t)255;
-      payload.resize(off + pl.size());
-      memcpy(payload.data() + off, pl.data(), pl.size());
-      st.payload_off = off;
+  std::vector<GateDesc> gates = opts.fuse ? fuse_1q(n, gates_in) : gates_in;
+  int L = opts.tile_qubits > 0 ? opts.tile_qubits : kMaxTileQubits;
+  L = std::min(std::min(L, kMaxTileQubits), n);
+  const bool tiles_on = opts.use_tiles && n >= kRegBits + 1 && L >= kRegBits + 1;
+  if (!tiles_on) {
+    for (const GateDesc& g : gates) add_gate_step(n, g, steps, payload, stats);
+    return QSV_OK;
+  }
+  const size_t G = gates.size();
+  std::vector<uint64_t> act(G, 0);
+  std::vector<char> ok(G, 0), done(G, 0);
+  for (size_t i = 0; i < G; ++i) ok[i] = active_qubits(gates[i], &act[i]) && popc64(act[i]) <= L;
+  size_t first = 0;
+  while (true) {
+    while (first < G && done[first]) ++first;
+    if (first >= G) break;
+    if (!ok[first]) {
+      add_gate_step(n, gates[first], steps, payload, stats);
+      done[first] = 1;
+      continue;
     }
+    PassSel ps = select_pass(n, L, gates, act, ok, done, first);
+    if (ps.taken.size() == 1) {
+      // a lone gate is cheaper as its own streaming kernel
+      add_gate_step(n, gates[ps.taken[0]], steps, payload, stats);
+      done[ps.taken[0]] = 1;
+      continue;
+    }
+    std::vector<const GateDesc*> pg;
+    for (int k : ps.taken) {
+      pg.push_back(&gates[k]);
+      done[k] = 1;
+    }
+    Encoded e = encode_pass(n, L, ps.S, pg);
+    TilePlan tp;
+    tp.L = L;
+    for (int q = 0; q < n; ++q)
+      if ((ps.S >> q) & 1ULL) tp.qubits.push_back(q);
+    tp.nphases = (int)e.phases.size();
+    tp.nops = (int)e.ops.size();
+    tp.num_gates = (int)pg.size();
+    tp.hbm_bytes = 32.0 * std::ldexp(1.0, n);
+    // payload: [TilePassDev][phases][ops][data]
+    size_t off = align_up(payload.size(), 256);
+    tp.dev_off = off;
+    put(payload, off, &e.pd, sizeof(e.pd));
+    off = align_up(off + sizeof(e.pd), 16);
+    put(payload, off, e.phases.data(), e.phases.size() * sizeof(TilePhase));
+    off = align_up(off + e.phases.size() * sizeof(TilePhase), 16);
+    put(payload, off, e.ops.data(), e.ops.size() * sizeof(TileOp));
+    off = align_up(off + e.ops.size() * sizeof(TileOp), 16);
+    put(payload, off, e.data.data(), std::max<size_t>(1, e.data.size()) * sizeof(Cplx));
+    Step st;
+    st.type = 1;
+    st.tile = (int)tiles.size();
+    st.has_payload = true;
+    st.payload_off = tp.dev_off;
+    tiles.push_back(tp);
     steps.push_back(st);
-    stats->num_gate_kernels += 1;
+    stats->num_tile_passes += 1;
     stats->num_steps += 1;
-    stats->hbm_bytes += gate_hbm_bytes(n, g);
+    stats->hbm_bytes += tp.hbm_bytes;
   }
   return QSV_OK;
 }
 
 int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,
                      cudaStream_t s) {
-  (void)amps; (void)n; (void)tp; (void)dev_payload; (void)s;
-  set_error("tile passes not available");
-  return QSV_EUNSUPPORTED;
+  const char* basep = (const char*)dev_payload + tp.dev_off;
+  size_t off = align_up(sizeof(TilePassDev), 16);
+  const TilePassDev* pd = reinterpret_cast<const TilePassDev*>(basep);
+  const TilePhase* ph = reinterpret_cast<const TilePhase*>(basep + off);
+  off = align_up(off + tp.nphases * sizeof(TilePhase), 16);
+  const TileOp* ops = reinterpret_cast<const TileOp*>(basep + off);
+  off = align_up(off + tp.nops * sizeof(TileOp), 16);
+  const double2* data = reinterpret_cast<const double2*>(basep + off);
+  int pos[kMaxTileQubits];
+  for (int j = 0; j < tp.L; ++j) pos[j] = tp.qubits[j];
+  FixedBits tb = make_fixed(pos, tp.L, 0);
+  const size_t smem = 2 * (sizeof(double2) << tp.L);
+  static int attr_dev = -1;
+  static int num_sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * (sizeof(double2) << kMaxTileQubits)));
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    attr_dev = dev;
+  }
+  const uint64_t ntiles = 1ULL << (n - tp.L);
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms);
+  k_tile<<<grid, kTileThreads, smem, s>>>(amps, pd, ph, ops, data, tb, ntiles);
+  QSV_CHECK_LAUNCH("k_tile");
+  return QSV_OK;
 }
 
 }  // namespace qsv

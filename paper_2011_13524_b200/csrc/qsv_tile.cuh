@@ -8,15 +8,65 @@
 
 namespace qsv {
 
-// A tile pass: the state is swept in tiles of 2^L amplitudes whose qubit
-// set is the low `c` qubits plus `high` (sorted); the tile's gates are
-// executed in shared memory / registers between one HBM load and one store.
+constexpr int kTileThreads = 256;   // threads per tile CTA
+constexpr int kRegBits = 4;         // amplitudes per thread = 2^kRegBits
+constexpr int kMaxTileQubits = 12;  // 2^12 amps = 64 KiB of shared memory
+constexpr int kLowQubits = 4;       // qubits 0..3 are in every tile (256 B runs)
+
+// ---- device-side program records (all POD, stored in the payload) ----
+enum TileOpKind : int32_t {
+  // register-phase ops (each thread updates its 2^kRegBits amplitudes)
+  T_DENSE1 = 1,   // 2x2 on one register slot (optionally controlled)
+  T_DIAG = 5,     // diagonal, targets on local or tile (global) bits
+  T_PHASE = 6,    // constant phase on a local/tile bit pattern
+  T_PARITY = 7,   // f[parity(idx & zmask)]
+  // shared-memory ops (a phase of their own; cosets read straight from smem)
+  S_DENSE = 9,    // 2^m x 2^m on m <= 4 local bits (tpos), optionally controlled
+  S_PAULI = 10,   // X/Y product on local bits (slots = local X mask), Z parity
+};
+
+struct TileOp {
+  int32_t kind;
+  int32_t slots;      // T_DENSE1: slot mask (bit i = register slot i)
+                      // S_PAULI: X/Y mask over local bits
+  int32_t flags;      // bit 0: DENSE1 matrix is X (swap, no flops)
+  int32_t m;          // DIAG / S_DENSE: number of targets
+  uint32_t lmask;     // control pattern over local bits
+  uint32_t lval;
+  uint64_t gmask;     // control pattern over global (non-tile) bits
+  uint64_t gval;
+  uint32_t zl;        // PARITY/PAULI: sign mask over local bits
+  uint32_t pad0;
+  uint64_t zg;        // PARITY/PAULI: sign mask over global bits
+  int32_t tpos[4];    // DIAG: target position; >= 0 local bit, < 0: -(global bit)-1
+                      // S_DENSE: local bit of matrix index bit j
+  uint32_t data;      // payload offset (double2 units) of matrix / table / coefs
+  uint32_t pad1;
+};
+
+struct TilePhase {
+  int32_t type;              // 0: register phase, 1: shared-memory ops
+  int32_t regpos[kRegBits];  // local bit of each register slot
+  int32_t thrpos[8];         // local bit of thread-id bit j (j < L - kRegBits)
+  int32_t op_begin, op_end;
+};
+
+struct TilePassDev {
+  int32_t L;
+  int32_t nthrbits;          // L - kRegBits (<= 8)
+  int32_t nphases;
+  int32_t pad;
+  uint64_t smask;            // tile qubits (global positions)
+  int32_t spos[kMaxTileQubits];  // local bit j -> global qubit
+};
+
+// ---- host-side plan of one pass ----
 struct TilePlan {
   int L = 0;
-  int c = 0;
-  std::vector<int> high;
-  size_t prog_off = 0;   // device payload offset of the tile program
-  int prog_words = 0;    // size of the tile program (in 8-byte words)
+  std::vector<int> qubits;       // sorted tile qubits (global positions)
+  size_t dev_off = 0;            // payload offset of TilePassDev, then phases, ops
+  int nphases = 0;
+  int nops = 0;
   int num_gates = 0;
   double hbm_bytes = 0;
 };

@@ -1,0 +1,97 @@
+"""Tile-pass engine (several gates per HBM sweep) against the per-gate path
+and the C oracle on random circuits mixing every gate kind."""
+
+import numpy as np
+import pytest
+
+import paper_2011_13524_b200 as qs
+from paper_2011_13524_b200 import gate as qg
+from paper_2011_13524_b200._circuit import circuit_records
+
+from oracle import c_oracle, qsim_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def random_circuit(n, ngates, seed, max_k=4):
+    rng = np.random.default_rng(seed)
+    c = qs.QuantumCircuit(n)
+    for _ in range(ngates):
+        kind = int(rng.integers(0, 10))
+        perm = [int(v) for v in rng.permutation(n)]
+        if kind == 0:
+            g = qg.RandomUnitary([perm[0]], seed=int(rng.integers(1 << 30)))
+        elif kind == 1:
+            k = int(rng.integers(2, max_k + 1))
+            g = qg.RandomUnitary(perm[:k], seed=int(rng.integers(1 << 30)))
+        elif kind == 2:
+            g = qg.CNOT(perm[0], perm[1])
+        elif kind == 3:
+            g = qg.CZ(perm[0], perm[1])
+        elif kind == 4:
+            g = qg.RZ(perm[0], float(rng.uniform(-7, 7)))
+        elif kind == 5:
+            g = qg.RX(perm[0], float(rng.uniform(-7, 7)))
+        elif kind == 6:
+            k = int(rng.integers(1, 4))
+            g = qg.DiagonalMatrix(perm[:k], np.exp(1j * rng.uniform(0, 6, 1 << k)))
+        elif kind == 7:
+            k = int(rng.integers(1, 5))
+            ids = [int(v) for v in rng.integers(1, 4, k)]
+            g = qg.PauliRotation(perm[:k], ids, float(rng.uniform(-7, 7)))
+        elif kind == 8:
+            k = int(rng.integers(1, 4))
+            g = qg.Pauli(perm[:k], [int(v) for v in rng.integers(1, 4, k)])
+        else:
+            g = qg.RandomUnitary([perm[0]], seed=int(rng.integers(1 << 30)))
+            g.add_control_qubit(perm[1], int(rng.integers(2)))
+            if rng.integers(2):
+                g.add_control_qubit(perm[2], int(rng.integers(2)))
+        c.add_gate(g)
+    return c
+
+
+@pytest.mark.parametrize("n,L,seed", [(6, 6, 0), (9, 8, 1), (13, 12, 2), (14, 8, 3),
+                                      (16, 12, 4), (18, 10, 5), (20, 12, 6)])
+def test_tiles_match_oracle(n, L, seed):
+    circ = random_circuit(n, 160, seed)
+    circ.set_plan_options(use_tiles=1, tile_qubits=L)
+    stats = circ.program_stats()
+    assert stats["num_tile_passes"] >= 1, stats
+    st = qs.QuantumState(n)
+    st.set_Haar_random_state(seed)
+    circ.update_quantum_state(st)
+    ref = orc.haar_state(n, seed)
+    c_oracle.run_records(ref, n, circuit_records(circ))
+    err = np.max(np.abs(st.get_vector() - ref))
+    assert err <= 1e-12, (err, stats)
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_tiles_equal_per_gate_path(fuse):
+    n = 15
+    circ = random_circuit(n, 300, 42)
+    a, b = qs.QuantumState(n), qs.QuantumState(n)
+    a.set_Haar_random_state(1)
+    b.set_Haar_random_state(1)
+    circ.set_plan_options(use_tiles=0, fuse=0)
+    circ.update_quantum_state(a)
+    circ.set_plan_options(use_tiles=1, fuse=fuse)
+    circ.update_quantum_state(b)
+    assert np.max(np.abs(a.get_vector() - b.get_vector())) <= 1e-12
+
+
+def test_tiles_cz_ladder_pass_count_and_parity():
+    """cz-ladder: diagonal gates (RZ, CZ) never force a tile qubit, so a
+    20-qubit, depth-8 ladder needs only a handful of passes."""
+    from paper_2011_13524_b200 import workloads
+    n = 20
+    circ = workloads.generate_cz_ladder(n, 8, seed=1)
+    stats = circ.program_stats()
+    assert stats["num_tile_passes"] <= 12, stats
+    st = qs.QuantumState(n)
+    st.set_Haar_random_state(3)
+    circ.update_quantum_state(st)
+    ref = orc.haar_state(n, 3)
+    c_oracle.run_records(ref, n, circuit_records(circ))
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
