@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqsv.so")
+# QSV_LIB overrides the in-tree build (used for A/B experiments of kernel variants)
+LIB_PATH = os.environ.get("QSV_LIB") or os.path.join(_HERE, "libqsv.so")
 
 QSV_OK = 0
 QSV_EINVAL = -1

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <map>
 #include <set>
+#include <cstdlib>
 
 #include "qsv_tile.cuh"
 
@@ -50,82 +51,171 @@ __device__ __forceinline__ bool lcond(const TileOp& op, uint32_t l) {
   return (l & op.lmask) == op.lval;
 }
 
-template <int I, bool CTRL>
-__device__ __forceinline__ void t_dense1_body(double2 (&v)[16], const TileCtx& c,
-                                              const TileOp& op, double2 m00, double2 m01,
-                                              double2 m10, double2 m11) {
+// A control / pattern test (l & mask) == val split into the thread's part
+// (fixed for the phase) and the register-slot part (compile-time in j).
+struct SplitCond {
+  bool t_ok;
+  uint32_t rm, rv;  // over register slots
+};
+
+__device__ __forceinline__ SplitCond split_cond(const TileCtx& c, uint32_t mask, uint32_t val) {
+  SplitCond sc;
+  sc.rm = 0;
+  sc.rv = 0;
+  uint32_t regmask = 0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int i = 0; i < kRegBits; ++i) {
+    regmask |= c.rb[i];
+    if (mask & c.rb[i]) {
+      sc.rm |= 1u << i;
+      if (val & c.rb[i]) sc.rv |= 1u << i;
+    }
+  }
+  const uint32_t tm = mask & ~regmask;
+  sc.t_ok = (c.lt & tm) == (val & tm);
+  return sc;
+}
+
+__device__ __forceinline__ bool jcond(const SplitCond& sc, int j) {
+  return ((uint32_t)j & sc.rm) == sc.rv;
+}
+
+// sign flip on the integer pipe (keeps the FP64 pipe for the math)
+__device__ __forceinline__ double2 neg_if(double2 v, bool f) {
+  const int s = f ? (int)0x80000000 : 0;
+  return make_double2(__hiloint2double(__double2hiint(v.x) ^ s, __double2loint(v.x)),
+                      __hiloint2double(__double2hiint(v.y) ^ s, __double2loint(v.y)));
+}
+
+template <int I, bool CTRL>
+__device__ __forceinline__ void t_dense1_body(double2 (&v)[kRegs], const SplitCond& sc,
+                                              double2 m00, double2 m01, double2 m10,
+                                              double2 m11) {
+#pragma unroll
+  for (int j = 0; j < kRegs; ++j) {
     if ((j >> I) & 1) continue;
     const int q = j | (1 << I);
     const double2 x = v[j], y = v[q];
-    double2 nx = cfma(m01, y, cmul(m00, x));
-    double2 ny = cfma(m11, y, cmul(m10, x));
-    if (CTRL) {
-      const bool ok = lcond(op, lidx(c, j));
-      nx = ok ? nx : x;
-      ny = ok ? ny : y;
+    const double2 nx = cfma(m01, y, cmul(m00, x));
+    const double2 ny = cfma(m11, y, cmul(m10, x));
+    if (CTRL) {  // predicated select, no branch
+      const bool ok = jcond(sc, j);
+      v[j].x = ok ? nx.x : x.x;
+      v[j].y = ok ? nx.y : x.y;
+      v[q].x = ok ? ny.x : y.x;
+      v[q].y = ok ? ny.y : y.y;
+    } else {
+      v[j] = nx;
+      v[q] = ny;
     }
-    v[j] = nx;
-    v[q] = ny;
   }
 }
 
 template <int I>
-__device__ __forceinline__ void t_dense1(double2 (&v)[16], const TileCtx& c, const TileOp& op,
-                                         const double2* __restrict__ data) {
-  const double2 m00 = __ldg(data + op.data + 0), m01 = __ldg(data + op.data + 1);
-  const double2 m10 = __ldg(data + op.data + 2), m11 = __ldg(data + op.data + 3);
-  if (op.lmask)
-    t_dense1_body<I, true>(v, c, op, m00, m01, m10, m11);
+__device__ __forceinline__ void t_dense1(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
+                                         const double2* data) {
+  const double2 m00 = (data[op.data + 0]), m01 = (data[op.data + 1]);
+  const double2 m10 = (data[op.data + 2]), m11 = (data[op.data + 3]);
+  SplitCond sc{true, 0, 0};
+  if (op.lmask) {
+    sc = split_cond(c, op.lmask, op.lval);
+    if (!sc.t_ok) return;
+  }
+  if (sc.rm)
+    t_dense1_body<I, true>(v, sc, m00, m01, m10, m11);
   else
-    t_dense1_body<I, false>(v, c, op, m00, m01, m10, m11);
+    t_dense1_body<I, false>(v, sc, m00, m01, m10, m11);
 }
 
-__device__ __forceinline__ void t_apply(double2 (&v)[16], const TileCtx& c, const TileOp& op,
-                                        const double2* __restrict__ data) {
+__device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
+                                        const double2* data) {
   // tile-constant part of the op
   if (op.gmask && ((c.base & op.gmask) != op.gval)) return;
   switch (op.kind) {
     case T_DENSE1:
       switch (op.slots) {
         case 1: t_dense1<0>(v, c, op, data); break;
-        case 2: t_dense1<1>(v, c, op, data); break;
-        case 4: t_dense1<2>(v, c, op, data); break;
-        case 8: t_dense1<3>(v, c, op, data); break;
+        case 2: t_dense1<1 % kRegBits>(v, c, op, data); break;
+        case 4: t_dense1<2 % kRegBits>(v, c, op, data); break;
+        case 8: t_dense1<3 % kRegBits>(v, c, op, data); break;
       }
       break;
-    case T_DIAG: {
-      int gsub = 0;
-      for (int t = 0; t < op.m; ++t)
-        if (op.tpos[t] < 0) gsub |= (int)((c.base >> (-op.tpos[t] - 1)) & 1ULL) << t;
+    case T_PHASE: {
+      const SplitCond sc = split_cond(c, op.lmask, op.lval);
+      if (!sc.t_ok) break;
+      if (op.flags & 2) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t l = lidx(c, j);
-        if (op.lmask && !lcond(op, l)) continue;
-        int sub = gsub;
-        for (int t = 0; t < op.m; ++t)
-          if (op.tpos[t] >= 0) sub |= (int)((l >> op.tpos[t]) & 1u) << t;
-        v[j] = cmul(v[j], __ldg(data + op.data + sub));
+        for (int j = 0; j < kRegs; ++j) v[j] = neg_if(v[j], jcond(sc, j));
+      } else {
+        const double2 f = (data[op.data]);
+#pragma unroll
+        for (int j = 0; j < kRegs; ++j) {
+          const double2 w = cmul(v[j], f);
+          const bool ok = jcond(sc, j);
+          v[j].x = ok ? w.x : v[j].x;
+          v[j].y = ok ? w.y : v[j].y;
+        }
       }
       break;
     }
-    case T_PHASE: {
-      const double2 f = __ldg(data + op.data);
-      const bool neg = (op.flags & 2);
+    case T_DIAG: {
+      const SplitCond sc = split_cond(c, op.lmask, op.lval);
+      if (!sc.t_ok) break;
+      // per target: tile/thread constant bit, or register slot
+      int fixed_sub = 0;
+      int slot[4] = {-1, -1, -1, -1};
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (!lcond(op, lidx(c, j))) continue;
-        v[j] = neg ? make_double2(-v[j].x, -v[j].y) : cmul(v[j], f);
+      for (int t = 0; t < 4; ++t) {
+        if (t >= op.m) continue;
+        const int p = op.tpos[t];
+        if (p < 0) {
+          fixed_sub |= (int)((c.base >> (-p - 1)) & 1ULL) << t;
+        } else {
+          int s = -1;
+#pragma unroll
+          for (int i = 0; i < kRegBits; ++i)
+            if (c.rb[i] == (1u << p)) s = i;
+          if (s < 0) fixed_sub |= (int)((c.lt >> p) & 1u) << t;
+          slot[t] = s;
+        }
+      }
+      const double2* tab = data + op.data;
+      if (op.m == 1 && slot[0] >= 0) {
+        const double2 d0 = tab[0], d1 = tab[1];
+        const int s0 = slot[0];
+#pragma unroll
+        for (int j = 0; j < kRegs; ++j) {
+          const double2 w = cmul(v[j], ((j >> s0) & 1) ? d1 : d0);
+          const bool ok = jcond(sc, j);
+          v[j].x = ok ? w.x : v[j].x;
+          v[j].y = ok ? w.y : v[j].y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kRegs; ++j) {
+          int sub = fixed_sub;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (slot[t] >= 0) sub |= ((j >> slot[t]) & 1) << t;
+          const double2 w = cmul(v[j], tab[sub]);
+          const bool ok = jcond(sc, j);
+          v[j].x = ok ? w.x : v[j].x;
+          v[j].y = ok ? w.y : v[j].y;
+        }
       }
       break;
     }
     case T_PARITY: {
-      const double2 f0 = __ldg(data + op.data), f1 = __ldg(data + op.data + 1);
-      const int gpar = __popcll(c.base & op.zg) & 1;
+      const double2 f0 = (data[op.data]), f1 = (data[op.data + 1]);
+      // parity = tile part ^ thread part ^ register part
+      int par0 = (__popcll(c.base & op.zg) ^ __popc(c.lt & op.zl)) & 1;
+      uint32_t rz = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int p = (__popc(lidx(c, j) & op.zl) ^ gpar) & 1;
+      for (int i = 0; i < kRegBits; ++i)
+        if (op.zl & c.rb[i]) rz |= 1u << i;
+#pragma unroll
+      for (int j = 0; j < kRegs; ++j) {
+        const int p = (par0 ^ __popc((uint32_t)j & rz)) & 1;
         v[j] = cmul(v[j], p ? f1 : f0);
       }
       break;
@@ -136,7 +226,7 @@ __device__ __forceinline__ void t_apply(double2 (&v)[16], const TileCtx& c, cons
 // ---- shared-memory ops: a phase of their own, all threads over cosets
 template <int K>
 __device__ __forceinline__ void s_dense(double2* sm, int L, const TileOp& op,
-                                        const double2* __restrict__ data, int tid) {
+                                        const double2* data, int tid) {
   constexpr int D = 1 << K;
   int sorted[K];
 #pragma unroll
@@ -170,9 +260,9 @@ __device__ __forceinline__ void s_dense(double2* sm, int L, const TileOp& op,
     }
 #pragma unroll
     for (int z = 0; z < D; ++z) {
-      double2 acc = cmul(__ldg(data + op.data + z * D), in[0]);
+      double2 acc = cmul((data[op.data + z * D]), in[0]);
 #pragma unroll
-      for (int w = 1; w < D; ++w) acc = cfma(__ldg(data + op.data + z * D + w), in[w], acc);
+      for (int w = 1; w < D; ++w) acc = cfma((data[op.data + z * D + w]), in[w], acc);
       uint32_t l = l0;
 #pragma unroll
       for (int j = 0; j < K; ++j)
@@ -183,10 +273,10 @@ __device__ __forceinline__ void s_dense(double2* sm, int L, const TileOp& op,
 }
 
 __device__ __forceinline__ void s_pauli(double2* sm, int L, const TileOp& op,
-                                        const double2* __restrict__ data, int tid, int gpar) {
+                                        const double2* data, int tid, int gpar) {
   const uint32_t xml = (uint32_t)op.slots;
   const int pivot = 31 - __clz(xml);
-  const double2 alpha = __ldg(data + op.data), bph = __ldg(data + op.data + 1);
+  const double2 alpha = (data[op.data]), bph = (data[op.data + 1]);
   const uint32_t np = 1u << (L - 1);
   for (uint32_t p = tid; p < np; p += kTileThreads) {
     const uint32_t lo = p & ((1u << pivot) - 1u);
@@ -203,7 +293,7 @@ __device__ __forceinline__ void s_pauli(double2* sm, int L, const TileOp& op,
 }
 
 __device__ __noinline__ void s_apply(double2* sm, int L, const TileOp& op,
-                                     const double2* __restrict__ data, uint64_t base, int tid) {
+                                     const double2* data, uint64_t base, int tid) {
   if (op.gmask && ((base & op.gmask) != op.gval)) return;
   if (op.kind == S_PAULI) {
     s_pauli(sm, L, op, data, tid, __popcll(base & op.zg) & 1);
@@ -228,12 +318,14 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// global offset of local index bits 8..11 (the loop index k of the copies)
+constexpr int kTidBits = 12 - kRegBits;  // log2(kTileThreads)
+
+// global offset of the local index bits above kTidBits (loop index k of the copies)
 __device__ __forceinline__ uint64_t hi_part(const TilePassDev* pd, int L, int k) {
   uint64_t g = 0;
 #pragma unroll
-  for (int b = 0; b < 4; ++b)
-    if (8 + b < L && ((k >> b) & 1)) g |= 1ULL << pd->spos[8 + b];
+  for (int b = 0; b < kRegBits; ++b)
+    if (kTidBits + b < L && ((k >> b) & 1)) g |= 1ULL << pd->spos[kTidBits + b];
   return g;
 }
 
@@ -242,27 +334,49 @@ __device__ __forceinline__ uint64_t hi_part(const TilePassDev* pd, int L, int k)
 // XOR-swizzled 16-byte slots) in flight while the current tile computes.
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_tile(double2* __restrict__ a, const TilePassDev* __restrict__ pd,
-           const TilePhase* __restrict__ phases, const TileOp* __restrict__ ops,
-           const double2* __restrict__ data, FixedBits tb, uint64_t ntiles) {
+           const TilePhase* __restrict__ phases, const TileOp* __restrict__ g_ops,
+           const double2* __restrict__ g_data, FixedBits tb, uint64_t ntiles, int nops,
+           int ndata) {
   extern __shared__ double2 smem_all[];
+  __shared__ uint64_t s_hi[kRegs];       // HBM offset of copy-index bits >= kTidBits
   const int L = pd->L;
   const uint32_t tile_amps = 1u << L;
   const int tid = threadIdx.x;
-  // local bits 0..7 of the copy index l = k * 256 + tid come from tid
+  const int nphases = (pd->debug & 2) ? 0 : pd->nphases;
+  const bool skip_ops = pd->debug & 1;
+  const int dbg = pd->debug;
+  // phase descriptors cached in shared memory after the two tile buffers
+  // [buf0][buf1][ops][data][phases]: the pass program is staged once per
+  // (persistent) CTA, so every op read in the tile loop is a broadcast LDS
+  TileOp* ops = reinterpret_cast<TileOp*>(smem_all + 2 * (size_t)tile_amps);
+  double2* data = reinterpret_cast<double2*>(ops + nops);
+  TilePhase* s_ph = reinterpret_cast<TilePhase*>(data + ndata);
+  {
+    const int4* src = reinterpret_cast<const int4*>(g_ops);
+    int4* dst = reinterpret_cast<int4*>(ops);
+    for (int i = tid; i < nops * (int)(sizeof(TileOp) / 16); i += kTileThreads) dst[i] = src[i];
+    for (int i = tid; i < ndata; i += kTileThreads) data[i] = g_data[i];
+    const int words = pd->nphases * (int)(sizeof(TilePhase) / 4);
+    const int* psrc = reinterpret_cast<const int*>(phases);
+    int* pdst = reinterpret_cast<int*>(s_ph);
+    for (int i = tid; i < words; i += kTileThreads) pdst[i] = psrc[i];
+    if (tid < kRegs) s_hi[tid] = hi_part(pd, L, tid);
+  }
+  // local bits below kTidBits of the copy index l = k * kTileThreads + tid
   uint64_t lo_part = 0;
-  for (int b = 0; b < 8 && b < L; ++b)
+  for (int b = 0; b < kTidBits && b < L; ++b)
     if ((tid >> b) & 1) lo_part |= 1ULL << pd->spos[b];
   const int nk = (int)((tile_amps + kTileThreads - 1) / kTileThreads);
   const bool copy_thread = (uint32_t)tid < tile_amps;
+  __syncthreads();
 
   auto issue_load = [&](uint64_t tile, double2* buf) {
-    const uint64_t base = widen(tile, tb);
+    const uint64_t base = widen(tile, tb) | lo_part;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
     if (copy_thread) {
       for (int k = 0; k < nk; ++k) {
         const uint32_t l = (uint32_t)k * kTileThreads + tid;
-        const uint64_t g = base | lo_part | hi_part(pd, L, k);
-        cp_async16(sbase + swz(l) * 16u, a + g);
+        cp_async16(sbase + swz(l) * 16u, a + (base | s_hi[k]));
       }
     }
     cp_async_commit();
@@ -282,10 +396,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     __syncthreads();
     const uint64_t base = widen(tile, tb);
 
-    for (int ph = 0; ph < pd->nphases; ++ph) {
-      const TilePhase& P = phases[ph];
+    for (int ph = 0; ph < nphases; ++ph) {
+      const TilePhase& P = s_ph[ph];
+      const int ob = P.op_begin, oe = P.op_end;
       if (P.type != 0) {
-        for (int o = P.op_begin; o < P.op_end; ++o) {
+        for (int o = ob; o < (skip_ops ? ob : oe); ++o) {
           s_apply(sm, L, ops[o], data, base, tid);
           __syncthreads();
         }
@@ -299,22 +414,45 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 #pragma unroll
       for (int i = 0; i < kRegBits; ++i) c.rb[i] = 1u << P.regpos[i];
       if (active) {
-        double2 v[16];
+        // the swizzle is XOR-linear: swz(lt | r) = swz(lt) ^ swz(r)
+        uint32_t srb[kRegBits];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = sm[swz(lidx(c, j))];
-        for (int o = P.op_begin; o < P.op_end; ++o) t_apply(v, c, ops[o], data);
+        for (int i = 0; i < kRegBits; ++i) srb[i] = swz(c.rb[i]);
+        const uint32_t slt = swz(c.lt);
+        double2 v[kRegs];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) sm[swz(lidx(c, j))] = v[j];
+        for (int j = 0; j < kRegs; ++j) {
+          uint32_t ad = slt;
+#pragma unroll
+          for (int i = 0; i < kRegBits; ++i)
+            if ((j >> i) & 1) ad ^= srb[i];
+          v[j] = sm[ad];
+        }
+        TileOp op = ops[ob];
+        for (int o = ob; o < (skip_ops ? ob : oe); ++o) {
+          const TileOp nxt = ops[o + 1 < oe ? o + 1 : o];  // prefetch
+          if (!((dbg & 4) && op.kind != T_DENSE1) && !((dbg & 8) && op.kind == T_DENSE1))
+            t_apply(v, c, op, data);
+          op = nxt;
+        }
+#pragma unroll
+        for (int j = 0; j < kRegs; ++j) {
+          uint32_t ad = slt;
+#pragma unroll
+          for (int i = 0; i < kRegBits; ++i)
+            if ((j >> i) & 1) ad ^= srb[i];
+          sm[ad] = v[j];
+        }
       }
       __syncthreads();
     }
 
     // shared -> HBM (same mapping as the load)
     if (copy_thread) {
+      const uint64_t gb = base | lo_part;
       for (int k = 0; k < nk; ++k) {
         const uint32_t l = (uint32_t)k * kTileThreads + tid;
-        const uint64_t g = base | lo_part | hi_part(pd, L, k);
-        st1(a + g, sm[swz(l)]);
+        st1(a + (gb | s_hi[k]), sm[swz(l)]);
       }
     }
     __syncthreads();  // buffer `cur` is refilled two tiles later
@@ -480,8 +618,14 @@ PassSel select_pass(int n, int L, const std::vector<GateDesc>& gates,
   ps.S = (c >= 64) ? ~0ULL : ((1ULL << c) - 1);
   uint64_t blocked = 0;
   const uint64_t all = (n >= 64) ? ~0ULL : ((1ULL << n) - 1);
+  size_t budget = kTileProgramBudget;  // staged program must fit in shared memory
   for (size_t i = first; i < gates.size(); ++i) {
     if (done[i]) continue;
+    const GateDesc& g = gates[i];
+    size_t cost = sizeof(TileOp) + sizeof(TilePhase) + 32;
+    if (g.kind == QSV_OP_DENSE) cost += sizeof(double2) << (2 * g.m);
+    if (g.kind == QSV_OP_DIAG) cost += sizeof(double2) << g.m;
+    if (cost > budget) break;
     const uint64_t T = touched_mask(gates[i]);
     if (!ok[i] || (T & blocked)) {
       blocked |= T;
@@ -491,9 +635,11 @@ PassSel select_pass(int n, int L, const std::vector<GateDesc>& gates,
     const uint64_t A = act[i];
     if ((A & ~ps.S) == 0) {
       ps.taken.push_back((int)i);
+      budget -= cost;
     } else if (popc64(ps.S | A) <= L) {
       ps.S |= A;
       ps.taken.push_back((int)i);
+      budget -= cost;
     } else {
       blocked |= T;
       if ((blocked & all) == all) break;
@@ -704,6 +850,7 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
   }
   close();
   e.pd.nphases = (int)e.phases.size();
+  if (const char* dbg = getenv("QSV_TILE_DEBUG")) e.pd.debug = atoi(dbg);
   return e;
 }
 
@@ -772,6 +919,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       if ((ps.S >> q) & 1ULL) tp.qubits.push_back(q);
     tp.nphases = (int)e.phases.size();
     tp.nops = (int)e.ops.size();
+    tp.ndata = (int)e.data.size();
     tp.num_gates = (int)pg.size();
     tp.hbm_bytes = 32.0 * std::ldexp(1.0, n);
     // payload: [TilePassDev][phases][ops][data]
@@ -811,20 +959,27 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
   int pos[kMaxTileQubits];
   for (int j = 0; j < tp.L; ++j) pos[j] = tp.qubits[j];
   FixedBits tb = make_fixed(pos, tp.L, 0);
-  const size_t smem = 2 * (sizeof(double2) << tp.L);
+  const size_t smem = 2 * (sizeof(double2) << tp.L) + tp.nops * sizeof(TileOp) +
+                      tp.ndata * sizeof(double2) + tp.nphases * sizeof(TilePhase);
+  if (smem > kTileSmemLimit) {
+    set_error("tile pass program (%d ops, %d phases) does not fit in shared memory", tp.nops,
+              tp.nphases);
+    return QSV_EUNSUPPORTED;
+  }
   static int attr_dev = -1;
   static int num_sms = 148;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(2 * (sizeof(double2) << kMaxTileQubits)));
+    QSV_TRY(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kTileSmemLimit));
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     attr_dev = dev;
   }
   const uint64_t ntiles = 1ULL << (n - tp.L);
   const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms);
-  k_tile<<<grid, kTileThreads, smem, s>>>(amps, pd, ph, ops, data, tb, ntiles);
+  k_tile<<<grid, kTileThreads, smem, s>>>(amps, pd, ph, ops, data, tb, ntiles, tp.nops,
+                                          tp.ndata);
   QSV_CHECK_LAUNCH("k_tile");
   return QSV_OK;
 }

@@ -8,10 +8,17 @@
 
 namespace qsv {
 
-constexpr int kTileThreads = 256;   // threads per tile CTA
-constexpr int kRegBits = 4;         // amplitudes per thread = 2^kRegBits
+#ifndef QSV_TILE_REGBITS
+#define QSV_TILE_REGBITS 4
+#endif
+constexpr int kRegBits = QSV_TILE_REGBITS;  // amplitudes per thread = 2^kRegBits
+constexpr int kRegs = 1 << kRegBits;
+constexpr int kTileThreads = 4096 / kRegs;  // threads per tile CTA (2^12 amps)
 constexpr int kMaxTileQubits = 12;  // 2^12 amps = 64 KiB of shared memory
 constexpr int kLowQubits = 4;       // qubits 0..3 are in every tile (256 B runs)
+constexpr int kTileSmemLimit = 227 * 1024 - 1024;  // dynamic part (static smem aside)
+// shared memory left for the staged pass program (ops, data, phases)
+constexpr int kTileProgramBudget = kTileSmemLimit - 2 * (16 << kMaxTileQubits) - 1024;
 
 // ---- device-side program records (all POD, stored in the payload) ----
 enum TileOpKind : int32_t {
@@ -25,37 +32,36 @@ enum TileOpKind : int32_t {
   S_PAULI = 10,   // X/Y product on local bits (slots = local X mask), Z parity
 };
 
-struct TileOp {
+struct __align__(16) TileOp {   // 64 bytes = 4 x 128-bit loads
   int32_t kind;
   int32_t slots;      // T_DENSE1: slot mask (bit i = register slot i)
                       // S_PAULI: X/Y mask over local bits
-  int32_t flags;      // bit 0: DENSE1 matrix is X (swap, no flops)
+  int32_t flags;      // bit 1: T_PHASE factor is -1 (sign flip)
   int32_t m;          // DIAG / S_DENSE: number of targets
   uint32_t lmask;     // control pattern over local bits
   uint32_t lval;
+  uint32_t zl;        // PARITY/PAULI: sign mask over local bits
+  uint32_t data;      // payload offset (double2 units) of matrix / table / coefs
   uint64_t gmask;     // control pattern over global (non-tile) bits
   uint64_t gval;
-  uint32_t zl;        // PARITY/PAULI: sign mask over local bits
-  uint32_t pad0;
   uint64_t zg;        // PARITY/PAULI: sign mask over global bits
-  int32_t tpos[4];    // DIAG: target position; >= 0 local bit, < 0: -(global bit)-1
+  int8_t tpos[4];     // DIAG: target position; >= 0 local bit, < 0: -(global bit)-1
                       // S_DENSE: local bit of matrix index bit j
-  uint32_t data;      // payload offset (double2 units) of matrix / table / coefs
-  uint32_t pad1;
+  int32_t pad;
 };
 
 struct TilePhase {
   int32_t type;              // 0: register phase, 1: shared-memory ops
   int32_t regpos[kRegBits];  // local bit of each register slot
-  int32_t thrpos[8];         // local bit of thread-id bit j (j < L - kRegBits)
+  int32_t thrpos[10];        // local bit of thread-id bit j (j < L - kRegBits)
   int32_t op_begin, op_end;
 };
 
 struct TilePassDev {
   int32_t L;
-  int32_t nthrbits;          // L - kRegBits (<= 8)
+  int32_t nthrbits;          // L - kRegBits
   int32_t nphases;
-  int32_t pad;
+  int32_t debug;             // profiling knobs (QSV_TILE_DEBUG): 1 skip ops, 2 skip phases
   uint64_t smask;            // tile qubits (global positions)
   int32_t spos[kMaxTileQubits];  // local bit j -> global qubit
 };
@@ -67,6 +73,7 @@ struct TilePlan {
   size_t dev_off = 0;            // payload offset of TilePassDev, then phases, ops
   int nphases = 0;
   int nops = 0;
+  int ndata = 0;
   int num_gates = 0;
   double hbm_bytes = 0;
 };
