@@ -1,0 +1,509 @@
+"""Sharded state vector across the GPUs of one node.
+
+The reference is single-process; this module is the B200
+extension the north star asks for.  With P = 2^p ranks the 2^n amplitudes
+are split by the top p *physical* qubits: rank r holds the 2^L amplitudes
+(L = n - p) whose physical global bits equal r.  A logical->physical qubit
+map is kept on the host and is never undone eagerly.
+
+* Gates whose non-diagonal targets are local need no communication.
+  Controls on global qubits become a per-rank predicate; diagonal factors
+  and Pauli-Z signs on global qubits become per-rank constants.  Runs of such
+  gates are compiled per rank into one libqsv program (fused + tiled).
+* A non-diagonal target on a global qubit triggers a global<->local swap:
+  rank r and its partner r ^ 2^(g-L) exchange the half of their shard whose
+  local bit l differs from r's bit g (16 * 2^(L-1) bytes each way), in chunks
+  through a staging buffer with NCCL send/recv over NVLink
+  (torch.distributed).  The victim local qubit is the one whose next
+  non-diagonal use is furthest away (Belady), preferring high positions so
+  the exchanged half is contiguous.
+* Reductions (norm, expectation) are local partial sums + all_reduce.
+
+The engine is SPMD over the shards a process owns: normally one (its rank),
+but a process may own several "virtual ranks" (exchanges then become local
+copies), which is how the single-GPU tests exercise every code path.  The
+shard backend is pluggable: ``CudaShard`` (libqsv) is the product; the CPU
+gloo tests plug the oracle in (tests/test_dist_gloo.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib
+from ._circuit import default_plan_opts
+from ._lib import check, lib
+
+
+# --------------------------------------------------------------------- records
+def _bit(x, q):
+    return (x >> q) & 1
+
+
+def specialize(rec, phys, L, rank):
+    """Map a logical gate record onto rank ``rank``'s local shard.
+
+    ``phys[q]`` is the physical position of logical qubit q.  Returns a
+    local record (targets/controls < L) or None when the gate does nothing
+    on this rank.  Raises if a non-diagonal target is global (the planner
+    swaps first)."""
+    kind = rec[0]
+    gbit = lambda p: (rank >> (p - L)) & 1  # noqa: E731
+
+    def ctl_local(ctl):
+        out = []
+        for q, v in ctl:
+            p = phys[q]
+            if p >= L:
+                if gbit(p) != v:
+                    return None
+            else:
+                out.append((p, v))
+        return tuple(out)
+
+    if kind == "dense":
+        _, t, mat, ctl = rec
+        pt = [phys[q] for q in t]
+        if any(p >= L for p in pt):
+            raise ValueError("dense target on a global qubit")
+        c = ctl_local(ctl)
+        if c is None:
+            return None
+        return ("dense", tuple(pt), mat, c)
+    if kind == "diag":
+        _, t, d, ctl = rec
+        c = ctl_local(ctl)
+        if c is None:
+            return None
+        d = np.asarray(d, dtype=np.complex128)
+        keep = [j for j, q in enumerate(t) if phys[q] < L]
+        fixed = 0
+        for j, q in enumerate(t):
+            if phys[q] >= L:
+                fixed |= gbit(phys[q]) << j
+        sub = np.empty(1 << len(keep), dtype=np.complex128)
+        for z in range(1 << len(keep)):
+            idx = fixed
+            for i, j in enumerate(keep):
+                idx |= ((z >> i) & 1) << j
+            sub[z] = d[idx]
+        return ("diag", tuple(phys[t[j]] for j in keep), sub, c)
+    if kind in ("pauli", "pauli_rot"):
+        t, ids = rec[1], rec[2]
+        ctl = rec[-1]
+        if ctl:
+            # controlled Paulis / rotations act through their dense matrix
+            from ._gates import pauli_product_matrix
+            if kind == "pauli":
+                mat = pauli_product_matrix(ids)
+            else:
+                ang = rec[3]
+                mat = (math.cos(ang / 2) * np.eye(1 << len(t))
+                       + 1j * math.sin(ang / 2) * pauli_product_matrix(ids))
+            return specialize(("dense", t, mat, ctl), phys, L, rank)
+        lt, lids = [], []
+        sign = 1
+        for q, a in zip(t, ids):
+            p = phys[q]
+            if p >= L:
+                if a in (1, 2):
+                    raise ValueError("Pauli X/Y on a global qubit")
+                if a == 3 and gbit(p):
+                    sign = -sign
+            else:
+                lt.append(p)
+                lids.append(a)
+        if kind == "pauli":
+            if not lt:
+                return ("diag", (), np.array([sign], dtype=np.complex128), ())
+            rec2 = ("pauli", tuple(lt), tuple(lids), ())
+            if sign < 0:
+                return [rec2, ("diag", (), np.array([-1.0 + 0j]), ())]
+            return rec2
+        ang = rec[3]
+        # exp(i a s P_local / 2) with s the global Z sign
+        if not lt:
+            ph = complex(math.cos(ang / 2), sign * math.sin(ang / 2))
+            return ("diag", (), np.array([ph], dtype=np.complex128), ())
+        return ("pauli_rot", tuple(lt), tuple(lids), sign * ang, ())
+    raise ValueError(kind)
+
+
+def active_qubits(rec):
+    """Logical qubits that must be local for the record to run."""
+    kind = rec[0]
+    if kind == "dense":
+        return set(rec[1])
+    if kind == "diag":
+        return set()
+    ids = rec[2]
+    if rec[-1]:  # controlled Pauli/rotation -> dense on all targets
+        return set(rec[1])
+    return {q for q, a in zip(rec[1], ids) if a in (1, 2)}
+
+
+def records_to_ops(records):
+    """Neutral records -> (qsv_op array, keep-alive list)."""
+    ops = (_lib.QsvOp * max(1, len(records)))()
+    keep = []
+    for i, rec in enumerate(records):
+        op = ops[i]
+        kind = rec[0]
+        if kind == "dense":
+            _, t, mat, ctl = rec
+            m = np.ascontiguousarray(mat, dtype=np.complex128)
+            keep.append(m)
+            op.kind, op.data = _lib.OP_DENSE, m.ctypes.data
+        elif kind == "diag":
+            _, t, d, ctl = rec
+            d = np.ascontiguousarray(d, dtype=np.complex128)
+            keep.append(d)
+            op.kind, op.data = _lib.OP_DIAG, d.ctypes.data
+        elif kind == "pauli":
+            _, t, ids, ctl = rec
+            op.kind, op.data = _lib.OP_PAULI, None
+        else:
+            _, t, ids, ang, ctl = rec
+            op.kind, op.data, op.angle = _lib.OP_PAULI_ROT, None, float(ang)
+        op.m = len(t)
+        for j, q in enumerate(t):
+            op.targets[j] = q
+        if kind in ("pauli", "pauli_rot"):
+            for j, a in enumerate(rec[2]):
+                op.ids[j] = a
+        op.nc = len(ctl)
+        for j, (q, v) in enumerate(ctl):
+            op.control_qubits[j] = q
+            op.control_values[j] = v
+    return ops, keep
+
+
+# --------------------------------------------------------------------- backends
+class CudaShard:
+    """A shard held by libqsv on one GPU (the product backend)."""
+
+    def __init__(self, L, device=0, stream_ptr=None):
+        from ._state import StateVector
+        self.L = L
+        self.state = StateVector(L, device=device)
+        if stream_ptr is not None:
+            self.state.set_stream(stream_ptr)
+        self._plan = default_plan_opts(use_graph=0)
+
+    def set_zero(self, one: bool):
+        if one:
+            self.state.set_zero_state()
+        else:
+            self.state.set_zero_state()
+            self.state.multiply_coef(0.0)
+
+    def set_basis(self, local_index):
+        self.state.set_computational_basis(local_index)
+
+    def set_random(self, seed):
+        self.state.set_random_state_device(seed)
+
+    def load(self, arr):
+        self.state.load(arr)
+
+    def get(self):
+        return self.state.get_vector()
+
+    def apply_records(self, records):
+        if not records:
+            return
+        ops, keep = records_to_ops(records)
+        h = C.c_void_p()
+        check(lib.qsv_program_create(self.L, ops, len(records), C.byref(self._plan), C.byref(h)))
+        try:
+            check(lib.qsv_program_run(h, self.state._handle()))
+        finally:
+            lib.qsv_program_destroy(h)
+
+    def norm2(self):
+        return self.state.get_squared_norm()
+
+    def scale(self, f):
+        self.state.multiply_coef(f)
+
+    def expect_terms(self, terms):
+        """terms: list of (coef, [(local qubit, axis)...]) -> complex partial."""
+        from ._observable import GeneralOperator, PauliProduct
+        op = GeneralOperator(self.L)
+        for coef, ops in terms:
+            op.add_operator(PauliProduct(ops, coef))
+        return op._accumulate(self.state, self.state)
+
+    def tensor(self):
+        """torch float64 view (2 * 2^L) aliasing the device shard."""
+        import torch
+        ptr = C.c_void_p()
+        check(lib.qsv_state_device_ptr(self.state._handle(), C.byref(ptr)))
+
+        class _Iface:
+            __cuda_array_interface__ = {
+                "shape": (2 << self.L,), "typestr": "<f8", "data": (ptr.value, False),
+                "version": 2, "strides": None}
+        return torch.as_tensor(_Iface(), device=f"cuda:{self.state.get_device()}")
+
+    def sync(self):
+        self.state.synchronize()
+
+
+# --------------------------------------------------------------------- engine
+class ShardedQuantumState:
+    """2^n amplitudes over P = 2^p shards (see module docstring).
+
+    ``owned``: list of ranks this process simulates (default: its own rank);
+    ``backend``: callable (L, rank) -> shard backend (default CudaShard)."""
+
+    def __init__(self, num_qubits, world=None, rank=None, owned=None, backend=None,
+                 group=None, chunk_bytes=1 << 30):
+        import torch.distributed as dist
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        if world is None:
+            world = self.dist.get_world_size(group) if self.dist else 1
+        if rank is None:
+            rank = self.dist.get_rank(group) if self.dist else 0
+        p = int(round(math.log2(world)))
+        if 1 << p != world:
+            raise ValueError("the number of shards must be a power of two")
+        if num_qubits - p < 1:
+            raise ValueError("too few qubits for this many shards")
+        self.n, self.p, self.L = num_qubits, p, num_qubits - p
+        self.world, self.group = world, group
+        self.owned = list(owned) if owned is not None else [rank]
+        self.chunk_bytes = int(chunk_bytes)
+        if backend is None:
+            import torch
+            dev = torch.cuda.current_device()
+            stream = torch.cuda.current_stream().cuda_stream
+            backend = lambda L, r: CudaShard(L, dev, stream)  # noqa: E731
+        self.shards = {r: backend(self.L, r) for r in self.owned}
+        self.phys = list(range(num_qubits))  # logical -> physical
+        self.stats = {"swaps": 0, "bytes_sent": 0, "segments": 0}
+        self.set_zero_state()
+
+    # -- helpers ------------------------------------------------------------
+    def _logical_of(self):
+        inv = [0] * self.n
+        for q, p in enumerate(self.phys):
+            inv[p] = q
+        return inv
+
+    def _allreduce(self, value: complex) -> complex:
+        if self.dist is None or len(self.owned) == self.world:
+            return value
+        import torch
+        dev = "cpu"
+        if self.dist.get_backend(self.group) == "nccl":
+            dev = f"cuda:{torch.cuda.current_device()}"
+        t = torch.tensor([value.real, value.imag], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, group=self.group)
+        return complex(float(t[0]), float(t[1]))
+
+    # -- state setup ----------------------------------------------------------
+    def set_zero_state(self):
+        self.phys = list(range(self.n))
+        for r, s in self.shards.items():
+            s.set_zero(r == 0)
+
+    def set_computational_basis(self, index):
+        if not 0 <= index < (1 << self.n):
+            raise ValueError("basis index out of range")
+        ph = 0
+        for q in range(self.n):
+            ph |= ((index >> q) & 1) << self.phys[q]
+        for r, s in self.shards.items():
+            if (ph >> self.L) == r:
+                s.set_basis(ph & ((1 << self.L) - 1))
+            else:
+                s.set_zero(False)
+
+    def load(self, vec):
+        """Scatter a full logical vector (every process passes the same)."""
+        vec = np.asarray(vec, dtype=np.complex128)
+        idx = np.arange(1 << self.n)
+        ph = np.zeros_like(idx)
+        for q in range(self.n):
+            ph |= ((idx >> q) & 1) << self.phys[q]
+        full = np.empty_like(vec)
+        full[ph] = vec
+        for r, s in self.shards.items():
+            s.load(full[r << self.L:(r + 1) << self.L])
+
+    def get_vector(self):
+        """Gather the full logical vector on every process (small n only)."""
+        part = {r: s.get() for r, s in self.shards.items()}
+        if self.dist is not None and len(self.owned) < self.world:
+            objs = [None] * self.world
+            self.dist.all_gather_object(objs, part, group=self.group)
+            for o in objs:
+                part.update(o)
+        full = np.concatenate([part[r] for r in range(self.world)])
+        idx = np.arange(1 << self.n)
+        ph = np.zeros_like(idx)
+        for q in range(self.n):
+            ph |= ((idx >> q) & 1) << self.phys[q]
+        return full[ph]
+
+    def get_squared_norm(self) -> float:
+        return self._allreduce(complex(sum(s.norm2() for s in self.shards.values()))).real
+
+    # -- gates ----------------------------------------------------------------
+    def plan(self, records):
+        """Split records into segments of local gates and swap lists.
+
+        Returns a list of ("swap", g_phys, l_phys) / ("seg", [records]) and
+        updates nothing (pure function of the current map)."""
+        phys = list(self.phys)
+        L = self.L
+        steps = []
+        seg = []
+        act = [active_qubits(r) for r in records]
+
+        def next_use(q, start):
+            for k in range(start, len(records)):
+                if q in act[k]:
+                    return k
+            return len(records) + (self.n - phys[q])  # never: prefer high phys
+
+        for i, rec in enumerate(records):
+            need = [q for q in act[i] if phys[q] >= L]
+            if need:
+                if seg:
+                    steps.append(("seg", seg))
+                    seg = []
+                busy = set(act[i])
+                for q in need:
+                    cands = [lq for lq in range(self.n) if phys[lq] < L and lq not in busy]
+                    if not cands:
+                        raise ValueError("gate needs more local qubits than the shard has")
+                    victim = max(cands, key=lambda lq: (next_use(lq, i + 1), phys[lq]))
+                    g, l = phys[q], phys[victim]
+                    steps.append(("swap", g, l))
+                    phys[q], phys[victim] = l, g
+                    busy.add(victim)
+            seg.append(rec)
+        if seg:
+            steps.append(("seg", seg))
+        return steps
+
+    def apply_records(self, records):
+        for step in self.plan(records):
+            if step[0] == "swap":
+                self._swap(step[1], step[2])
+            else:
+                self.stats["segments"] += 1
+                for r, s in self.shards.items():
+                    local = []
+                    for rec in step[1]:
+                        out = specialize(rec, self.phys, self.L, r)
+                        if out is None:
+                            continue
+                        if isinstance(out, list):
+                            local.extend(out)
+                        else:
+                            local.append(out)
+                    s.apply_records(local)
+
+    def update_quantum_state(self, circuit):
+        from ._circuit import circuit_records
+        self.apply_records(circuit_records(circuit))
+
+    def expectation(self, terms) -> complex:
+        """terms: (coef, [(logical qubit, axis)...]); X/Y factors on global
+        qubits are brought local by swaps first."""
+        need = set()
+        for _, ops in terms:
+            need |= {q for q, a in ops if a in (1, 2)}
+        if any(self.phys[q] >= self.L for q in need):
+            if len(need) > self.L:
+                raise ValueError("X/Y factors on more qubits than a shard holds")
+            # one placeholder touching every X/Y qubit: all become local together
+            recs = [("dense", tuple(sorted(need)), None, ())]
+            for step in self.plan(recs):
+                if step[0] == "swap":
+                    self._swap(step[1], step[2])
+        total = 0j
+        for r, s in self.shards.items():
+            loc = []
+            for coef, ops in terms:
+                sign = 1
+                lops = []
+                for q, a in ops:
+                    p = self.phys[q]
+                    if p >= self.L:
+                        if a != 3:
+                            raise AssertionError("X/Y factor left on a global qubit")
+                        if (r >> (p - self.L)) & 1:
+                            sign = -sign
+                    else:
+                        lops.append((p, a))
+                loc.append((coef * sign, lops))
+            total += s.expect_terms(loc)
+        return self._allreduce(total)
+
+    # -- the exchange ---------------------------------------------------------
+    def _swap(self, g, l):
+        """Exchange physical global qubit g with local qubit l."""
+        L = self.L
+        step = 1 << (g - L)
+        done = set()
+        for r in self.owned:
+            if r in done:
+                continue
+            partner = r ^ step
+            b = (r >> (g - L)) & 1
+            mine = self._half_view(r, l, 1 - b)
+            if partner in self.shards:
+                theirs = self._half_view(partner, l, b)
+                tmp = mine.clone()
+                mine.copy_(theirs)
+                theirs.copy_(tmp)
+                done.add(partner)
+            else:
+                self._exchange(mine, partner)
+            done.add(r)
+            self.stats["bytes_sent"] += 16 << (L - 1)
+        # logical map: whoever sat at g now sits at l and vice versa
+        inv = self._logical_of()
+        qg, ql = inv[g], inv[l]
+        self.phys[qg], self.phys[ql] = l, g
+        self.stats["swaps"] += 1
+
+    def _half_view(self, r, l, v):
+        """Float64 view of shard r restricted to local bit l == v, shaped
+        (outer, 2^l * 2) (complex as float pairs)."""
+        t = self.shards[r].tensor()
+        L = self.L
+        return t.view(1 << (L - 1 - l), 2, 2 << l)[:, v, :]
+
+    def _exchange(self, view, partner):
+        """Send ``view`` to partner and overwrite it with the partner's data,
+        chunked through staging buffers."""
+        import torch
+        dist = self.dist
+        outer, inner = view.shape
+        row = inner * 8
+        rows = max(1, self.chunk_bytes // max(row, 1))
+        if rows >= outer:
+            chunks = [(0, outer, None)]
+        else:
+            chunks = [(a, min(a + rows, outer), None) for a in range(0, outer, rows)]
+        if inner * 8 > self.chunk_bytes and outer == 1:
+            # contiguous half larger than a chunk: split the inner axis
+            cols = self.chunk_bytes // 8
+            chunks = [(0, 1, (c, min(c + cols, inner))) for c in range(0, inner, cols)]
+        for a, b, cols in chunks:
+            part = view[a:b] if cols is None else view[a:b, cols[0]:cols[1]]
+            send = part.contiguous() if not part.is_contiguous() else part.clone()
+            recv = torch.empty_like(send)
+            ops = [dist.P2POp(dist.isend, send, partner, group=self.group),
+                   dist.P2POp(dist.irecv, recv, partner, group=self.group)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            part.copy_(recv)
