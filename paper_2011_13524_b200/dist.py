@@ -185,13 +185,14 @@ def records_to_ops(records):
 class CudaShard:
     """A shard held by libqsv on one GPU (the product backend)."""
 
-    def __init__(self, L, device=0, stream_ptr=None):
+    def __init__(self, L, device=0, stream_ptr=None, **plan):
         from ._state import StateVector
         self.L = L
         self.state = StateVector(L, device=device)
         if stream_ptr is not None:
             self.state.set_stream(stream_ptr)
-        self._plan = default_plan_opts(use_graph=0)
+        plan.setdefault("use_graph", 0)
+        self._plan = default_plan_opts(**plan)
 
     def set_zero(self, one: bool):
         if one:
@@ -215,6 +216,10 @@ class CudaShard:
     def apply_records(self, records):
         if not records:
             return
+        if not self._plan.use_tiles and not self._plan.fuse:
+            for rec in records:  # per-gate mode: one kernel per gate, no program
+                self._apply_direct(rec)
+            return
         ops, keep = records_to_ops(records)
         h = C.c_void_p()
         check(lib.qsv_program_create(self.L, ops, len(records), C.byref(self._plan), C.byref(h)))
@@ -222,6 +227,25 @@ class CudaShard:
             check(lib.qsv_program_run(h, self.state._handle()))
         finally:
             lib.qsv_program_destroy(h)
+
+    def _apply_direct(self, rec):
+        from ._lib import int_array
+        h = self.state._handle()
+        kind = rec[0]
+        ctl = rec[-1]
+        cq, cv = int_array(q for q, _ in ctl), int_array(v for _, v in ctl)
+        t = int_array(rec[1])
+        if kind == "dense":
+            m = np.ascontiguousarray(rec[2], dtype=np.complex128)
+            check(lib.qsv_apply_dense(h, t, len(rec[1]), m.ctypes.data, cq, cv, len(ctl)))
+        elif kind == "diag":
+            d = np.ascontiguousarray(rec[2], dtype=np.complex128)
+            check(lib.qsv_apply_diag(h, t, len(rec[1]), d.ctypes.data, cq, cv, len(ctl)))
+        elif kind == "pauli":
+            check(lib.qsv_apply_pauli(h, t, int_array(rec[2]), len(rec[1]), cq, cv, len(ctl)))
+        else:
+            check(lib.qsv_apply_pauli_rot(h, t, int_array(rec[2]), len(rec[1]),
+                                          C.c_double(rec[3]), cq, cv, len(ctl)))
 
     def norm2(self):
         return self.state.get_squared_norm()
@@ -261,7 +285,7 @@ class ShardedQuantumState:
     ``backend``: callable (L, rank) -> shard backend (default CudaShard)."""
 
     def __init__(self, num_qubits, world=None, rank=None, owned=None, backend=None,
-                 group=None, chunk_bytes=1 << 30):
+                 group=None, chunk_bytes=1 << 30, plan=None):
         import torch.distributed as dist
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
         if world is None:
@@ -281,7 +305,8 @@ class ShardedQuantumState:
             import torch
             dev = torch.cuda.current_device()
             stream = torch.cuda.current_stream().cuda_stream
-            backend = lambda L, r: CudaShard(L, dev, stream)  # noqa: E731
+            plan = dict(plan or {})
+            backend = lambda L, r: CudaShard(L, dev, stream, **plan)  # noqa: E731
         self.shards = {r: backend(self.L, r) for r in self.owned}
         self.phys = list(range(num_qubits))  # logical -> physical
         self.stats = {"swaps": 0, "bytes_sent": 0, "segments": 0}

@@ -43,3 +43,18 @@ def test_cuda_sharded_cz_ladder():
     st.apply_records(recs)
     ref = c_oracle.run_records(orc.zero_state(n), n, recs)
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+
+
+def test_cuda_sharded_per_gate_mode():
+    """Per-gate mode (the sharded benchmark path): direct ABI calls, no programs."""
+    import torch
+    stream = torch.cuda.current_stream().cuda_stream
+    n, world = 12, 4
+    recs = random_records(n, 60, seed=9)
+    st = ShardedQuantumState(n, world=world, owned=list(range(world)),
+                             backend=lambda L, r: CudaShard(L, 0, stream, use_tiles=0, fuse=0))
+    st.load(orc.haar_state(n, 2))
+    for r in recs:
+        st.apply_records([r])
+    ref = c_oracle.run_records(orc.haar_state(n, 2), n, recs)
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
