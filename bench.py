@@ -331,6 +331,8 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     if rank == 0 and not args.skip_circuit:
         extra["random_circuit"] = run_random_circuit(args, dev, stream, qs, workloads, torch)
+        extra["cfg1_cnot_ring"] = run_cfg1(qs, workloads, torch, dev, stream)
+        extra["cfg3_vqe"] = run_cfg3(qs, workloads, torch, dev, stream)
         del st
         torch.cuda.empty_cache()
     if rank == 0 and not args.skip_cpu:
@@ -497,6 +499,61 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
            "hbm_gbs_effective": stats.get("hbm_bytes", 0.0) / best / 1e9}
     del st
     return out
+
+
+def run_cfg1(qs, workloads, torch, dev, stream, n=16, reps=20):
+    """cfg1: cnot-ring(16) from |0> through the public API (reference
+    time_circuit semantics: fresh zero state, wall clock around
+    update_quantum_state, min of repeats), plus device time per run."""
+    circ = workloads.generate_cnot_ring(n, seed=1)
+    st = qs.QuantumState(n, device=dev)
+    st.set_stream(stream.cuda_stream)
+    circ.update_quantum_state(st)  # compile + graph capture
+    torch.cuda.synchronize(dev)
+    walls, devs = [], []
+    for _ in range(reps):
+        st.set_zero_state()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(stream)
+        circ.update_quantum_state(st)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        walls.append(time.perf_counter() - t0)
+        devs.append(a.elapsed_time(b) / 1e3)
+    return {"metric": "random-circuit sec/layer", "unit": "s/layer",
+            "workload": f"cnot-ring n={n} seed=1 ({circ.get_gate_count()} gates, 11 layers)",
+            "value": min(walls) / 11, "circuit_wall_s_best": min(walls),
+            "circuit_device_s_best": min(devs), "program": circ.program_stats()}
+
+
+def run_cfg3(qs, workloads, torch, dev, stream, n=24, reps=5):
+    """cfg3: 24-qubit VQE ansatz (4 layers RY/RZ + CNOT ladder, 284 gates)
+    from |0> then the 47-term TFIM expectation; wall clock, min of repeats."""
+    circ = workloads.vqe_ansatz(n)
+    obs = workloads.tfim_observable(n)
+    st = qs.QuantumState(n, device=dev)
+    st.set_stream(stream.cuda_stream)
+    circ.update_quantum_state(st)
+    value = obs.get_expectation_value(st)
+    t_circ, t_exp = [], []
+    for _ in range(reps):
+        st.set_zero_state()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        circ.update_quantum_state(st)
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        v = obs.get_expectation_value(st)
+        t2 = time.perf_counter()
+        t_circ.append(t1 - t0)
+        t_exp.append(t2 - t1)
+    return {"workload": f"VQE ansatz n={n} (284 gates) + TFIM ({obs.get_term_count()} terms)",
+            "energy": v, "energy_reference": -0.201996915076406,
+            "ansatz_s_best": min(t_circ), "expectation_s_best": min(t_exp),
+            "total_s_best": min(a + b for a, b in zip(t_circ, t_exp)),
+            "program": circ.program_stats()}
 
 
 def main():

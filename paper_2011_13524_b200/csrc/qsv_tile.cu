@@ -140,6 +140,17 @@ __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, c
         case 8: t_dense1<3 % kRegBits>(v, c, op, data); break;
       }
       break;
+    case T_DENSE1X4: {
+      const double2* M = data + op.data;
+      {
+        const SplitCond sc{true, 0, 0};
+        t_dense1_body<0, false>(v, sc, M[0], M[1], M[2], M[3]);
+        t_dense1_body<1 % kRegBits, false>(v, sc, M[4], M[5], M[6], M[7]);
+        t_dense1_body<2 % kRegBits, false>(v, sc, M[8], M[9], M[10], M[11]);
+        t_dense1_body<3 % kRegBits, false>(v, sc, M[12], M[13], M[14], M[15]);
+      }
+      break;
+    }
     case T_PHASE: {
       const SplitCond sc = split_cond(c, op.lmask, op.lval);
       if (!sc.t_ok) break;
@@ -704,25 +715,60 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
   std::vector<std::pair<size_t, int>> d1;  // (op index, local bit) of T_DENSE1 ops
   auto close = [&]() {
     if (!open) return;
-    for (int b = L - 1; b >= 0 && __builtin_popcount(R) < kRegBits; --b) R |= 1u << b;
+    // register slots in order of first use by a 1-qubit dense op, so runs of
+    // kRegBits such ops land on slots 0,1,2,3 and can be batched
+    std::vector<int> order;
+    for (auto& pr : d1)
+      if (std::find(order.begin(), order.end(), pr.second) == order.end())
+        order.push_back(pr.second);
+    for (int b = 0; b < L; ++b)
+      if (((R >> b) & 1u) && std::find(order.begin(), order.end(), b) == order.end())
+        order.push_back(b);
+    for (int b = L - 1; b >= 0 && (int)order.size() < kRegBits; --b)
+      if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
+    uint32_t Rall = 0;
+    for (int b : order) Rall |= 1u << b;
     TilePhase ph;
     memset(&ph, 0, sizeof(ph));
     ph.type = 0;
     int slot_of[32];
     for (int b = 0; b < 32; ++b) slot_of[b] = -1;
-    int sidx = 0;
-    std::vector<int> tb;
-    for (int b = 0; b < L; ++b) {
-      if ((R >> b) & 1u) {
-        ph.regpos[sidx] = b;
-        slot_of[b] = sidx++;
-      } else {
-        tb.push_back(b);
-      }
+    for (int i = 0; i < kRegBits; ++i) {
+      ph.regpos[i] = order[i];
+      slot_of[order[i]] = i;
     }
+    std::vector<int> tb;
+    for (int b = 0; b < L; ++b)
+      if (!((Rall >> b) & 1u)) tb.push_back(b);
     order_thread_bits(tb);
     for (size_t k = 0; k < tb.size(); ++k) ph.thrpos[k] = tb[k];
     for (auto& pr : d1) e.ops[pr.first].slots = 1 << slot_of[pr.second];
+    // batch runs of kRegBits uncontrolled 1-qubit dense ops on slots 0..3
+    if (kRegBits == 4) {
+      std::vector<TileOp> merged;
+      const size_t end = e.ops.size();
+      size_t k = op_begin;
+      while (k < end) {
+        bool run = k + 4 <= end;
+        for (int q = 0; run && q < 4; ++q) {
+          const TileOp& o = e.ops[k + q];
+          run = o.kind == T_DENSE1 && o.slots == (1 << q) && o.lmask == 0 && o.gmask == 0 &&
+                o.data == e.ops[k].data + 4 * q;
+        }
+        if (run) {
+          TileOp b = e.ops[k];
+          b.kind = T_DENSE1X4;
+          b.slots = 15;
+          merged.push_back(b);
+          k += 4;
+        } else {
+          merged.push_back(e.ops[k]);
+          ++k;
+        }
+      }
+      e.ops.resize(op_begin);
+      e.ops.insert(e.ops.end(), merged.begin(), merged.end());
+    }
     ph.op_begin = (int)op_begin;
     ph.op_end = (int)e.ops.size();
     e.phases.push_back(ph);

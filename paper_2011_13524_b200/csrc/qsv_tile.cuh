@@ -27,6 +27,7 @@ enum TileOpKind : int32_t {
   T_DIAG = 5,     // diagonal, targets on local or tile (global) bits
   T_PHASE = 6,    // constant phase on a local/tile bit pattern
   T_PARITY = 7,   // f[parity(idx & zmask)]
+  T_DENSE1X4 = 8, // four uncontrolled 2x2 on slots 0,1,2,3 in order (data: 16 entries)
   // shared-memory ops (a phase of their own; cosets read straight from smem)
   S_DENSE = 9,    // 2^m x 2^m on m <= 4 local bits (tpos), optionally controlled
   S_PAULI = 10,   // X/Y product on local bits (slots = local X mask), Z parity
