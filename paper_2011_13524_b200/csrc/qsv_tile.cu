@@ -13,6 +13,8 @@
 // amplitudes whose local indices differ in kRegBits register bits, so every
 // gate acting on register bits is pure register arithmetic; a phase boundary
 // is one shared-memory round trip (XOR-swizzled, bank-conflict free).
+// A CTA holds kGroups independent tile groups with their own named barriers,
+// so one group's HBM copies and transposes overlap the other's FP64 math.
 //
 // HBM bytes per pass: 32 * 2^n (read + write once), independent of the number
 // of gates in it; FP64 work: 8 FMA per amplitude per 1-qubit dense gate.
@@ -138,17 +140,17 @@ __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, c
         case 2: t_dense1<1 % kRegBits>(v, c, op, data); break;
         case 4: t_dense1<2 % kRegBits>(v, c, op, data); break;
         case 8: t_dense1<3 % kRegBits>(v, c, op, data); break;
+        case 16: t_dense1<4 % kRegBits>(v, c, op, data); break;
       }
       break;
-    case T_DENSE1X4: {
+    case T_DENSE1XR: {
       const double2* M = data + op.data;
-      {
-        const SplitCond sc{true, 0, 0};
-        t_dense1_body<0, false>(v, sc, M[0], M[1], M[2], M[3]);
-        t_dense1_body<1 % kRegBits, false>(v, sc, M[4], M[5], M[6], M[7]);
-        t_dense1_body<2 % kRegBits, false>(v, sc, M[8], M[9], M[10], M[11]);
-        t_dense1_body<3 % kRegBits, false>(v, sc, M[12], M[13], M[14], M[15]);
-      }
+      const SplitCond sc{true, 0, 0};
+      t_dense1_body<0, false>(v, sc, M[0], M[1], M[2], M[3]);
+      t_dense1_body<1 % kRegBits, false>(v, sc, M[4], M[5], M[6], M[7]);
+      if (op.m > 2) t_dense1_body<2 % kRegBits, false>(v, sc, M[8], M[9], M[10], M[11]);
+      if (op.m > 3) t_dense1_body<3 % kRegBits, false>(v, sc, M[12], M[13], M[14], M[15]);
+      if (op.m > 4) t_dense1_body<4 % kRegBits, false>(v, sc, M[16], M[17], M[18], M[19]);
       break;
     }
     case T_PHASE: {
@@ -252,7 +254,7 @@ __device__ __forceinline__ void s_dense(double2* sm, int L, const TileOp& op,
         sorted[j - 1] = t;
       }
   const uint32_t ncos = 1u << (L - K);
-  for (uint32_t cidx = tid; cidx < ncos; cidx += kTileThreads) {
+  for (uint32_t cidx = tid; cidx < ncos; cidx += kGroupThreads) {
     uint32_t l0 = cidx;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -289,7 +291,7 @@ __device__ __forceinline__ void s_pauli(double2* sm, int L, const TileOp& op,
   const int pivot = 31 - __clz(xml);
   const double2 alpha = (data[op.data]), bph = (data[op.data + 1]);
   const uint32_t np = 1u << (L - 1);
-  for (uint32_t p = tid; p < np; p += kTileThreads) {
+  for (uint32_t p = tid; p < np; p += kGroupThreads) {
     const uint32_t lo = p & ((1u << pivot) - 1u);
     const uint32_t l = ((p ^ lo) << 1) | lo;
     const uint32_t q = l ^ xml;
@@ -329,7 +331,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-constexpr int kTidBits = 12 - kRegBits;  // log2(kTileThreads)
+constexpr int kTidBits = kMaxTileQubits - kRegBits;  // log2(kGroupThreads)
 
 // global offset of the local index bits above kTidBits (loop index k of the copies)
 __device__ __forceinline__ uint64_t hi_part(const TilePassDev* pd, int L, int k) {
@@ -340,10 +342,17 @@ __device__ __forceinline__ uint64_t hi_part(const TilePassDev* pd, int L, int k)
   return g;
 }
 
-// Persistent tile kernel: one CTA per SM walks tiles blockIdx.x, +gridDim.x,
-// ...; two shared-memory buffers, the next tile's HBM->smem copy (cp.async,
-// XOR-swizzled 16-byte slots) in flight while the current tile computes.
-__global__ void __launch_bounds__(kTileThreads, 1)
+__device__ __forceinline__ void group_sync(int group) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(kGroupThreads) : "memory");
+}
+
+// Persistent tile kernel.  Each CTA = kGroups groups of kGroupThreads threads;
+// group g of CTA b walks tiles g + kGroups * (b + k * gridDim.x).  A group
+// copies its tile HBM -> shared memory (cp.async, XOR-swizzled 16-byte
+// slots), runs the phases with its own named barrier, and writes it back;
+// the groups drift apart so copies/transposes of one overlap the math of the
+// other.  The pass program is staged in shared memory once per CTA.
+__global__ void __launch_bounds__(kCtaThreads, 1)
     k_tile(double2* __restrict__ a, const TilePassDev* __restrict__ pd,
            const TilePhase* __restrict__ phases, const TileOp* __restrict__ g_ops,
            const double2* __restrict__ g_data, FixedBits tb, uint64_t ntiles, int nops,
@@ -352,60 +361,52 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   __shared__ uint64_t s_hi[kRegs];       // HBM offset of copy-index bits >= kTidBits
   const int L = pd->L;
   const uint32_t tile_amps = 1u << L;
-  const int tid = threadIdx.x;
+  const int group = threadIdx.x / kGroupThreads;
+  const int tid = threadIdx.x % kGroupThreads;
   const int nphases = (pd->debug & 2) ? 0 : pd->nphases;
   const bool skip_ops = pd->debug & 1;
   const int dbg = pd->debug;
-  // phase descriptors cached in shared memory after the two tile buffers
-  // [buf0][buf1][ops][data][phases]: the pass program is staged once per
-  // (persistent) CTA, so every op read in the tile loop is a broadcast LDS
-  TileOp* ops = reinterpret_cast<TileOp*>(smem_all + 2 * (size_t)tile_amps);
+  // [tile g0][tile g1][ops][data][phases]
+  TileOp* ops = reinterpret_cast<TileOp*>(smem_all + (size_t)kGroups * tile_amps);
   double2* data = reinterpret_cast<double2*>(ops + nops);
   TilePhase* s_ph = reinterpret_cast<TilePhase*>(data + ndata);
   {
     const int4* src = reinterpret_cast<const int4*>(g_ops);
     int4* dst = reinterpret_cast<int4*>(ops);
-    for (int i = tid; i < nops * (int)(sizeof(TileOp) / 16); i += kTileThreads) dst[i] = src[i];
-    for (int i = tid; i < ndata; i += kTileThreads) data[i] = g_data[i];
+    for (int i = threadIdx.x; i < nops * (int)(sizeof(TileOp) / 16); i += kCtaThreads)
+      dst[i] = src[i];
+    for (int i = threadIdx.x; i < ndata; i += kCtaThreads) data[i] = g_data[i];
     const int words = pd->nphases * (int)(sizeof(TilePhase) / 4);
     const int* psrc = reinterpret_cast<const int*>(phases);
     int* pdst = reinterpret_cast<int*>(s_ph);
-    for (int i = tid; i < words; i += kTileThreads) pdst[i] = psrc[i];
-    if (tid < kRegs) s_hi[tid] = hi_part(pd, L, tid);
+    for (int i = threadIdx.x; i < words; i += kCtaThreads) pdst[i] = psrc[i];
+    if (threadIdx.x < kRegs) s_hi[threadIdx.x] = hi_part(pd, L, threadIdx.x);
   }
-  // local bits below kTidBits of the copy index l = k * kTileThreads + tid
+  // local bits below kTidBits of the copy index l = k * kGroupThreads + tid
   uint64_t lo_part = 0;
   for (int b = 0; b < kTidBits && b < L; ++b)
     if ((tid >> b) & 1) lo_part |= 1ULL << pd->spos[b];
-  const int nk = (int)((tile_amps + kTileThreads - 1) / kTileThreads);
+  const int nk = (int)((tile_amps + kGroupThreads - 1) / kGroupThreads);
   const bool copy_thread = (uint32_t)tid < tile_amps;
+  const int nthr = pd->nthrbits;
+  const bool active = tid < (1 << nthr);
+  double2* sm = smem_all + (size_t)group * tile_amps;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
   __syncthreads();
 
-  auto issue_load = [&](uint64_t tile, double2* buf) {
-    const uint64_t base = widen(tile, tb) | lo_part;
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
+  for (uint64_t tile = (uint64_t)blockIdx.x * kGroups + group; tile < ntiles;
+       tile += (uint64_t)gridDim.x * kGroups) {
+    const uint64_t base = widen(tile, tb);
+    const uint64_t gb = base | lo_part;
     if (copy_thread) {
       for (int k = 0; k < nk; ++k) {
-        const uint32_t l = (uint32_t)k * kTileThreads + tid;
-        cp_async16(sbase + swz(l) * 16u, a + (base | s_hi[k]));
+        const uint32_t l = (uint32_t)k * kGroupThreads + tid;
+        cp_async16(sbase + swz(l) * 16u, a + (gb | s_hi[k]));
       }
     }
     cp_async_commit();
-  };
-
-  uint64_t tile = blockIdx.x;
-  int cur = 0;
-  if (tile < ntiles) issue_load(tile, smem_all);
-  const int nthr = pd->nthrbits;
-  const bool active = tid < (1 << nthr);
-  for (; tile < ntiles; tile += gridDim.x, cur ^= 1) {
-    double2* sm = smem_all + (size_t)cur * tile_amps;
-    const uint64_t next = tile + gridDim.x;
-    if (next < ntiles) issue_load(next, smem_all + (size_t)(cur ^ 1) * tile_amps);
-    else cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const uint64_t base = widen(tile, tb);
+    cp_async_wait<0>();
+    group_sync(group);
 
     for (int ph = 0; ph < nphases; ++ph) {
       const TilePhase& P = s_ph[ph];
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (P.type != 0) {
         for (int o = ob; o < (skip_ops ? ob : oe); ++o) {
           s_apply(sm, L, ops[o], data, base, tid);
-          __syncthreads();
+          group_sync(group);
         }
         continue;
       }
@@ -439,12 +440,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             if ((j >> i) & 1) ad ^= srb[i];
           v[j] = sm[ad];
         }
-        TileOp op = ops[ob];
         for (int o = ob; o < (skip_ops ? ob : oe); ++o) {
-          const TileOp nxt = ops[o + 1 < oe ? o + 1 : o];  // prefetch
-          if (!((dbg & 4) && op.kind != T_DENSE1) && !((dbg & 8) && op.kind == T_DENSE1))
+          const TileOp& op = ops[o];
+          if (!((dbg & 4) && op.kind != T_DENSE1 && op.kind != T_DENSE1XR) &&
+              !((dbg & 8) && (op.kind == T_DENSE1 || op.kind == T_DENSE1XR)))
             t_apply(v, c, op, data);
-          op = nxt;
         }
 #pragma unroll
         for (int j = 0; j < kRegs; ++j) {
@@ -455,20 +455,18 @@ __global__ void __launch_bounds__(kTileThreads, 1)
           sm[ad] = v[j];
         }
       }
-      __syncthreads();
+      group_sync(group);
     }
 
     // shared -> HBM (same mapping as the load)
     if (copy_thread) {
-      const uint64_t gb = base | lo_part;
       for (int k = 0; k < nk; ++k) {
-        const uint32_t l = (uint32_t)k * kTileThreads + tid;
+        const uint32_t l = (uint32_t)k * kGroupThreads + tid;
         st1(a + (gb | s_hi[k]), sm[swz(l)]);
       }
     }
-    __syncthreads();  // buffer `cur` is refilled two tiles later
+    group_sync(group);  // the tile buffer is refilled next iteration
   }
-  cp_async_wait<0>();
 }
 
 // ======================================================================= host
@@ -716,7 +714,7 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
   auto close = [&]() {
     if (!open) return;
     // register slots in order of first use by a 1-qubit dense op, so runs of
-    // kRegBits such ops land on slots 0,1,2,3 and can be batched
+    // such ops land on slots 0, 1, ... and can be batched
     std::vector<int> order;
     for (auto& pr : d1)
       if (std::find(order.begin(), order.end(), pr.second) == order.end())
@@ -743,24 +741,27 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
     order_thread_bits(tb);
     for (size_t k = 0; k < tb.size(); ++k) ph.thrpos[k] = tb[k];
     for (auto& pr : d1) e.ops[pr.first].slots = 1 << slot_of[pr.second];
-    // batch runs of kRegBits uncontrolled 1-qubit dense ops on slots 0..3
-    if (kRegBits == 4) {
+    // batch runs of >= 2 uncontrolled 1-qubit dense ops on slots 0, 1, ... in order
+    {
       std::vector<TileOp> merged;
       const size_t end = e.ops.size();
       size_t k = op_begin;
       while (k < end) {
-        bool run = k + 4 <= end;
-        for (int q = 0; run && q < 4; ++q) {
-          const TileOp& o = e.ops[k + q];
-          run = o.kind == T_DENSE1 && o.slots == (1 << q) && o.lmask == 0 && o.gmask == 0 &&
-                o.data == e.ops[k].data + 4 * q;
+        int len = 0;
+        while (k + len < end && len < kRegBits) {
+          const TileOp& o = e.ops[k + len];
+          if (!(o.kind == T_DENSE1 && o.slots == (1 << len) && o.lmask == 0 && o.gmask == 0 &&
+                o.data == e.ops[k].data + 4 * len))
+            break;
+          ++len;
         }
-        if (run) {
+        if (len >= 2) {
           TileOp b = e.ops[k];
-          b.kind = T_DENSE1X4;
-          b.slots = 15;
+          b.kind = T_DENSE1XR;
+          b.m = len;
+          b.slots = (1 << len) - 1;
           merged.push_back(b);
-          k += 4;
+          k += len;
         } else {
           merged.push_back(e.ops[k]);
           ++k;
@@ -1005,7 +1006,7 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
   int pos[kMaxTileQubits];
   for (int j = 0; j < tp.L; ++j) pos[j] = tp.qubits[j];
   FixedBits tb = make_fixed(pos, tp.L, 0);
-  const size_t smem = 2 * (sizeof(double2) << tp.L) + tp.nops * sizeof(TileOp) +
+  const size_t smem = kGroups * (sizeof(double2) << tp.L) + tp.nops * sizeof(TileOp) +
                       tp.ndata * sizeof(double2) + tp.nphases * sizeof(TilePhase);
   if (smem > kTileSmemLimit) {
     set_error("tile pass program (%d ops, %d phases) does not fit in shared memory", tp.nops,
@@ -1023,8 +1024,9 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     attr_dev = dev;
   }
   const uint64_t ntiles = 1ULL << (n - tp.L);
-  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms);
-  k_tile<<<grid, kTileThreads, smem, s>>>(amps, pd, ph, ops, data, tb, ntiles, tp.nops,
+  const uint64_t ctas = (ntiles + kGroups - 1) / kGroups;
+  const unsigned grid = (unsigned)std::min<uint64_t>(ctas, (uint64_t)num_sms);
+  k_tile<<<grid, kCtaThreads, smem, s>>>(amps, pd, ph, ops, data, tb, ntiles, tp.nops,
                                           tp.ndata);
   QSV_CHECK_LAUNCH("k_tile");
   return QSV_OK;

@@ -9,16 +9,19 @@
 namespace qsv {
 
 #ifndef QSV_TILE_REGBITS
-#define QSV_TILE_REGBITS 4
+#define QSV_TILE_REGBITS 5
 #endif
 constexpr int kRegBits = QSV_TILE_REGBITS;  // amplitudes per thread = 2^kRegBits
 constexpr int kRegs = 1 << kRegBits;
-constexpr int kTileThreads = 4096 / kRegs;  // threads per tile CTA (2^12 amps)
-constexpr int kMaxTileQubits = 12;  // 2^12 amps = 64 KiB of shared memory
+constexpr int kMaxTileQubits = 12;          // 2^12 amps = 64 KiB of shared memory
+constexpr int kGroupThreads = (1 << kMaxTileQubits) / kRegs;  // threads per tile group
+constexpr int kGroups = 2;                  // independent tile groups per CTA
+constexpr int kCtaThreads = kGroups * kGroupThreads;
 constexpr int kLowQubits = 4;       // qubits 0..3 are in every tile (256 B runs)
 constexpr int kTileSmemLimit = 227 * 1024 - 1024;  // dynamic part (static smem aside)
 // shared memory left for the staged pass program (ops, data, phases)
-constexpr int kTileProgramBudget = kTileSmemLimit - 2 * (16 << kMaxTileQubits) - 1024;
+constexpr int kTileProgramBudget =
+    kTileSmemLimit - kGroups * (16 << kMaxTileQubits) - 1024;
 
 // ---- device-side program records (all POD, stored in the payload) ----
 enum TileOpKind : int32_t {
@@ -27,7 +30,7 @@ enum TileOpKind : int32_t {
   T_DIAG = 5,     // diagonal, targets on local or tile (global) bits
   T_PHASE = 6,    // constant phase on a local/tile bit pattern
   T_PARITY = 7,   // f[parity(idx & zmask)]
-  T_DENSE1X4 = 8, // four uncontrolled 2x2 on slots 0,1,2,3 in order (data: 16 entries)
+  T_DENSE1XR = 8, // m uncontrolled 2x2 on slots 0..m-1 in order (data: 4m entries)
   // shared-memory ops (a phase of their own; cosets read straight from smem)
   S_DENSE = 9,    // 2^m x 2^m on m <= 4 local bits (tpos), optionally controlled
   S_PAULI = 10,   // X/Y product on local bits (slots = local X mask), Z parity
