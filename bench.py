@@ -67,6 +67,17 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def fp64_peak():
+    """Sustained FP64 FMA peak measured by profiles/micro/fp64_peak.cu."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["fp64_tflops_sustained"]), "measured sustained (profiles/fp64_peak.json)"
+    except Exception:
+        return 32.3, "measured burst (DESIGN.md)"
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -482,21 +493,29 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
     circ.update_quantum_state(st)  # warm (graph capture)
     torch.cuda.synchronize(dev)
     times = []
-    for _ in range(args.circuit_reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        circ.update_quantum_state(st)
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        times.append(a.elapsed_time(b) / 1e3)
+    with ClockSampler(dev) as clk:
+        for _ in range(args.circuit_reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            circ.update_quantum_state(st)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            times.append(a.elapsed_time(b) / 1e3)
     best = min(times)
+    fpeak, fsrc = fp64_peak()
+    achieved = stats.get("fp64_flops", 0.0) / best / 1e12
     out = {"metric": "random-circuit sec/layer", "unit": "s/layer",
            "value": best / (depth + 1), "higher_is_better": False,
            "workload": f"cz-ladder n={n} depth={depth} seed=1 ({gates_in} gates), "
                        "native planner (fusion + tile passes)",
            "circuit_s_best": best, "circuit_s_all": times, "plan_s": plan_s,
            "program": stats,
-           "hbm_gbs_effective": stats.get("hbm_bytes", 0.0) / best / 1e9}
+           "hbm_gbs_effective": stats.get("hbm_bytes", 0.0) / best / 1e9,
+           "roofline": {"bound": "fp64", "achieved": achieved, "peak": fpeak,
+                        "unit": "TFLOP/s", "frac": achieved / fpeak, "peak_source": fsrc,
+                        "kernel": "k_tile (tile passes)",
+                        "note": "FP64 flops counted by the planner (2 per FMA) / device time"},
+           "clocks": clk.summary()}
     del st
     return out
 

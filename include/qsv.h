@@ -156,6 +156,7 @@ typedef struct qsv_program_stats {
   int32_t num_tile_passes;/* of which tile passes                          */
   int32_t num_gate_kernels;
   double hbm_bytes;       /* algorithmic HBM bytes per run                 */
+  double fp64_flops;      /* FP64 flops per run (2 per FMA), planner count */
 } qsv_program_stats;
 
 int qsv_program_create(int num_qubits, const qsv_op* ops, int nops,

@@ -59,6 +59,7 @@ class QsvProgramStats(C.Structure):
         ("num_tile_passes", C.c_int32),
         ("num_gate_kernels", C.c_int32),
         ("hbm_bytes", C.c_double),
+        ("fp64_flops", C.c_double),
     ]
 
 

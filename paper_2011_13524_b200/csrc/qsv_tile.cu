@@ -901,6 +901,18 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
   return e;
 }
 
+// FP64 flops of one gate applied to a 2^n state (2 per FMA): a complex
+// multiply-add is 8 flops, a complex multiply 6, a sign flip 0.
+double gate_fp64_flops(int n, const GateDesc& g) {
+  const double amps = std::ldexp(1.0, n - g.nc);
+  if (g.kind == QSV_OP_DENSE) return amps * 8.0 * (double)(1 << g.m);
+  if (g.kind == QSV_OP_DIAG) {
+    if (g.m == 0 && g.data.size() == 1 && g.data[0].re == -1.0 && g.data[0].im == 0.0) return 0.0;
+    return amps * 6.0;
+  }
+  return std::ldexp(1.0, n) * 14.0;  // Pauli rotation: alpha*x + beta*phase*y
+}
+
 void add_gate_step(int n, const GateDesc& g, std::vector<Step>& steps, std::vector<char>& payload,
                    qsv_program_stats* stats) {
   Step st;
@@ -919,6 +931,7 @@ void add_gate_step(int n, const GateDesc& g, std::vector<Step>& steps, std::vect
   stats->num_gate_kernels += 1;
   stats->num_steps += 1;
   stats->hbm_bytes += gate_hbm_bytes(n, g);
+  stats->fp64_flops += gate_fp64_flops(n, g);
 }
 
 }  // namespace
@@ -969,6 +982,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
     tp.ndata = (int)e.data.size();
     tp.num_gates = (int)pg.size();
     tp.hbm_bytes = 32.0 * std::ldexp(1.0, n);
+    for (const GateDesc* gp : pg) stats->fp64_flops += gate_fp64_flops(n, *gp);
     // payload: [TilePassDev][phases][ops][data]
     size_t off = align_up(payload.size(), 256);
     tp.dev_off = off;
