@@ -119,6 +119,30 @@ int qsv_expect(const qsv_state* bra, const qsv_state* ket, int nterms,
                const int* term_len, const int* qubits, const int* ids,
                const double* coefs, double out_re_im[2]);
 
+/* --------------------------------------------- analysis and reshaping
+ * qsv_marginal_prob    <- get_marginal_probability (state.py:83-95): sum of
+ *                         |psi_x|^2 over x with (x & mask) == value.
+ * qsv_sampling         <- sampling (state.py:97-106): uniforms[i] are the
+ *                         host draws rng.random(count) (numpy PCG64, for
+ *                         seed parity); out[i] = searchsorted(cumsum(|psi|^2),
+ *                         uniforms[i] * total, side="right").
+ * qsv_mul_elementwise  <- multiply_elementwise_function (state.py:116-119):
+ *                         amps *= coefs (coefs evaluated by the caller).
+ * qsv_tensor_product   <- tensor_product (state.py:142-146): out =
+ *                         kron(second, first), first on the low qubits.
+ * qsv_permutate_qubit  <- permutate_qubit (state.py:149-161): new qubit i
+ *                         carries old qubit order[i]; out must differ from src.
+ * qsv_drop_qubit       <- drop_qubit (state.py:164-192): project targets onto
+ *                         values and remove them (not renormalised).
+ */
+int qsv_marginal_prob(const qsv_state* st, uint64_t mask, uint64_t value, double* out);
+int qsv_sampling(const qsv_state* st, const double* uniforms, int count, uint64_t* out);
+int qsv_mul_elementwise(qsv_state* st, const double* coefs_interleaved, uint64_t n_amps);
+int qsv_tensor_product(const qsv_state* first, const qsv_state* second, qsv_state* out);
+int qsv_permutate_qubit(const qsv_state* src, const int* order, int n, qsv_state* out);
+int qsv_drop_qubit(const qsv_state* src, const int* targets, const int* values, int k,
+                   qsv_state* out);
+
 /* ------------------------------------------------------------ programs
  * A program is a compiled gate list: the replacement for the per-gate loop
  * of Circuit.update_state (circuit.py:48-55).  qsv_program_create copies the

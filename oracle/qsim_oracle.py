@@ -293,6 +293,71 @@ def expectation(amps_bra, amps_ket, n, terms):
     return total
 
 
+# ------------------------------------------------- analysis / reshaping
+WILDCARD = 2
+
+
+def marginal_probability(amps, n, pattern):
+    """state.py:83-95: sum of |psi|^2 over indices matching 0/1 per qubit,
+    WILDCARD (2) leaves a qubit free."""
+    probs = np.abs(amps) ** 2
+    idx = np.arange(1 << n)
+    mask = np.ones(1 << n, dtype=bool)
+    for qubit, want in enumerate(pattern):
+        if want == WILDCARD:
+            continue
+        mask &= ((idx >> qubit) & 1) == want
+    return float(probs[mask].sum())
+
+
+def sampling(amps, count, seed):
+    """state.py:97-106: cumulative distribution + searchsorted(side=right)
+    on draws rng.random(count) * cumulative[-1]."""
+    if count == 0:
+        return []
+    cumulative = np.cumsum(np.abs(amps) ** 2)
+    rng = np.random.default_rng(seed)
+    draws = rng.random(count) * cumulative[-1]
+    return np.searchsorted(cumulative, draws, side="right").tolist()
+
+
+def multiply_elementwise(amps, func):
+    """state.py:116-119: amps *= [func(i) for i in range(dim)]."""
+    coefs = np.fromiter((func(i) for i in range(amps.size)), dtype=np.complex128,
+                        count=amps.size)
+    amps *= coefs
+    return amps
+
+
+def tensor_product(first, second):
+    """state.py:142-146: kron(second, first) (first on the low qubits)."""
+    return np.kron(second, first)
+
+
+def permutate_qubit(amps, n, order):
+    """state.py:149-161: new qubit i carries old qubit order[i]."""
+    src = np.arange(1 << n)
+    dst = np.zeros(1 << n, dtype=np.intp)
+    for new_q, old_q in enumerate(order):
+        dst |= ((src >> old_q) & 1) << new_q
+    out = np.zeros(1 << n, dtype=np.complex128)
+    out[dst] = amps[src]
+    return out
+
+
+def drop_qubit(amps, n, targets, values):
+    """state.py:164-192: project targets onto values, remove them, no
+    renormalisation."""
+    keep = [q for q in range(n) if q not in set(targets)]
+    src = np.arange(1 << len(keep), dtype=np.intp)
+    full = np.zeros(1 << len(keep), dtype=np.intp)
+    for j, q in enumerate(keep):
+        full |= ((src >> j) & 1) << q
+    for t, v in zip(targets, values):
+        full |= v << t
+    return amps[full].copy()
+
+
 # ---------------------------------------------------------------- workloads
 def _rot(q, pid, ang):
     return ("pauli_rot", (q,), (pid,), float(ang), ())

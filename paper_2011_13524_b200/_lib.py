@@ -104,6 +104,12 @@ _SIGS = {
     "qsv_add": ([_P, _P], _I),
     "qsv_inner": ([_P, _P, C.POINTER(C.c_double)], _I),
     "qsv_expect": ([_P, _P, _I, _IP, _IP, _IP, _DP, C.POINTER(C.c_double)], _I),
+    "qsv_marginal_prob": ([_P, _U64, _U64, C.POINTER(C.c_double)], _I),
+    "qsv_sampling": ([_P, _DP, _I, _DP], _I),
+    "qsv_mul_elementwise": ([_P, _DP, _U64], _I),
+    "qsv_tensor_product": ([_P, _P, _P], _I),
+    "qsv_permutate_qubit": ([_P, _IP, _I, _P], _I),
+    "qsv_drop_qubit": ([_P, _IP, _IP, _I, _P], _I),
     "qsv_program_create": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts), C.POINTER(_P)], _I),
     "qsv_program_run": ([_P, _P], _I),
     "qsv_program_stats_get": ([_P, C.POINTER(QsvProgramStats)], _I),

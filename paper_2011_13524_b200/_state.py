@@ -13,7 +13,7 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import check, lib
+from ._lib import check, int_array, lib
 
 WILDCARD = 2
 
@@ -144,6 +144,46 @@ class StateVector:
             raise ValueError("qubit counts differ")
         check(lib.qsv_add(self._h, other._h))
 
+    def multiply_elementwise_function(self, func) -> None:
+        """amps[i] *= func(i) (state.py:116-119).  ``func`` is arbitrary
+        Python, so it is evaluated on the host exactly as the reference does
+        (one call per index, in index order); the multiply runs on the GPU."""
+        coefs = np.fromiter((func(i) for i in range(self.dim)), dtype=np.complex128,
+                            count=self.dim)
+        check(lib.qsv_mul_elementwise(self._h, coefs.ctypes.data, coefs.size))
+
+    # -- measurement statistics (state.py:83-106) --------------------------
+    def get_marginal_probability(self, measured_value) -> float:
+        """Sum of |psi_x|^2 over the x matching a pattern of 0 / 1 / WILDCARD
+        (=2) per qubit (state.py:83-95), as one masked GPU reduction."""
+        pattern = list(measured_value)
+        if len(pattern) != self._n:
+            raise ValueError("pattern length must equal the qubit count")
+        mask = value = 0
+        for q, want in enumerate(pattern):
+            if want == WILDCARD:
+                continue
+            if want not in (0, 1):
+                raise ValueError(f"pattern entry must be 0, 1 or WILDCARD, got {want!r}")
+            mask |= 1 << q
+            value |= int(want) << q
+        out = C.c_double()
+        check(lib.qsv_marginal_prob(self._h, mask, value, C.byref(out)))
+        return float(out.value)
+
+    def sampling(self, count: int, seed=None) -> list[int]:
+        """Z-basis samples (state.py:97-106): draws ``rng.random(count)`` on
+        the host (numpy PCG64, so a seed gives the reference's draws) and
+        inverts the cumulative distribution of |psi|^2 on the GPU."""
+        if count == 0:
+            return []
+        if count < 0:
+            raise ValueError("sample count must be non-negative")
+        u = np.random.default_rng(seed).random(count)
+        out = np.empty(count, dtype=np.uint64)
+        check(lib.qsv_sampling(self._h, u.ctypes.data, int(count), out.ctypes.data))
+        return out.astype(np.int64).tolist()
+
     # -- classical registers (state.py:116-127) ----------------------------
     def get_classical_value(self, index: int) -> int:
         if index < 0:
@@ -179,3 +219,44 @@ def inner_product(bra: StateVector, ket: StateVector) -> complex:
     out = (C.c_double * 2)()
     check(lib.qsv_inner(bra._h, ket._h, out))
     return complex(out[0], out[1])
+
+
+def tensor_product(first: StateVector, second: StateVector) -> StateVector:
+    """kron(second, first): ``first`` on the low qubits (state.py:142-146)."""
+    out = StateVector(first._n + second._n, first._device)
+    check(lib.qsv_tensor_product(first._h, second._h, out._h))
+    return out
+
+
+def permutate_qubit(state: StateVector, order) -> StateVector:
+    """New qubit i carries the role of old qubit order[i] (state.py:149-161)."""
+    n = state._n
+    order = [int(q) for q in order]
+    if sorted(order) != list(range(n)):
+        raise ValueError(f"order must be a permutation of 0..{n - 1}")
+    out = StateVector(n, state._device)
+    check(lib.qsv_permutate_qubit(state._h, int_array(order), n, out._h))
+    return out
+
+
+def drop_qubit(state: StateVector, targets, values) -> StateVector:
+    """Project ``targets`` onto ``values`` and remove them, without
+    renormalising (state.py:164-192)."""
+    n = state._n
+    targets = [int(t) for t in targets]
+    values = list(values)
+    if len(targets) != len(values):
+        raise ValueError("targets and projection values must pair up")
+    if len(set(targets)) != len(targets):
+        raise ValueError("target qubits must be distinct")
+    if len(targets) >= n:
+        raise ValueError("cannot drop every qubit")
+    for t, v in zip(targets, values):
+        if not 0 <= t < n:
+            raise ValueError(f"target {t} out of range")
+        if v not in (0, 1):
+            raise ValueError("projection values must be 0 or 1")
+    out = StateVector(n - len(targets), state._device)
+    check(lib.qsv_drop_qubit(state._h, int_array(targets), int_array([int(v) for v in values]),
+                             len(targets), out._h))
+    return out

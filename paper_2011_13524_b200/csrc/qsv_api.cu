@@ -33,6 +33,18 @@ int launch_expect_sweep(const double2* bra, const double2* ket, int n, uint64_t 
                         const uint64_t* zm, int nt, double* partials, double* dev_out,
                         cudaStream_t s);
 
+int launch_marginal(const double2* a, int n, uint64_t mask, uint64_t value, double* partials,
+                    double* dev_out, cudaStream_t s);
+int launch_sampling(const double2* a, int n, const double* dev_u, int count, double* scratch,
+                    uint64_t* dev_out, cudaStream_t s);
+size_t sampling_scratch_doubles(int n);
+int launch_mul_elementwise(double2* a, const double2* f, uint64_t dim, cudaStream_t s);
+int launch_kron(const double2* first, int n1, const double2* second, int n2, double2* out,
+                cudaStream_t s);
+int launch_permute(const double2* in, double2* out, int n, const int* order, cudaStream_t s);
+int launch_drop(const double2* in, int n, const int* targets, const int* values, int k,
+                double2* out, cudaStream_t s);
+
 __global__ void k_set1(double2* a, uint64_t idx) { a[idx] = make_double2(1.0, 0.0); }
 
 // Device scratch owned by a state: payloads of direct gate calls and
@@ -43,6 +55,7 @@ struct Scratch {
 };
 static std::map<const qsv_state*, Scratch> g_payload;
 static std::map<const qsv_state*, Scratch> g_results;
+static std::map<const qsv_state*, Scratch> g_analysis;
 
 static int ensure(Scratch& s, size_t bytes, cudaStream_t stream) {
   if (s.cap >= bytes) return QSV_OK;
@@ -201,7 +214,7 @@ int qsv_state_destroy(qsv_state* st) {
   cudaStreamSynchronize(st->stream);
   cudaFree(st->amps);
   cudaFree(st->partials);
-  for (auto* mp : {&g_payload, &g_results}) {
+  for (auto* mp : {&g_payload, &g_results, &g_analysis}) {
     auto it = mp->find(st);
     if (it != mp->end()) {
       cudaFree(it->second.ptr);
@@ -553,6 +566,141 @@ int qsv_add(qsv_state* dst, const qsv_state* src) {
   DeviceGuard dg(dst->device);
   if (src->stream != dst->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
   return launch_add(dst->amps, src->amps, dst->dim, dst->stream);
+}
+
+// ------------------------------------------------- analysis / reshaping
+int qsv_marginal_prob(const qsv_state* st, uint64_t mask, uint64_t value, double* out) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (st->n < 64 && (mask >> st->n) != 0) {
+    set_error("pattern mask touches qubits beyond %d", st->n);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(st->device);
+  Scratch& sc = g_results[st];
+  int rc = ensure(sc, sizeof(double) * 2 * kMaxTerms, st->stream);
+  if (rc) return rc;
+  double* dout = reinterpret_cast<double*>(sc.ptr);
+  rc = launch_marginal(st->amps, st->n, mask, value, st->partials, dout, st->stream);
+  if (rc) return rc;
+  QSV_TRY(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+  QSV_TRY(cudaStreamSynchronize(st->stream));
+  return QSV_OK;
+}
+
+int qsv_sampling(const qsv_state* st, const double* uniforms, int count, uint64_t* out) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (count < 0) {
+    set_error("sample count must be non-negative");
+    return QSV_EINVAL;
+  }
+  if (count == 0) return QSV_OK;
+  DeviceGuard dg(st->device);
+  const size_t nd = sampling_scratch_doubles(st->n);
+  const size_t bytes = (nd + 2 * (size_t)count) * sizeof(double);
+  Scratch& sc = g_analysis[st];
+  int rc = ensure(sc, bytes, st->stream);
+  if (rc) return rc;
+  double* scratch = reinterpret_cast<double*>(sc.ptr);
+  double* du = scratch + nd;
+  uint64_t* dout = reinterpret_cast<uint64_t*>(du + count);
+  QSV_TRY(cudaMemcpyAsync(du, uniforms, sizeof(double) * count, cudaMemcpyHostToDevice,
+                          st->stream));
+  rc = launch_sampling(st->amps, st->n, du, count, scratch, dout, st->stream);
+  if (rc) return rc;
+  QSV_TRY(cudaMemcpyAsync(out, dout, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost,
+                          st->stream));
+  QSV_TRY(cudaStreamSynchronize(st->stream));
+  return QSV_OK;
+}
+
+int qsv_mul_elementwise(qsv_state* st, const double* coefs, uint64_t n_amps) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (n_amps != st->dim) {
+    set_error("expected %llu coefficients, got %llu", (unsigned long long)st->dim,
+              (unsigned long long)n_amps);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(st->device);
+  Scratch& sc = g_analysis[st];
+  int rc = ensure(sc, st->dim * sizeof(double2), st->stream);
+  if (rc) return rc;
+  QSV_TRY(cudaMemcpyAsync(sc.ptr, coefs, st->dim * sizeof(double2), cudaMemcpyHostToDevice,
+                          st->stream));
+  rc = launch_mul_elementwise(st->amps, reinterpret_cast<const double2*>(sc.ptr), st->dim,
+                              st->stream);
+  if (rc) return rc;
+  QSV_TRY(cudaStreamSynchronize(st->stream));  // the scratch is reused by the next call
+  return QSV_OK;
+}
+
+static int same_device3(const qsv_state* a, const qsv_state* b, const qsv_state* c) {
+  if (a->device != b->device || a->device != c->device) {
+    set_error("states live on different devices");
+    return QSV_EINVAL;
+  }
+  return QSV_OK;
+}
+
+int qsv_tensor_product(const qsv_state* first, const qsv_state* second, qsv_state* out) {
+  if (bad_state(first) || bad_state(second) || bad_state(out)) return QSV_EINVAL;
+  if (out->n != first->n + second->n) {
+    set_error("output has %d qubits, expected %d", out->n, first->n + second->n);
+    return QSV_EINVAL;
+  }
+  if (same_device3(first, second, out)) return QSV_EINVAL;
+  DeviceGuard dg(out->device);
+  if (first->stream != out->stream) QSV_TRY(cudaStreamSynchronize(first->stream));
+  if (second->stream != out->stream) QSV_TRY(cudaStreamSynchronize(second->stream));
+  return launch_kron(first->amps, first->n, second->amps, second->n, out->amps, out->stream);
+}
+
+int qsv_permutate_qubit(const qsv_state* src, const int* order, int n, qsv_state* out) {
+  if (bad_state(src) || bad_state(out)) return QSV_EINVAL;
+  if (n != src->n || out->n != src->n) {
+    set_error("order / output width must equal the state's %d qubits", src->n);
+    return QSV_EINVAL;
+  }
+  if (src == out) {
+    set_error("permutate_qubit needs a distinct output state");
+    return QSV_EINVAL;
+  }
+  uint64_t seen = 0;
+  for (int i = 0; i < n; ++i) {
+    if (order[i] < 0 || order[i] >= n || ((seen >> order[i]) & 1ULL)) {
+      set_error("order must be a permutation of 0..%d", n - 1);
+      return QSV_EINVAL;
+    }
+    seen |= 1ULL << order[i];
+  }
+  if (same_device3(src, out, out)) return QSV_EINVAL;
+  DeviceGuard dg(out->device);
+  if (src->stream != out->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
+  return launch_permute(src->amps, out->amps, n, order, out->stream);
+}
+
+int qsv_drop_qubit(const qsv_state* src, const int* targets, const int* values, int k,
+                   qsv_state* out) {
+  if (bad_state(src) || bad_state(out)) return QSV_EINVAL;
+  if (k < 0 || k >= src->n || out->n != src->n - k) {
+    set_error("cannot drop %d of %d qubits into a %d-qubit state", k, src->n, out->n);
+    return QSV_EINVAL;
+  }
+  uint64_t seen = 0;
+  for (int i = 0; i < k; ++i) {
+    if (targets[i] < 0 || targets[i] >= src->n || ((seen >> targets[i]) & 1ULL)) {
+      set_error("targets must be distinct qubits of the state");
+      return QSV_EINVAL;
+    }
+    if (values[i] != 0 && values[i] != 1) {
+      set_error("projection values must be 0 or 1");
+      return QSV_EINVAL;
+    }
+    seen |= 1ULL << targets[i];
+  }
+  if (same_device3(src, out, out)) return QSV_EINVAL;
+  DeviceGuard dg(out->device);
+  if (src->stream != out->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
+  return launch_drop(src->amps, src->n, targets, values, k, out->amps, out->stream);
 }
 
 }  // extern "C"

@@ -17,6 +17,8 @@ fixtures next to this script:
   (cnot-ring, cz-ladder), reference optimizer gate counts and final states.
 * ``observables.json`` -- expectation values computed by the reference.
 * ``haar.npz`` -- set_haar_random outputs (bit-exact pin of the PCG64 path).
+* ``analysis.json`` + ``analysis.npz`` -- marginal probabilities, sampling
+  results, tensor_product / permutate_qubit / drop_qubit outputs.
 
 Nothing on the GPU box reads /root/reference; only these files travel.
 """
@@ -296,14 +298,62 @@ def make_haar():
     np.savez_compressed(os.path.join(HERE, "haar.npz"), **outs)
 
 
+def analysis_cases():
+    """Inputs of the state-analysis fixtures (also rebuilt by the tests)."""
+    marg = [(5, 3, [0, 1, 2, 2, 1]), (5, 3, [2, 2, 2, 2, 2]), (8, 11, [1, 0, 2, 2, 0, 1, 2, 2]),
+            (12, 4, [2] * 6 + [1, 0, 1, 0, 2, 2]), (12, 4, [0] * 12), (13, 9, [2, 1] * 6 + [0])]
+    samp = [(4, 1, 10, 0), (9, 2, 1000, 5), (13, 3, 4096, 77), (16, 8, 20000, 1), (16, 8, 0, 1)]
+    kron = [(3, 1, 4, 2), (1, 5, 6, 6), (7, 3, 5, 4)]
+    perm = [(4, 2, [3, 2, 1, 0]), (6, 5, [1, 4, 0, 5, 2, 3]), (11, 6, [10, 0, 9, 1, 8, 2, 7, 3, 6, 4, 5])]
+    drop = [(4, 2, [1], [1]), (6, 3, [5, 0], [0, 1]), (10, 8, [2, 7, 4], [1, 1, 0]),
+            (9, 1, [0, 1, 2, 3, 4, 5, 6, 7], [1, 0, 1, 1, 0, 0, 1, 0])]
+    return {"marginal": marg, "sampling": samp, "tensor": kron, "permutate": perm, "drop": drop}
+
+
+def make_analysis():
+    cases = analysis_cases()
+    meta = {"marginal": [], "sampling": [], "tensor": [], "permutate": [], "drop": []}
+    outs = {}
+
+    def haar(n, seed):
+        st = core.StateVector(n)
+        st.set_haar_random(seed)
+        return st
+
+    for i, (n, seed, pat) in enumerate(cases["marginal"]):
+        meta["marginal"].append({"n": n, "seed": seed, "pattern": pat,
+                                 "value": haar(n, seed).get_marginal_probability(pat)})
+    for i, (n, seed, count, sseed) in enumerate(cases["sampling"]):
+        meta["sampling"].append({"n": n, "seed": seed, "count": count, "sample_seed": sseed,
+                                 "samples": haar(n, seed).sampling(count, seed=sseed)})
+    for i, (n1, s1, n2, s2) in enumerate(cases["tensor"]):
+        outs[f"tensor{i}"] = core.tensor_product(haar(n1, s1), haar(n2, s2)).get_vector()
+        meta["tensor"].append({"n1": n1, "s1": s1, "n2": n2, "s2": s2, "key": f"tensor{i}"})
+    for i, (n, seed, order) in enumerate(cases["permutate"]):
+        outs[f"perm{i}"] = core.permutate_qubit(haar(n, seed), order).get_vector()
+        meta["permutate"].append({"n": n, "seed": seed, "order": order, "key": f"perm{i}"})
+    for i, (n, seed, tg, vals) in enumerate(cases["drop"]):
+        outs[f"drop{i}"] = core.drop_qubit(haar(n, seed), tg, vals).get_vector()
+        meta["drop"].append({"n": n, "seed": seed, "targets": tg, "values": vals,
+                             "key": f"drop{i}"})
+    with open(os.path.join(HERE, "analysis.json"), "w") as fh:
+        json.dump(meta, fh)
+    np.savez_compressed(os.path.join(HERE, "analysis.npz"), **outs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-cfg3", action="store_true",
                     help="also run the 24-qubit VQE instance (~3 min)")
+    ap.add_argument("--only", default=None, help="regenerate one fixture set (e.g. analysis)")
     args = ap.parse_args()
     if not core.__file__.startswith("/root/reference"):
         sys.exit("qsimcore must be imported from /root/reference")
+    if args.only == "analysis":
+        make_analysis()
+        return
     make_haar()
+    make_analysis()
     make_gates()
     make_circuits()
     make_observables(args.with_cfg3)
