@@ -172,6 +172,8 @@ typedef struct qsv_plan_opts {
   int32_t tile_qubits;    /* qubits per tile, 0 = engine default           */
   int32_t fuse;           /* 1: fuse same-support runs on the host (def.)  */
   int32_t use_graph;      /* 1: replay through a CUDA graph                */
+  int32_t real_frames;    /* 1: run 1-qubit gates as real rotations with   */
+                          /*    their phases merged into diagonal flushes */
 } qsv_plan_opts;
 
 typedef struct qsv_program_stats {

@@ -52,6 +52,7 @@ def default_plan_opts(**kw) -> _lib.QsvPlanOpts:
     o.tile_qubits = int(kw.get("tile_qubits", 0))
     o.fuse = int(kw.get("fuse", 1))
     o.use_graph = int(kw.get("use_graph", 1))
+    o.real_frames = int(kw.get("real_frames", 1))
     return o
 
 
@@ -122,7 +123,7 @@ class Circuit:
 
     # -- execution -------------------------------------------------------------
     def set_plan_options(self, **kw) -> None:
-        """Engine knobs: use_tiles, tile_qubits, fuse, use_graph."""
+        """Engine knobs: use_tiles, tile_qubits, fuse, use_graph, real_frames."""
         self._plan = default_plan_opts(**kw)
         self._prog = None
 

@@ -49,6 +49,7 @@ class QsvPlanOpts(C.Structure):
         ("tile_qubits", C.c_int32),
         ("fuse", C.c_int32),
         ("use_graph", C.c_int32),
+        ("real_frames", C.c_int32),
     ]
 
 

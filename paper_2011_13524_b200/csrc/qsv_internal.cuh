@@ -155,6 +155,12 @@ struct GateDesc {
   int cv[QSV_MAX_CONTROLS];
   double angle;
   std::vector<Cplx> data;  // DENSE: 4^m, DIAG: 2^m
+  // real-frame form of an uncontrolled 1-qubit dense gate (tile planner):
+  // data = R diag(rf_b) with R = rf_r real; the tile encoder applies
+  // diag(rf_b) inside a merged diagonal flush and R as real arithmetic
+  int rf = 0;
+  Cplx rf_b[2] = {{1, 0}, {1, 0}};
+  double rf_r[4] = {0, 0, 0, 0};
 };
 
 int validate_gate(int n, const GateDesc& g);

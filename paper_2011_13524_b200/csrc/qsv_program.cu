@@ -122,7 +122,7 @@ int qsv_plan_stats(int n, const qsv_op* ops, int nops, const qsv_plan_opts* opts
     set_error("bad plan arguments");
     return QSV_EINVAL;
   }
-  qsv_plan_opts o{1, 0, 1, 1};
+  qsv_plan_opts o{1, 0, 1, 1, 1};
   if (opts) o = *opts;
   std::vector<GateDesc> gates;
   int rc = convert_ops(n, ops, nops, gates);
@@ -146,7 +146,7 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
     set_error("bad program arguments");
     return QSV_EINVAL;
   }
-  qsv_plan_opts o{1, 0, 1, 1};
+  qsv_plan_opts o{1, 0, 1, 1, 1};
   if (opts) o = *opts;
   std::vector<GateDesc> gates;
   int rc0 = convert_ops(n, ops, nops, gates);

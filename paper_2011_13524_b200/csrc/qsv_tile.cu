@@ -35,46 +35,30 @@ __device__ __forceinline__ uint32_t swz(uint32_t l) {
   return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
 }
 
+// Register-phase ops arrive in "slot space" (the encoder rewrites them when
+// the phase's register slots are known): a control / pattern over local bits
+// is split into its thread part (lmask, lval over the non-register local
+// bits) and its register part (zl = rm | rv << 16 over slots), so a thread
+// needs only its tile base and its thread bits.
 struct TileCtx {
   uint64_t base;       // global bits of this tile
   uint32_t lt;         // thread's local base (thread bits placed)
-  uint32_t rb[kRegBits];  // local bit mask of each register slot
 };
-
-__device__ __forceinline__ uint32_t lidx(const TileCtx& c, int j) {
-  uint32_t l = c.lt;
-#pragma unroll
-  for (int i = 0; i < kRegBits; ++i)
-    if ((j >> i) & 1) l |= c.rb[i];
-  return l;
-}
 
 __device__ __forceinline__ bool lcond(const TileOp& op, uint32_t l) {
   return (l & op.lmask) == op.lval;
 }
 
-// A control / pattern test (l & mask) == val split into the thread's part
-// (fixed for the phase) and the register-slot part (compile-time in j).
 struct SplitCond {
   bool t_ok;
   uint32_t rm, rv;  // over register slots
 };
 
-__device__ __forceinline__ SplitCond split_cond(const TileCtx& c, uint32_t mask, uint32_t val) {
+__device__ __forceinline__ SplitCond split_cond(const TileCtx& c, const TileOp& op) {
   SplitCond sc;
-  sc.rm = 0;
-  sc.rv = 0;
-  uint32_t regmask = 0;
-#pragma unroll
-  for (int i = 0; i < kRegBits; ++i) {
-    regmask |= c.rb[i];
-    if (mask & c.rb[i]) {
-      sc.rm |= 1u << i;
-      if (val & c.rb[i]) sc.rv |= 1u << i;
-    }
-  }
-  const uint32_t tm = mask & ~regmask;
-  sc.t_ok = (c.lt & tm) == (val & tm);
+  sc.rm = op.zl & 0xffffu;
+  sc.rv = op.zl >> 16;
+  sc.t_ok = (c.lt & op.lmask) == op.lval;
   return sc;
 }
 
@@ -119,14 +103,161 @@ __device__ __forceinline__ void t_dense1(double2 (&v)[kRegs], const TileCtx& c, 
   const double2 m00 = (data[op.data + 0]), m01 = (data[op.data + 1]);
   const double2 m10 = (data[op.data + 2]), m11 = (data[op.data + 3]);
   SplitCond sc{true, 0, 0};
-  if (op.lmask) {
-    sc = split_cond(c, op.lmask, op.lval);
+  if (op.lmask | op.zl) {
+    sc = split_cond(c, op);
     if (!sc.t_ok) return;
   }
   if (sc.rm)
     t_dense1_body<I, true>(v, sc, m00, m01, m10, m11);
   else
     t_dense1_body<I, false>(v, sc, m00, m01, m10, m11);
+}
+
+// real 2x2 [[a, b], [c, d]]: 4 FP64 ops per amplitude instead of 8
+template <int I, bool CTRL>
+__device__ __forceinline__ void t_real1_body(double2 (&v)[kRegs], const SplitCond& sc, double a,
+                                             double b, double c, double d) {
+#pragma unroll
+  for (int j = 0; j < kRegs; ++j) {
+    if ((j >> I) & 1) continue;
+    const int q = j | (1 << I);
+    const double2 x = v[j], y = v[q];
+    const double2 nx = make_double2(fma(b, y.x, a * x.x), fma(b, y.y, a * x.y));
+    const double2 ny = make_double2(fma(d, y.x, c * x.x), fma(d, y.y, c * x.y));
+    if (CTRL) {
+      const bool ok = jcond(sc, j);
+      v[j].x = ok ? nx.x : x.x;
+      v[j].y = ok ? nx.y : x.y;
+      v[q].x = ok ? ny.x : y.x;
+      v[q].y = ok ? ny.y : y.y;
+    } else {
+      v[j] = nx;
+      v[q] = ny;
+    }
+  }
+}
+
+// X on a register slot: a predicated swap, no arithmetic
+template <int I>
+__device__ __forceinline__ void t_swap_body(double2 (&v)[kRegs], const SplitCond& sc) {
+#pragma unroll
+  for (int j = 0; j < kRegs; ++j) {
+    if ((j >> I) & 1) continue;
+    const int q = j | (1 << I);
+    const double2 x = v[j], y = v[q];
+    const bool ok = jcond(sc, j);
+    v[j].x = ok ? y.x : x.x;
+    v[j].y = ok ? y.y : x.y;
+    v[q].x = ok ? x.x : y.x;
+    v[q].y = ok ? x.y : y.y;
+  }
+}
+
+template <int I>
+__device__ __forceinline__ void t_real1(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
+                                        const double2* data) {
+  SplitCond sc{true, 0, 0};
+  if (op.lmask | op.zl) {
+    sc = split_cond(c, op);
+    if (!sc.t_ok) return;
+  }
+  if (op.flags & 1) {  // X
+    t_swap_body<I>(v, sc);
+    return;
+  }
+  const double2 ab = data[op.data], cd = data[op.data + 1];
+  if (sc.rm)
+    t_real1_body<I, true>(v, sc, ab.x, ab.y, cd.x, cd.y);
+  else
+    t_real1_body<I, false>(v, sc, ab.x, ab.y, cd.x, cd.y);
+}
+
+// batched uncontrolled 1-qubit ops on the slots of a mask (slot order)
+__device__ __forceinline__ void t_real1x(double2 (&v)[kRegs], const TileOp& op,
+                                         const double2* data) {
+  const double2* M = data + op.data;
+  const SplitCond sc{true, 0, 0};
+  const int s = op.slots;
+#define QSV_REAL_SLOT(I)                                                   \
+  if ((s >> (I)) & 1) {                                                    \
+    const double2 ab = M[0], cd = M[1];                                    \
+    t_real1_body<(I) % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y);    \
+    M += 2;                                                                \
+  }
+  QSV_REAL_SLOT(0) QSV_REAL_SLOT(1) QSV_REAL_SLOT(2) QSV_REAL_SLOT(3) QSV_REAL_SLOT(4)
+#undef QSV_REAL_SLOT
+}
+
+__device__ __forceinline__ void t_dense1x(double2 (&v)[kRegs], const TileOp& op,
+                                          const double2* data) {
+  const double2* M = data + op.data;
+  const SplitCond sc{true, 0, 0};
+  const int s = op.slots;
+#define QSV_DENSE_SLOT(I)                                                  \
+  if ((s >> (I)) & 1) {                                                    \
+    t_dense1_body<(I) % kRegBits, false>(v, sc, M[0], M[1], M[2], M[3]);   \
+    M += 4;                                                                \
+  }
+  QSV_DENSE_SLOT(0) QSV_DENSE_SLOT(1) QSV_DENSE_SLOT(2) QSV_DENSE_SLOT(3) QSV_DENSE_SLOT(4)
+#undef QSV_DENSE_SLOT
+}
+
+// sign flip of amplitude slot J when bit J of `bits` is set: one shift and
+// two LOP3 on the integer pipe, no FP64 work
+template <int J>
+__device__ __forceinline__ double2 neg_bit(double2 v, uint32_t bits) {
+  const int s = (int)((bits << (31 - J)) & 0x80000000u);
+  return make_double2(__hiloint2double(__double2hiint(v.x) ^ s, __double2loint(v.x)),
+                      __hiloint2double(__double2hiint(v.y) ^ s, __double2loint(v.y)));
+}
+
+template <int J>
+struct NegAll {
+  __device__ __forceinline__ static void run(double2 (&v)[kRegs], uint32_t bits) {
+    NegAll<J - 1>::run(v, bits);
+    v[J] = neg_bit<J>(v[J], bits);
+  }
+};
+template <>
+struct NegAll<0> {
+  __device__ __forceinline__ static void run(double2 (&v)[kRegs], uint32_t bits) {
+    v[0] = neg_bit<0>(v[0], bits);
+  }
+};
+
+// merged diagonal: v[j] *= T[j] * C(thread) * (-1)^(sign(j, thread))
+__device__ __forceinline__ void t_flush(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
+                                        const double2* data) {
+  const bool table = op.flags & 1;
+  const double2* T = data + op.data;
+  const FlushSign* sg = reinterpret_cast<const FlushSign*>(T + (table ? kRegs : 0));
+  // sign bits over the 2^kRegBits slots: the table's own signs, then the
+  // linear rules (j_slot parity patterns are the constant columns below)
+  uint32_t bits = table ? 0u : op.lmask;
+  for (int r = 0; r < op.m; ++r) {
+    const FlushSign R = sg[r];
+    if ((c.lt & R.lm) == R.lv && (c.base & R.gm) == R.gv) bits ^= R.col;
+  }
+  const FlushFactor* fc = reinterpret_cast<const FlushFactor*>(sg + op.m);
+  double2 C = make_double2(1.0, 0.0);
+  for (int f = 0; f < op.slots; ++f) {
+    const int p = fc[f].pos;
+    const int bit = p >= 0 ? (int)((c.lt >> p) & 1u) : (int)((c.base >> (-p - 1)) & 1ULL);
+    C = cmul(C, bit ? fc[f].d1 : fc[f].d0);
+  }
+  if (table) {
+    if (op.slots) {
+#pragma unroll
+      for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], cmul(T[j], C));
+    } else {
+#pragma unroll
+      for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], T[j]);
+    }
+  } else if (op.slots) {
+#pragma unroll
+    for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], C);
+  }
+  if (bits) NegAll<kRegs - 1>::run(v, bits);
 }
 
 __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
@@ -143,18 +274,26 @@ __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, c
         case 16: t_dense1<4 % kRegBits>(v, c, op, data); break;
       }
       break;
-    case T_DENSE1XR: {
-      const double2* M = data + op.data;
-      const SplitCond sc{true, 0, 0};
-      t_dense1_body<0, false>(v, sc, M[0], M[1], M[2], M[3]);
-      t_dense1_body<1 % kRegBits, false>(v, sc, M[4], M[5], M[6], M[7]);
-      if (op.m > 2) t_dense1_body<2 % kRegBits, false>(v, sc, M[8], M[9], M[10], M[11]);
-      if (op.m > 3) t_dense1_body<3 % kRegBits, false>(v, sc, M[12], M[13], M[14], M[15]);
-      if (op.m > 4) t_dense1_body<4 % kRegBits, false>(v, sc, M[16], M[17], M[18], M[19]);
+    case T_REAL1:
+      switch (op.slots) {
+        case 1: t_real1<0>(v, c, op, data); break;
+        case 2: t_real1<1 % kRegBits>(v, c, op, data); break;
+        case 4: t_real1<2 % kRegBits>(v, c, op, data); break;
+        case 8: t_real1<3 % kRegBits>(v, c, op, data); break;
+        case 16: t_real1<4 % kRegBits>(v, c, op, data); break;
+      }
       break;
-    }
+    case T_REAL1X:
+      t_real1x(v, op, data);
+      break;
+    case T_DENSE1X:
+      t_dense1x(v, op, data);
+      break;
+    case T_FLUSH:
+      t_flush(v, c, op, data);
+      break;
     case T_PHASE: {
-      const SplitCond sc = split_cond(c, op.lmask, op.lval);
+      const SplitCond sc = split_cond(c, op);
       if (!sc.t_ok) break;
       if (op.flags & 2) {
 #pragma unroll
@@ -172,25 +311,18 @@ __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, c
       break;
     }
     case T_DIAG: {
-      const SplitCond sc = split_cond(c, op.lmask, op.lval);
+      const SplitCond sc = split_cond(c, op);
       if (!sc.t_ok) break;
-      // per target: tile/thread constant bit, or register slot
+      // per target: register slot (0..7), thread bit (8 + bit) or tile bit (< 0)
       int fixed_sub = 0;
       int slot[4] = {-1, -1, -1, -1};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         if (t >= op.m) continue;
         const int p = op.tpos[t];
-        if (p < 0) {
-          fixed_sub |= (int)((c.base >> (-p - 1)) & 1ULL) << t;
-        } else {
-          int s = -1;
-#pragma unroll
-          for (int i = 0; i < kRegBits; ++i)
-            if (c.rb[i] == (1u << p)) s = i;
-          if (s < 0) fixed_sub |= (int)((c.lt >> p) & 1u) << t;
-          slot[t] = s;
-        }
+        if (p < 0) fixed_sub |= (int)((c.base >> (-p - 1)) & 1ULL) << t;
+        else if (p >= 8) fixed_sub |= (int)((c.lt >> (p - 8)) & 1u) << t;
+        else slot[t] = p;
       }
       const double2* tab = data + op.data;
       if (op.m == 1 && slot[0] >= 0) {
@@ -222,10 +354,7 @@ __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, c
       const double2 f0 = (data[op.data]), f1 = (data[op.data + 1]);
       // parity = tile part ^ thread part ^ register part
       int par0 = (__popcll(c.base & op.zg) ^ __popc(c.lt & op.zl)) & 1;
-      uint32_t rz = 0;
-#pragma unroll
-      for (int i = 0; i < kRegBits; ++i)
-        if (op.zl & c.rb[i]) rz |= 1u << i;
+      const uint32_t rz = (uint32_t)op.m;  // register part (slot mask)
 #pragma unroll
       for (int j = 0; j < kRegs; ++j) {
         const int p = (par0 ^ __popc((uint32_t)j & rz)) & 1;
@@ -317,6 +446,47 @@ __device__ __noinline__ void s_apply(double2* sm, int L, const TileOp& op,
     case 2: s_dense<2>(sm, L, op, data, tid); break;
     case 3: s_dense<3>(sm, L, op, data, tid); break;
     case 4: s_dense<4>(sm, L, op, data, tid); break;
+  }
+}
+
+// One register phase of one thread: load its 2^kRegBits amplitudes from the
+// tile in shared memory, run the phase's ops in registers, store them back.
+__device__ __forceinline__ void reg_phase(double2* sm, const TilePhase& P, const TileOp* ops,
+                                       const double2* data, uint64_t base, int tid, int nthr,
+                                       bool skip_ops, int dbg) {
+  TileCtx c;
+  c.base = base;
+  c.lt = 0;
+  for (int j = 0; j < nthr; ++j)
+    if ((tid >> j) & 1) c.lt |= 1u << P.thrpos[j];
+  // the swizzle is XOR-linear: swz(lt | r) = swz(lt) ^ swz(r)
+  uint32_t srb[kRegBits];
+#pragma unroll
+  for (int i = 0; i < kRegBits; ++i) srb[i] = swz(1u << P.regpos[i]);
+  const uint32_t slt = swz(c.lt);
+  double2 v[kRegs];
+#pragma unroll
+  for (int j = 0; j < kRegs; ++j) {
+    uint32_t ad = slt;
+#pragma unroll
+    for (int i = 0; i < kRegBits; ++i)
+      if ((j >> i) & 1) ad ^= srb[i];
+    v[j] = sm[ad];
+  }
+  const int ob = P.op_begin, oe = skip_ops ? P.op_begin : P.op_end;
+  for (int o = ob; o < oe; ++o) {
+    const TileOp& op = ops[o];
+    const bool dense1 = op.kind == T_DENSE1 || op.kind == T_DENSE1X || op.kind == T_REAL1 ||
+                        op.kind == T_REAL1X;
+    if (!((dbg & 4) && !dense1) && !((dbg & 8) && dense1)) t_apply(v, c, op, data);
+  }
+#pragma unroll
+  for (int j = 0; j < kRegs; ++j) {
+    uint32_t ad = slt;
+#pragma unroll
+    for (int i = 0; i < kRegBits; ++i)
+      if ((j >> i) & 1) ad ^= srb[i];
+    sm[ad] = v[j];
   }
 }
 
@@ -418,43 +588,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         }
         continue;
       }
-      TileCtx c;
-      c.base = base;
-      c.lt = 0;
-      for (int j = 0; j < nthr; ++j)
-        if ((tid >> j) & 1) c.lt |= 1u << P.thrpos[j];
-#pragma unroll
-      for (int i = 0; i < kRegBits; ++i) c.rb[i] = 1u << P.regpos[i];
-      if (active) {
-        // the swizzle is XOR-linear: swz(lt | r) = swz(lt) ^ swz(r)
-        uint32_t srb[kRegBits];
-#pragma unroll
-        for (int i = 0; i < kRegBits; ++i) srb[i] = swz(c.rb[i]);
-        const uint32_t slt = swz(c.lt);
-        double2 v[kRegs];
-#pragma unroll
-        for (int j = 0; j < kRegs; ++j) {
-          uint32_t ad = slt;
-#pragma unroll
-          for (int i = 0; i < kRegBits; ++i)
-            if ((j >> i) & 1) ad ^= srb[i];
-          v[j] = sm[ad];
-        }
-        for (int o = ob; o < (skip_ops ? ob : oe); ++o) {
-          const TileOp& op = ops[o];
-          if (!((dbg & 4) && op.kind != T_DENSE1 && op.kind != T_DENSE1XR) &&
-              !((dbg & 8) && (op.kind == T_DENSE1 || op.kind == T_DENSE1XR)))
-            t_apply(v, c, op, data);
-        }
-#pragma unroll
-        for (int j = 0; j < kRegs; ++j) {
-          uint32_t ad = slt;
-#pragma unroll
-          for (int i = 0; i < kRegBits; ++i)
-            if ((j >> i) & 1) ad ^= srb[i];
-          sm[ad] = v[j];
-        }
-      }
+      if (active) reg_phase(sm, P, ops, data, base, tid, nthr, skip_ops, dbg);
       group_sync(group);
     }
 
@@ -634,6 +768,9 @@ PassSel select_pass(int n, int L, const std::vector<GateDesc>& gates,
     size_t cost = sizeof(TileOp) + sizeof(TilePhase) + 32;
     if (g.kind == QSV_OP_DENSE) cost += sizeof(double2) << (2 * g.m);
     if (g.kind == QSV_OP_DIAG) cost += sizeof(double2) << g.m;
+    // merged diagonal flushes: at most one table per R op, one rule per D op
+    if (g.kind == QSV_OP_DENSE && g.m == 1) cost += sizeof(TileOp) + sizeof(double2) * kRegs;
+    else cost += sizeof(FlushFactor);
     if (cost > budget) break;
     const uint64_t T = touched_mask(gates[i]);
     if (!ok[i] || (T & blocked)) {
@@ -687,7 +824,270 @@ struct Encoded {
   std::vector<TilePhase> phases;
   std::vector<TileOp> ops;
   std::vector<Cplx> data;
+  double fp64_ops_per_amp = 0;  // FP64 pipe operations per amplitude
 };
+
+Cplx cconj(Cplx a) { return {a.re, -a.im}; }
+bool is_one_c(Cplx a) { return a.re == 1.0 && a.im == 0.0; }
+bool is_real_mat(const Cplx* M, int n) {
+  for (int i = 0; i < n; ++i)
+    if (M[i].im != 0.0) return false;
+  return true;
+}
+
+// Register-phase scheduling.  Inside one register phase every op is either
+// an R op (a 2x2 acting non-diagonally on one register slot, possibly with
+// controls) or a D op (diagonal).  D ops commute with each other and with R
+// ops on other qubits, so the phase is re-ordered into alternating layers
+// "all ready D ops, then all ready R ops": each D layer becomes ONE merged
+// T_FLUSH (a 2^kRegBits table over the register slots, linear sign rules
+// for sign patterns that involve thread / tile bits, per-thread factors for
+// 1-qubit diagonals on non-register qubits) and each R layer runs as
+// batched register arithmetic.
+struct PhaseOp {
+  TileOp op;
+  std::vector<Cplx> data;
+  bool isR = false;
+  uint32_t nd = 0, sup = 0;  // local bits acted on non-diagonally / touched
+};
+
+void emit_op(Encoded& e, TileOp op, const std::vector<Cplx>& data) {
+  op.data = (uint32_t)e.data.size();
+  e.data.insert(e.data.end(), data.begin(), data.end());
+  e.ops.push_back(op);
+}
+
+// Merge a layer of D ops: returns the ops that could not be merged.
+std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, const int* regpos) {
+  uint32_t Rall = 0;
+  int slot_of[32];
+  for (int b = 0; b < 32; ++b) slot_of[b] = -1;
+  for (int i = 0; i < kRegBits; ++i) {
+    Rall |= 1u << regpos[i];
+    slot_of[regpos[i]] = i;
+  }
+  std::vector<Cplx> T(kRegs, Cplx{1, 0});
+  std::vector<FlushSign> signs;
+  std::vector<FlushFactor> facs;
+  std::vector<PhaseOp> rest;
+  bool changed = false;
+  auto jpat = [&](uint32_t mask, uint32_t val, uint32_t* jm, uint32_t* jv) {
+    *jm = 0;
+    *jv = 0;
+    for (int b = 0; b < 32; ++b)
+      if (((mask >> b) & 1u) && slot_of[b] >= 0) {
+        *jm |= 1u << slot_of[b];
+        if ((val >> b) & 1u) *jv |= 1u << slot_of[b];
+      }
+  };
+  for (const PhaseOp& po : dl) {
+    const TileOp& op = po.op;
+    if (op.kind == T_PHASE) {
+      const Cplx f = (op.flags & 2) ? Cplx{-1, 0} : po.data[0];
+      uint32_t jm, jv;
+      jpat(op.lmask, op.lval, &jm, &jv);
+      const uint32_t tm = op.lmask & ~Rall;
+      if (op.gmask == 0 && tm == 0) {
+        for (int j = 0; j < kRegs; ++j)
+          if (((uint32_t)j & jm) == jv) T[j] = cm(T[j], f);
+        changed = true;
+        continue;
+      }
+      if (f.re == -1.0 && f.im == 0.0 && __builtin_popcount(jm) <= 1) {
+        FlushSign r;
+        memset(&r, 0, sizeof(r));
+        r.lm = tm;
+        r.lv = op.lval & tm;
+        r.gm = op.gmask;
+        r.gv = op.gval;
+        // slots j where the register part of the pattern holds
+        for (int j = 0; j < kRegs; ++j)
+          if (((uint32_t)j & jm) == jv) r.col |= 1u << j;
+        signs.push_back(r);
+        changed = true;
+        continue;
+      }
+    } else if (op.kind == T_DIAG) {
+      bool all_reg = true;
+      for (int t = 0; t < op.m; ++t)
+        if (op.tpos[t] < 0 || slot_of[(int)op.tpos[t]] < 0) all_reg = false;
+      if (all_reg && op.gmask == 0 && (op.lmask & ~Rall) == 0) {
+        uint32_t jm, jv;
+        jpat(op.lmask, op.lval, &jm, &jv);
+        for (int j = 0; j < kRegs; ++j) {
+          if (((uint32_t)j & jm) != jv) continue;
+          int sub = 0;
+          for (int t = 0; t < op.m; ++t) sub |= ((j >> slot_of[(int)op.tpos[t]]) & 1) << t;
+          T[j] = cm(T[j], po.data[sub]);
+        }
+        changed = true;
+        continue;
+      }
+      if (op.m == 1 && op.lmask == 0 && op.gmask == 0) {  // non-register qubit
+        FlushFactor f;
+        memset(&f, 0, sizeof(f));
+        f.pos = op.tpos[0];
+        f.d0 = make_double2(po.data[0].re, po.data[0].im);
+        f.d1 = make_double2(po.data[1].re, po.data[1].im);
+        facs.push_back(f);
+        changed = true;
+        continue;
+      }
+    }
+    rest.push_back(po);
+  }
+  if (!changed) return rest;
+  bool table = false;
+  uint32_t tsign = 0;
+  for (int j = 0; j < kRegs; ++j) {
+    if (T[j].im != 0.0 || (T[j].re != 1.0 && T[j].re != -1.0)) table = true;
+    if (T[j].re == -1.0 && T[j].im == 0.0) tsign |= 1u << j;
+  }
+  if (!table && tsign == 0 && signs.empty() && facs.empty()) return rest;
+  TileOp op;
+  memset(&op, 0, sizeof(op));
+  op.kind = T_FLUSH;
+  op.flags = table ? 1 : 0;
+  op.m = (int32_t)signs.size();
+  op.slots = (int32_t)facs.size();
+  op.lmask = table ? 0 : tsign;
+  std::vector<Cplx> data;
+  if (table) data = T;
+  for (const FlushSign& r : signs) {
+    Cplx w[2];
+    memcpy(w, &r, sizeof(r));
+    data.push_back(w[0]);
+    data.push_back(w[1]);
+  }
+  for (const FlushFactor& f : facs) {
+    Cplx w[3];
+    memcpy(w, &f, sizeof(f));
+    for (int k = 0; k < 3; ++k) data.push_back(w[k]);
+  }
+  emit_op(e, op, data);
+  e.fp64_ops_per_amp += (table ? 4.0 : 0.0) + (facs.empty() ? 0.0 : 4.0);
+  return rest;
+}
+
+double d_op_cost(const TileOp& op) {
+  if (op.kind == T_PHASE) return (op.flags & 2) ? 0.0 : 4.0;
+  return 4.0;  // T_DIAG / T_PARITY: one complex multiply per amplitude
+}
+
+void emit_rlayer(Encoded& e, const std::vector<PhaseOp>& rl) {
+  // uncontrolled 1-qubit ops are collected into slot-mask batches; a batch
+  // stays open while every op emitted after it commutes with the joiner
+  struct Batch {
+    bool real;
+    int slots = 0;
+    std::vector<Cplx> mat[kRegBits];
+    size_t pos;  // index into `seq`
+    uint32_t after_nd = 0, after_sup = 0;
+  };
+  std::vector<int> seq;              // >= 0: rl index, < 0: -(batch)-1
+  std::vector<Batch> batches;
+  int open = -1;
+  for (size_t k = 0; k < rl.size(); ++k) {
+    const PhaseOp& po = rl[k];
+    const int slot = __builtin_ctz((uint32_t)po.op.slots);
+    const bool real = po.op.kind == T_REAL1;
+    const bool plain = po.op.lmask == 0 && po.op.gmask == 0 && !(po.op.flags & 1);
+    if (plain) {
+      if (open >= 0) {
+        Batch& B = batches[open];
+        if (B.real == real && !((B.slots >> slot) & 1) && !(po.nd & B.after_sup) &&
+            !(po.sup & B.after_nd)) {
+          B.slots |= 1 << slot;
+          B.mat[slot] = po.data;
+          continue;
+        }
+      }
+      Batch B;
+      B.real = real;
+      B.slots = 1 << slot;
+      B.mat[slot] = po.data;
+      B.pos = seq.size();
+      batches.push_back(B);
+      open = (int)batches.size() - 1;
+      seq.push_back(-open - 1);
+      continue;
+    }
+    seq.push_back((int)k);
+    if (open >= 0) {
+      batches[open].after_nd |= po.nd;
+      batches[open].after_sup |= po.sup;
+    }
+  }
+  for (int x : seq) {
+    if (x >= 0) {
+      const PhaseOp& po = rl[x];
+      emit_op(e, po.op, po.data);
+      e.fp64_ops_per_amp += (po.op.flags & 1) ? 0.0 : (po.op.kind == T_REAL1 ? 4.0 : 8.0);
+      continue;
+    }
+    const Batch& B = batches[-x - 1];
+    TileOp op;
+    memset(&op, 0, sizeof(op));
+    std::vector<Cplx> data;
+    const int cnt = __builtin_popcount(B.slots);
+    if (cnt == 1) {
+      const int slot = __builtin_ctz(B.slots);
+      op.kind = B.real ? T_REAL1 : T_DENSE1;
+      op.slots = B.slots;
+      data = B.mat[slot];
+    } else {
+      op.kind = B.real ? T_REAL1X : T_DENSE1X;
+      op.slots = B.slots;
+      op.m = cnt;
+      for (int i = 0; i < kRegBits; ++i)
+        if ((B.slots >> i) & 1) data.insert(data.end(), B.mat[i].begin(), B.mat[i].end());
+    }
+    emit_op(e, op, data);
+    e.fp64_ops_per_amp += cnt * (B.real ? 4.0 : 8.0);
+  }
+}
+
+// Rewrite a register-phase op into slot space once the phase's register
+// slots are known: controls / patterns split into a thread part (lmask,
+// lval) and a register part (zl = rm | rv << 16); diagonal targets become a
+// slot (0..7) or 8 + thread bit; parity masks a slot mask in m.
+void to_slot_space(TileOp& op, const int* slot_of, uint32_t Rall) {
+  auto split = [&](uint32_t mask, uint32_t val) {
+    uint32_t rm = 0, rv = 0;
+    for (int b = 0; b < 32; ++b)
+      if (((mask >> b) & 1u) && slot_of[b] >= 0) {
+        rm |= 1u << slot_of[b];
+        if ((val >> b) & 1u) rv |= 1u << slot_of[b];
+      }
+    op.zl = rm | (rv << 16);
+    op.lmask = mask & ~Rall;
+    op.lval = val & ~Rall;
+  };
+  switch (op.kind) {
+    case T_DENSE1:
+    case T_REAL1:
+    case T_PHASE:
+      split(op.lmask, op.lval);
+      break;
+    case T_DIAG:
+      split(op.lmask, op.lval);
+      for (int t = 0; t < op.m; ++t) {
+        const int p = op.tpos[t];
+        if (p >= 0) op.tpos[t] = (int8_t)(slot_of[p] >= 0 ? slot_of[p] : 8 + p);
+      }
+      break;
+    case T_PARITY: {
+      uint32_t rz = 0;
+      for (int b = 0; b < 32; ++b)
+        if (((op.zl >> b) & 1u) && slot_of[b] >= 0) rz |= 1u << slot_of[b];
+      op.m = (int32_t)rz;
+      op.zl &= ~Rall;
+      break;
+    }
+    default:
+      break;  // T_FLUSH and the batches are built in slot space
+  }
+}
 
 // Build phases and ops of one pass.
 Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>& pg) {
@@ -706,19 +1106,21 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
         local_of[q] = j++;
       }
   }
-  // current register phase
+  // current register phase: ops collected with their own data, scheduled at close
   bool open = false;
   uint32_t R = 0;
-  size_t op_begin = 0;
-  std::vector<std::pair<size_t, int>> d1;  // (op index, local bit) of T_DENSE1 ops
-  auto close = [&]() {
+  std::vector<PhaseOp> cur;
+  std::vector<int> d1bit;  // local target bit of each 1-qubit op in `cur` (-1 otherwise)
+  std::vector<PhaseOp> carry;  // trailing D layer handed to the next register phase
+  // carry_ok: the next phase is a register phase, so a trailing D layer can
+  // be merged into that phase's first flush instead of running on its own
+  auto close = [&](bool carry_ok) {
     if (!open) return;
-    // register slots in order of first use by a 1-qubit dense op, so runs of
-    // such ops land on slots 0, 1, ... and can be batched
+    // register slots in order of first use by a 1-qubit op, then the other
+    // R bits, then filled with the highest remaining bits
     std::vector<int> order;
-    for (auto& pr : d1)
-      if (std::find(order.begin(), order.end(), pr.second) == order.end())
-        order.push_back(pr.second);
+    for (int b : d1bit)
+      if (b >= 0 && std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
     for (int b = 0; b < L; ++b)
       if (((R >> b) & 1u) && std::find(order.begin(), order.end(), b) == order.end())
         order.push_back(b);
@@ -740,48 +1142,94 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
       if (!((Rall >> b) & 1u)) tb.push_back(b);
     order_thread_bits(tb);
     for (size_t k = 0; k < tb.size(); ++k) ph.thrpos[k] = tb[k];
-    for (auto& pr : d1) e.ops[pr.first].slots = 1 << slot_of[pr.second];
-    // batch runs of >= 2 uncontrolled 1-qubit dense ops on slots 0, 1, ... in order
-    {
-      std::vector<TileOp> merged;
-      const size_t end = e.ops.size();
-      size_t k = op_begin;
-      while (k < end) {
-        int len = 0;
-        while (k + len < end && len < kRegBits) {
-          const TileOp& o = e.ops[k + len];
-          if (!(o.kind == T_DENSE1 && o.slots == (1 << len) && o.lmask == 0 && o.gmask == 0 &&
-                o.data == e.ops[k].data + 4 * len))
-            break;
-          ++len;
-        }
-        if (len >= 2) {
-          TileOp b = e.ops[k];
-          b.kind = T_DENSE1XR;
-          b.m = len;
-          b.slots = (1 << len) - 1;
-          merged.push_back(b);
-          k += len;
-        } else {
-          merged.push_back(e.ops[k]);
-          ++k;
+    // classify
+    const size_t K = cur.size();
+    for (size_t k = 0; k < K; ++k) {
+      PhaseOp& po = cur[k];
+      if (d1bit[k] >= 0) {
+        po.op.slots = 1 << slot_of[d1bit[k]];
+        po.isR = true;
+        po.nd = 1u << d1bit[k];
+        po.sup = po.nd | po.op.lmask;
+      } else {
+        po.isR = false;
+        po.nd = 0;
+        if (po.op.kind == T_PHASE) po.sup = po.op.lmask;
+        else if (po.op.kind == T_PARITY) po.sup = po.op.zl;
+        else {
+          po.sup = po.op.lmask;
+          for (int t = 0; t < po.op.m; ++t)
+            if (po.op.tpos[t] >= 0) po.sup |= 1u << po.op.tpos[t];
         }
       }
-      e.ops.resize(op_begin);
-      e.ops.insert(e.ops.end(), merged.begin(), merged.end());
     }
-    ph.op_begin = (int)op_begin;
+    // dependencies (i < j): R-R share a non-diagonal bit, R-D share the R bit
+    std::vector<std::vector<int>> pred(K);
+    for (size_t j = 0; j < K; ++j)
+      for (size_t i = 0; i < j; ++i) {
+        const PhaseOp &a = cur[i], &b = cur[j];
+        bool dep;
+        if (a.isR && b.isR) dep = (a.nd & b.sup) || (b.nd & a.sup);
+        else if (a.isR) dep = a.nd & b.sup;
+        else if (b.isR) dep = b.nd & a.sup;
+        else dep = false;
+        if (dep) pred[j].push_back((int)i);
+      }
+    std::vector<char> done(K, 0);
+    size_t left = K;
+    ph.op_begin = (int)e.ops.size();
+    while (left) {
+      auto ready = [&](size_t k) {
+        for (int p : pred[k])
+          if (!done[p]) return false;
+        return true;
+      };
+      std::vector<PhaseOp> dl, rl;
+      for (size_t k = 0; k < K; ++k)
+        if (!done[k] && !cur[k].isR && ready(k)) dl.push_back(cur[k]);
+      for (size_t k = 0; k < K; ++k)
+        if (!done[k] && !cur[k].isR && ready(k)) done[k] = 1;
+      for (size_t k = 0; k < K; ++k)  // preds have lower indices: one scan closes chains
+        if (!done[k] && cur[k].isR && ready(k)) {
+          done[k] = 1;
+          rl.push_back(cur[k]);
+        }
+      left -= dl.size() + rl.size();
+      if (dl.empty() && rl.empty()) break;  // cannot happen (the DAG is acyclic)
+      if (carry_ok && rl.empty() && left == 0) {
+        carry = dl;
+        break;
+      }
+      for (const PhaseOp& po : emit_flush(e, dl, ph.regpos)) {
+        emit_op(e, po.op, po.data);
+        e.fp64_ops_per_amp += d_op_cost(po.op);
+      }
+      emit_rlayer(e, rl);
+    }
     ph.op_end = (int)e.ops.size();
-    e.phases.push_back(ph);
+    for (int o = ph.op_begin; o < ph.op_end; ++o) to_slot_space(e.ops[o], slot_of, Rall);
+    if (ph.op_end > ph.op_begin) e.phases.push_back(ph);
     open = false;
     R = 0;
-    d1.clear();
+    cur.clear();
+    d1bit.clear();
   };
   auto open_reg = [&]() {
     if (open) return;
     open = true;
     R = 0;
-    op_begin = e.ops.size();
+    for (const PhaseOp& po : carry) {
+      cur.push_back(po);
+      d1bit.push_back(-1);
+    }
+    carry.clear();
+  };
+  auto push_cur = [&](const TileOp& op, std::vector<Cplx> data, int bit) {
+    PhaseOp po;
+    po.op = op;
+    po.data = std::move(data);
+    cur.push_back(po);
+    d1bit.push_back(bit);
   };
   for (const GateDesc* gp : pg) {
     const GateDesc& g = *gp;
@@ -797,38 +1245,56 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
         if (g.cv[c]) op.gval |= 1ULL << q;
       }
     }
-    op.data = (uint32_t)e.data.size();
     if (g.kind == QSV_OP_DENSE && g.m == 1) {
       const int b = local_of[g.targets[0]];
       open_reg();
       if (!((R >> b) & 1u) && __builtin_popcount(R) >= kRegBits) {
-        close();
+        close(true);
         open_reg();
       }
       R |= 1u << b;
-      op.kind = T_DENSE1;
+      if (g.rf) {  // diag(b) as a D op in front of the real rotation
+        if (!(is_one_c(g.rf_b[0]) && is_one_c(g.rf_b[1]))) {
+          TileOp dop;
+          memset(&dop, 0, sizeof(dop));
+          dop.kind = T_DIAG;
+          dop.m = 1;
+          dop.tpos[0] = (int8_t)b;
+          push_cur(dop, {g.rf_b[0], g.rf_b[1]}, -1);
+        }
+        op.kind = T_REAL1;
+        if (g.rf_r[0] == 0.0 && g.rf_r[3] == 0.0 && g.rf_r[1] == 1.0 && g.rf_r[2] == 1.0)
+          op.flags |= 1;
+        push_cur(op, {{g.rf_r[0], g.rf_r[1]}, {g.rf_r[2], g.rf_r[3]}}, b);
+        continue;
+      }
       const Cplx* M = g.data.data();
-      if (is_zero(M[0]) && is_zero(M[3]) && M[1].re == 1.0 && M[1].im == 0.0 &&
-          M[2].re == 1.0 && M[2].im == 0.0)
-        op.flags |= 1;
-      e.data.insert(e.data.end(), g.data.begin(), g.data.end());
-      d1.push_back({e.ops.size(), b});
-      e.ops.push_back(op);
+      if (is_zero(M[0]) && is_zero(M[3]) && is_one_c(M[1]) && is_one_c(M[2])) op.flags |= 1;
+      std::vector<Cplx> data;
+      if (is_real_mat(M, 4)) {
+        op.kind = T_REAL1;
+        data = {{M[0].re, M[1].re}, {M[2].re, M[3].re}};  // (a, b), (c, d) as double2
+      } else {
+        op.kind = T_DENSE1;
+        op.flags &= ~1;
+        data.assign(g.data.begin(), g.data.end());
+      }
+      push_cur(op, std::move(data), b);
       continue;
     }
     if (g.kind == QSV_OP_DENSE) {  // m = 2..4: shared-memory op
-      close();
+      close(false);
       op.kind = S_DENSE;
       op.m = g.m;
       for (int t = 0; t < g.m; ++t) op.tpos[t] = local_of[g.targets[t]];
-      e.data.insert(e.data.end(), g.data.begin(), g.data.end());
       TilePhase ph;
       memset(&ph, 0, sizeof(ph));
       ph.type = 1;
       ph.op_begin = (int)e.ops.size();
-      e.ops.push_back(op);
+      emit_op(e, op, g.data);
       ph.op_end = (int)e.ops.size();
       e.phases.push_back(ph);
+      e.fp64_ops_per_amp += 4.0 * (double)(1 << g.m);
       continue;
     }
     if (g.kind == QSV_OP_DIAG) {
@@ -837,7 +1303,7 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
         op.kind = T_PHASE;
         const Cplx f = g.data[0];
         if (f.re == -1.0 && f.im == 0.0) op.flags |= 2;
-        e.data.push_back(f);
+        push_cur(op, {f}, -1);
       } else {
         op.kind = T_DIAG;
         op.m = g.m;
@@ -845,9 +1311,8 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
           const int q = g.targets[t];
           op.tpos[t] = local_of[q] >= 0 ? local_of[q] : -(q + 1);
         }
-        e.data.insert(e.data.end(), g.data.begin(), g.data.end());
+        push_cur(op, g.data, -1);
       }
-      e.ops.push_back(op);
       continue;
     }
     // PAULI / PAULI_ROT, uncontrolled
@@ -874,31 +1339,204 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
     if (xm == 0) {
       open_reg();
       op.kind = T_PARITY;
-      e.data.push_back(ca(alpha, bph));
-      e.data.push_back({alpha.re - bph.re, alpha.im - bph.im});
-      e.ops.push_back(op);
+      push_cur(op, {ca(alpha, bph), {alpha.re - bph.re, alpha.im - bph.im}}, -1);
       continue;
     }
-    close();
+    close(false);
     op.kind = S_PAULI;
     uint32_t xl = 0;
     for (int q = 0; q < n; ++q)
       if ((xm >> q) & 1ULL) xl |= 1u << local_of[q];
     op.slots = (int32_t)xl;
-    e.data.push_back(alpha);
-    e.data.push_back(bph);
     TilePhase ph;
     memset(&ph, 0, sizeof(ph));
     ph.type = 1;
     ph.op_begin = (int)e.ops.size();
-    e.ops.push_back(op);
+    emit_op(e, op, {alpha, bph});
     ph.op_end = (int)e.ops.size();
     e.phases.push_back(ph);
+    e.fp64_ops_per_amp += 8.0;
   }
-  close();
+  close(false);
   e.pd.nphases = (int)e.phases.size();
   if (const char* dbg = getenv("QSV_TILE_DEBUG")) e.pd.debug = atoi(dbg);
   return e;
+}
+
+// ------------------------------------------------------- real frames
+// U = diag(a) R diag(b) with R real (Euler: RZ RY RZ up to phase); false if
+// U has no such form (non-unitary shapes), then it stays complex.
+bool euler_real(const M2& U, Cplx a[2], Cplx b[2], double R[4]) {
+  auto mag = [](Cplx z) { return std::hypot(z.re, z.im); };
+  auto ph = [&](Cplx z) {
+    const double r = mag(z);
+    return Cplx{z.re / r, z.im / r};
+  };
+  double mx = 0;
+  for (int i = 0; i < 4; ++i) mx = std::max(mx, mag(U.m[i]));
+  if (!(mx > 0) || !std::isfinite(mx)) return false;
+  const double eps = 1e-12 * mx;
+  const Cplx U00 = U.m[0], U01 = U.m[1], U10 = U.m[2], U11 = U.m[3];
+  Cplx a0{1, 0}, a1{1, 0}, b1{1, 0};
+  const bool h0 = mag(U00) > eps, h1 = mag(U10) > eps;
+  if (h0) a0 = ph(U00);
+  if (h1) a1 = ph(U10);
+  if (h0 && mag(U01) > eps) b1 = cm(ph(U01), cconj(a0));
+  else if (h1 && mag(U11) > eps) b1 = cm(ph(U11), cconj(a1));
+  if (!h0) {
+    if (!(mag(U01) > eps)) return false;
+    a0 = cm(ph(U01), cconj(b1));
+  }
+  if (!h1) {
+    if (!(mag(U11) > eps)) return false;
+    a1 = cm(ph(U11), cconj(b1));
+  }
+  const Cplx A[2] = {a0, a1}, B[2] = {{1, 0}, b1};
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) {
+      const Cplx z = cm(cm(cconj(A[i]), U.m[2 * i + j]), cconj(B[j]));
+      if (std::fabs(z.im) > 1e-13 * mx) return false;
+      R[2 * i + j] = z.re;
+    }
+  a[0] = a0;
+  a[1] = a1;
+  b[0] = B[0];
+  b[1] = B[1];
+  return true;
+}
+
+// qubits a gate acts on non-diagonally
+uint64_t nondiag_mask(const GateDesc& g) {
+  uint64_t m = 0;
+  if (g.kind == QSV_OP_DENSE) {
+    for (int j = 0; j < g.m; ++j) m |= 1ULL << g.targets[j];
+  } else if (g.kind == QSV_OP_PAULI || g.kind == QSV_OP_PAULI_ROT) {
+    for (int j = 0; j < g.m; ++j)
+      if (g.ids[j] == 1 || g.ids[j] == 2) m |= 1ULL << g.targets[j];
+  }
+  return m;
+}
+
+// an uncontrolled 1-qubit diagonal in either canonical form
+bool diag_1q(const GateDesc& g, int* q, Cplx d[2]) {
+  if (g.kind != QSV_OP_DIAG) return false;
+  if (g.m == 1 && g.nc == 0) {
+    *q = g.targets[0];
+    d[0] = g.data[0];
+    d[1] = g.data[1];
+    return true;
+  }
+  if (g.m == 0 && g.nc == 1) {
+    *q = g.cq[0];
+    d[g.cv[0] ? 1 : 0] = g.data[0];
+    d[g.cv[0] ? 0 : 1] = {1, 0};
+    return true;
+  }
+  return false;
+}
+
+GateDesc diag_desc(int q, Cplx d0, Cplx d1) {
+  M2 D;
+  D.m[0] = d0;
+  D.m[1] = {0, 0};
+  D.m[2] = {0, 0};
+  D.m[3] = d1;
+  return canonicalize(desc_from_m2(q, D));
+}
+
+// Every uncontrolled 1-qubit dense gate U on q is written U = diag(a) R diag(b)
+// with R real: diag(b) (applied first) is emitted as a diagonal gate right
+// before R (the tile encoder merges such diagonals of one register phase
+// into a single T_FLUSH), diag(a) stays pending on q and is folded into the
+// next gate on q.  1-qubit diagonals join the pending factor.
+// A gate is only split when the next gate acting non-diagonally on its qubit
+// is again an uncontrolled 1-qubit gate (which absorbs diag(a)); otherwise
+// (a CNOT target, a multi-qubit gate, the end of the circuit) it stays one
+// complex 2x2 that absorbs the pending factor, so no extra flush is needed.
+bool is_plain_1q_dense(const GateDesc& g) {
+  return g.kind == QSV_OP_DENSE && g.m == 1 && g.nc == 0;
+}
+
+std::vector<GateDesc> realify(int n, const std::vector<GateDesc>& in) {
+  // split[i]: the next non-diagonal gate on the target of gate i is plain 1q
+  std::vector<char> split(in.size(), 0);
+  {
+    std::vector<int> next_plain(n, 0);  // scanning backwards
+    for (size_t k = in.size(); k-- > 0;) {
+      const GateDesc& g = in[k];
+      if (is_plain_1q_dense(g)) split[k] = next_plain[g.targets[0]];
+      const uint64_t nd = nondiag_mask(g);
+      for (int q = 0; q < n; ++q)
+        if ((nd >> q) & 1ULL) next_plain[q] = is_plain_1q_dense(g);
+    }
+  }
+  std::vector<GateDesc> out;
+  std::vector<Cplx> p0(n, Cplx{1, 0}), p1(n, Cplx{1, 0});
+  std::vector<char> has(n, 0);
+  auto push = [&](const GateDesc& g) {
+    if (g.nc >= 0) out.push_back(g);
+  };
+  auto flush = [&](int q) {
+    if (!has[q]) return;
+    push(diag_desc(q, p0[q], p1[q]));
+    has[q] = 0;
+    p0[q] = p1[q] = {1, 0};
+  };
+  for (size_t i = 0; i < in.size(); ++i) {
+    const GateDesc& g = in[i];
+    int q;
+    Cplx d[2];
+    if (diag_1q(g, &q, d)) {
+      p0[q] = cm(d[0], p0[q]);
+      p1[q] = cm(d[1], p1[q]);
+      has[q] = !(is_one_c(p0[q]) && is_one_c(p1[q]));
+      continue;
+    }
+    if (g.kind == QSV_OP_DENSE && g.m == 1 && g.nc == 0) {
+      q = g.targets[0];
+      M2 U;
+      for (int k = 0; k < 4; ++k) U.m[k] = g.data[k];
+      if (has[q]) {  // U . diag(p)
+        U.m[0] = cm(U.m[0], p0[q]);
+        U.m[2] = cm(U.m[2], p0[q]);
+        U.m[1] = cm(U.m[1], p1[q]);
+        U.m[3] = cm(U.m[3], p1[q]);
+        has[q] = 0;
+        p0[q] = p1[q] = {1, 0};
+      }
+      Cplx a[2], b[2];
+      double Rm[4];
+      if (!split[i] || !euler_real(U, a, b, Rm)) {
+        push(canonicalize(desc_from_m2(q, U)));
+        continue;
+      }
+      // one gate carrying both factors, so the pass packer cannot separate
+      // diag(b) from R (R diag(b) is what a standalone kernel applies)
+      M2 RB;
+      RB.m[0] = {Rm[0] * b[0].re, Rm[0] * b[0].im};
+      RB.m[1] = {Rm[1] * b[1].re, Rm[1] * b[1].im};
+      RB.m[2] = {Rm[2] * b[0].re, Rm[2] * b[0].im};
+      RB.m[3] = {Rm[3] * b[1].re, Rm[3] * b[1].im};
+      GateDesc gr = desc_from_m2(q, RB);
+      if (gr.kind == QSV_OP_DENSE) {
+        gr.rf = 1;
+        gr.rf_b[0] = b[0];
+        gr.rf_b[1] = b[1];
+        for (int k = 0; k < 4; ++k) gr.rf_r[k] = Rm[k];
+      }
+      push(canonicalize(gr));
+      p0[q] = a[0];
+      p1[q] = a[1];
+      has[q] = !(is_one_c(a[0]) && is_one_c(a[1]));
+      continue;
+    }
+    const uint64_t nd = nondiag_mask(g);
+    for (int k = 0; k < n; ++k)
+      if ((nd >> k) & 1ULL) flush(k);
+    out.push_back(g);
+  }
+  for (int q = 0; q < n; ++q) flush(q);
+  return out;
 }
 
 // FP64 flops of one gate applied to a 2^n state (2 per FMA): a complex
@@ -943,6 +1581,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
   int L = opts.tile_qubits > 0 ? opts.tile_qubits : kMaxTileQubits;
   L = std::min(std::min(L, kMaxTileQubits), n);
   const bool tiles_on = opts.use_tiles && n >= kRegBits + 1 && L >= kRegBits + 1;
+  if (tiles_on && opts.real_frames) gates = realify(n, gates);
   if (!tiles_on) {
     for (const GateDesc& g : gates) add_gate_step(n, g, steps, payload, stats);
     return QSV_OK;
@@ -973,6 +1612,22 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       done[k] = 1;
     }
     Encoded e = encode_pass(n, L, ps.S, pg);
+    if (getenv("QSV_PLAN_DUMP")) {
+      fprintf(stderr, "pass %zu: %zu gates, %zu phases, %zu ops, %zu data, fp64 ops/amp %.1f\n",
+              tiles.size(), pg.size(), e.phases.size(), e.ops.size(), e.data.size(),
+              e.fp64_ops_per_amp);
+      for (const TilePhase& ph : e.phases) {
+        fprintf(stderr, "  phase type %d regs", ph.type);
+        for (int i = 0; i < kRegBits; ++i) fprintf(stderr, " %d", ph.regpos[i]);
+        fprintf(stderr, " :");
+        for (int o = ph.op_begin; o < ph.op_end; ++o) {
+          const TileOp& op = e.ops[o];
+          fprintf(stderr, " %d/%x", op.kind, op.slots);
+          if (op.kind == T_FLUSH) fprintf(stderr, "[t%d s%d f%d]", op.flags & 1, op.m, op.slots);
+        }
+        fprintf(stderr, "\n");
+      }
+    }
     TilePlan tp;
     tp.L = L;
     for (int q = 0; q < n; ++q)
@@ -982,7 +1637,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
     tp.ndata = (int)e.data.size();
     tp.num_gates = (int)pg.size();
     tp.hbm_bytes = 32.0 * std::ldexp(1.0, n);
-    for (const GateDesc* gp : pg) stats->fp64_flops += gate_fp64_flops(n, *gp);
+    stats->fp64_flops += 2.0 * e.fp64_ops_per_amp * std::ldexp(1.0, n);
     // payload: [TilePassDev][phases][ops][data]
     size_t off = align_up(payload.size(), 256);
     tp.dev_off = off;

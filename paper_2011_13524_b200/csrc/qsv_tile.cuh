@@ -30,7 +30,11 @@ enum TileOpKind : int32_t {
   T_DIAG = 5,     // diagonal, targets on local or tile (global) bits
   T_PHASE = 6,    // constant phase on a local/tile bit pattern
   T_PARITY = 7,   // f[parity(idx & zmask)]
-  T_DENSE1XR = 8, // m uncontrolled 2x2 on slots 0..m-1 in order (data: 4m entries)
+  T_DENSE1X = 8,  // uncontrolled 2x2 on every slot of the mask (data: 4 per slot, slot order)
+  T_REAL1 = 11,   // real 2x2 on one slot (optionally controlled; data: 2 double2 = a b, c d)
+  T_REAL1X = 12,  // uncontrolled real 2x2 on every slot of the mask (2 double2 per slot)
+  T_FLUSH = 13,   // merged diagonal: table over the register slots, linear sign
+                  // rules and per-thread factors (see FlushSign / FlushFactor)
   // shared-memory ops (a phase of their own; cosets read straight from smem)
   S_DENSE = 9,    // 2^m x 2^m on m <= 4 local bits (tpos), optionally controlled
   S_PAULI = 10,   // X/Y product on local bits (slots = local X mask), Z parity
@@ -52,6 +56,19 @@ struct __align__(16) TileOp {   // 64 bytes = 4 x 128-bit loads
   int8_t tpos[4];     // DIAG: target position; >= 0 local bit, < 0: -(global bit)-1
                       // S_DENSE: local bit of matrix index bit j
   int32_t pad;
+};
+
+// T_FLUSH payload: [T: 2^kRegBits double2 if flags & 1][m FlushSign][slots FlushFactor]
+// TileOp.lmask holds the sign bits of a +-1 table (flags & 1 clear).
+struct __align__(16) FlushSign {  // where the thread/tile pattern matches, flip the
+  uint32_t lm, lv;                // sign of the register slots j with bit j of col
+  uint32_t col, pad;              // set (col: all ones, or the j_slot == value column)
+  uint64_t gm, gv;
+};
+struct __align__(16) FlushFactor {  // factor d[bit] of one non-register qubit
+  int32_t pos;                      // >= 0 local (thread) bit, < 0: -(global bit)-1
+  int32_t pad[3];
+  double2 d0, d1;
 };
 
 struct TilePhase {

@@ -17,7 +17,9 @@ from paper_2011_13524_b200 import workloads  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 28
 depth = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-variants = [dict(tile_qubits=L) for L in (10, 11, 12)]
+variants = [dict(tile_qubits=12, real_frames=rf) for rf in (0, 1)]
+if os.environ.get('TC_VARIANTS'):
+    variants = eval(os.environ['TC_VARIANTS'])
 st = qs.QuantumState(n)
 st.set_random_state_device(1)
 for fam in ("cz-ladder", "cnot-ring"):

@@ -51,11 +51,12 @@ def random_circuit(n, ngates, seed, max_k=4):
     return c
 
 
+@pytest.mark.parametrize("rf", [0, 1])
 @pytest.mark.parametrize("n,L,seed", [(6, 6, 0), (9, 8, 1), (13, 12, 2), (14, 8, 3),
                                       (16, 12, 4), (18, 10, 5), (20, 12, 6)])
-def test_tiles_match_oracle(n, L, seed):
+def test_tiles_match_oracle(n, L, seed, rf):
     circ = random_circuit(n, 160, seed)
-    circ.set_plan_options(use_tiles=1, tile_qubits=L)
+    circ.set_plan_options(use_tiles=1, tile_qubits=L, real_frames=rf)
     stats = circ.program_stats()
     assert stats["num_tile_passes"] >= 1, stats
     st = qs.QuantumState(n)
@@ -95,3 +96,68 @@ def test_tiles_cz_ladder_pass_count_and_parity():
     ref = orc.haar_state(n, 3)
     c_oracle.run_records(ref, n, circuit_records(circ))
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+
+
+def layered_circuit(n, layers, seed):
+    """Random-circuit shape the real-frame planner targets: layers of random
+    1-qubit unitaries / rotations, then CZ / CNOT / controlled-phase ladders."""
+    rng = np.random.default_rng(seed)
+    c = qs.QuantumCircuit(n)
+    for layer in range(layers):
+        for q in range(n):
+            r = int(rng.integers(4))
+            if r == 0:
+                c.add_gate(qg.RandomUnitary([q], seed=int(rng.integers(1 << 30))))
+            elif r == 1:
+                c.add_gate(qg.RZ(q, float(rng.uniform(-7, 7))))
+                c.add_gate(qg.RX(q, float(rng.uniform(-7, 7))))
+                c.add_gate(qg.RZ(q, float(rng.uniform(-7, 7))))
+            elif r == 2:
+                c.add_gate(qg.H(q))
+                c.add_gate(qg.T(q))
+            else:
+                c.add_gate(qg.RX(q, float(rng.uniform(-7, 7))))
+        for q in range(layer % 2, n - 1, 2):
+            r = int(rng.integers(4))
+            a, b = (q, q + 1) if rng.integers(2) else (q + 1, q)
+            if r == 0:
+                c.add_gate(qg.CNOT(a, b))
+            elif r == 1:
+                g = qg.DiagonalMatrix([b], [1, np.exp(1j * rng.uniform(0, 6))])
+                g.add_control_qubit(a, 1)
+                c.add_gate(g)
+            else:
+                c.add_gate(qg.CZ(a, b))
+        if layer % 3 == 2:
+            c.add_gate(qg.Z(int(rng.integers(n))))
+            c.add_gate(qg.S(int(rng.integers(n))))
+    return c
+
+
+@pytest.mark.parametrize("n,L,layers,seed", [(7, 6, 6, 0), (12, 8, 8, 1), (16, 12, 10, 2),
+                                             (20, 12, 12, 3), (22, 11, 6, 4)])
+def test_real_frames_layered_circuits(n, L, layers, seed):
+    circ = layered_circuit(n, layers, seed)
+    ref = orc.haar_state(n, seed)
+    c_oracle.run_records(ref, n, circuit_records(circ))
+    for rf in (1, 0):
+        circ.set_plan_options(use_tiles=1, tile_qubits=L, real_frames=rf)
+        st = qs.QuantumState(n)
+        st.set_Haar_random_state(seed)
+        circ.update_quantum_state(st)
+        err = np.max(np.abs(st.get_vector() - ref))
+        assert err <= 1e-12, (rf, err, circ.program_stats())
+
+
+def test_real_frames_benchmark_circuits():
+    from paper_2011_13524_b200 import workloads
+    n = 20
+    for circ in (workloads.generate_cz_ladder(n, 6, seed=2), workloads.generate_cnot_ring(n, seed=2)):
+        ref = orc.haar_state(n, 9)
+        c_oracle.run_records(ref, n, circuit_records(circ))
+        for rf in (1, 0):
+            circ.set_plan_options(real_frames=rf)
+            st = qs.QuantumState(n)
+            st.set_Haar_random_state(9)
+            circ.update_quantum_state(st)
+            assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12, rf
