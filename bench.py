@@ -517,6 +517,26 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
                         "note": "FP64 flops counted by the planner (2 per FMA) / device time"},
            "clocks": clk.summary()}
     del st
+    # the headline curve: sec/layer vs qubits (same generator, same depth)
+    curve = {}
+    for m in range(20, n + 1, 2):
+        c = workloads.generate_cz_ladder(m, depth, seed=1)
+        s2 = qs.QuantumState(m, device=dev)
+        s2.set_stream(stream.cuda_stream)
+        s2.set_random_state_device(7)
+        c.update_quantum_state(s2)
+        torch.cuda.synchronize(dev)
+        tb = 1e9
+        for _ in range(2):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            c.update_quantum_state(s2)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            tb = min(tb, a.elapsed_time(b) / 1e3)
+        curve[str(m)] = tb / (depth + 1)
+        del s2
+    out["sec_per_layer_vs_qubits"] = curve
     return out
 
 
