@@ -143,6 +143,15 @@ int qsv_permutate_qubit(const qsv_state* src, const int* order, int n, qsv_state
 int qsv_drop_qubit(const qsv_state* src, const int* targets, const int* values, int k,
                    qsv_state* out);
 
+/* qsv_branch_norm2 <- the branch probability |K_i psi|^2 of CptpMap.apply
+ *                     (maps.py:55-73): squared norm of matrix|psi> for a
+ *                     2^k x 2^k matrix on k = 1..5 targets, computed coset by
+ *                     coset without copying the state (the reference copies
+ *                     the state per Kraus operator).  Controls are expanded
+ *                     into the matrix by the caller. */
+int qsv_branch_norm2(const qsv_state* st, const int* targets, int k, const double* matrix,
+                     double* out);
+
 /* ------------------------------------------------------------ programs
  * A program is a compiled gate list: the replacement for the per-gate loop
  * of Circuit.update_state (circuit.py:48-55).  qsv_program_create copies the

@@ -256,6 +256,67 @@ def run_records(amps, n, records):
     return amps
 
 
+# ---------------------------------------------------------------- maps
+def apply_map_record(amps, n, rec, rng, cregs):
+    """Quantum maps (maps.py:35-187) on a state vector.  Records:
+    ("cptp", kraus_records, register_or_None), ("prob", probs, records),
+    ("adaptive", condition, inner_record).  Returns the new amplitude array
+    (a CPTP map rebinds it, maps.py:84)."""
+    kind = rec[0]
+    if kind == "cptp":
+        _, kraus, reg = rec
+        draw = rng.random()
+        cumulative = 0.0
+        chosen = branch = None
+        for i, k in enumerate(kraus):
+            cand = amps.copy()
+            apply_record(cand, n, k)
+            prob = squared_norm(cand)
+            cumulative += prob
+            if cumulative >= draw or i == len(kraus) - 1:
+                if prob <= 0:
+                    continue
+                chosen, branch = i, cand
+                break
+        if chosen is None:
+            raise ValueError("all Kraus branches have zero probability")
+        branch /= np.sqrt(squared_norm(branch))
+        if reg is not None:
+            if reg >= len(cregs):
+                cregs.extend([0] * (reg + 1 - len(cregs)))
+            cregs[reg] = chosen
+        return branch
+    if kind == "prob":
+        _, probs, gates = rec
+        draw = rng.random()
+        cumulative = 0.0
+        for p, g in zip(probs, gates):
+            cumulative += p
+            if draw < cumulative:
+                apply_record(amps, n, g)
+                break
+        return amps
+    if kind == "adaptive":
+        _, cond, inner = rec
+        if cond(list(cregs)):
+            if inner[0] in ("cptp", "prob", "adaptive"):
+                return apply_map_record(amps, n, inner, rng, cregs)
+            apply_record(amps, n, inner)
+        return amps
+    apply_record(amps, n, rec)
+    return amps
+
+
+def run_records_rng(amps, n, records, seed):
+    """update_state with maps: one default_rng(seed) shared by every map in
+    gate order (circuit.py:48-55); returns (amplitudes, classical registers)."""
+    rng = seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
+    cregs = []
+    for rec in records:
+        amps = apply_map_record(amps, n, rec, rng, cregs)
+    return amps, cregs
+
+
 # ---------------------------------------------------------------- states
 def zero_state(n):
     """state.py:25-30."""

@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from . import _lib
 from ._gates import BasicGate, PauliRotationGate, QuantumGate
 from ._handles import QuantumGateBase, unwrap
@@ -72,9 +74,6 @@ class Circuit:
     def _check_gate(self, gate) -> None:
         if not isinstance(gate, QuantumGate):
             raise TypeError(f"expected a gate, got {type(gate).__name__}")
-        if not isinstance(gate, BasicGate):
-            raise ValueError("only basic gates run on the B200 engine (quantum maps are "
-                             "outside the accelerated path)")
         top = max(gate.touched_qubits(), default=-1)
         if top >= self.num_qubits:
             raise ValueError(f"gate touches qubit {top} but the circuit has "
@@ -134,33 +133,72 @@ class Circuit:
                 bytes(self._plan))
 
     def compile(self):
+        """Lower the gate list: runs of basic gates become native programs,
+        quantum maps (maps.py) stay host-driven steps between them.  Returns
+        the program of an all-basic circuit, else the list of steps."""
         key = self._key()
         if self._prog is None or self._prog_key != key:
-            self._prog = _Program(self.num_qubits, self.gates, self._plan)
+            if all(isinstance(g, BasicGate) for g in self.gates):
+                self._prog = _Program(self.num_qubits, self.gates, self._plan)
+            else:
+                steps, run = [], []
+                for g in self.gates:
+                    if isinstance(g, BasicGate):
+                        run.append(g)
+                        continue
+                    if run:
+                        steps.append(_Program(self.num_qubits, run, self._plan))
+                        run = []
+                    steps.append(g)
+                if run:
+                    steps.append(_Program(self.num_qubits, run, self._plan))
+                self._prog = steps
             self._prog_key = key
         return self._prog
 
     def program_stats(self) -> dict:
-        return dict(self.compile().stats)
+        prog = self.compile()
+        if isinstance(prog, _Program):
+            return dict(prog.stats)
+        total = {f: 0 for f, _ in _lib.QsvProgramStats._fields_}
+        for st in prog:
+            if isinstance(st, _Program):
+                for k, v in st.stats.items():
+                    total[k] += v
+        total["num_maps"] = sum(1 for st in prog if not isinstance(st, _Program))
+        return total
 
     def plan_stats(self, **kw) -> dict:
         """Host-only planning statistics (no GPU needed)."""
         opts = default_plan_opts(**kw) if kw else self._plan
-        ops = (_lib.QsvOp * max(1, len(self.gates)))()
+        basic = [g for g in self.gates if isinstance(g, BasicGate)]  # maps run on the host
+        ops = (_lib.QsvOp * max(1, len(basic)))()
         keep = []
-        for i, g in enumerate(self.gates):
+        for i, g in enumerate(basic):
             g.fill_op(ops[i], keep)
         st = _lib.QsvProgramStats()
-        check(lib.qsv_plan_stats(self.num_qubits, ops, len(self.gates), C.byref(opts),
+        check(lib.qsv_plan_stats(self.num_qubits, ops, len(basic), C.byref(opts),
                                  C.byref(st)))
         return {f: getattr(st, f) for f, _ in _lib.QsvProgramStats._fields_}
 
     def update_state(self, state, rng=None) -> None:
+        """circuit.py:48-55: one generator (seed / Generator / None) shared by
+        every map of the circuit, drawn in gate order."""
         if state.get_qubit_count() != self.num_qubits:
             raise ValueError("state and circuit qubit counts differ")
         if not self.gates:
             return
-        self.compile().run(state)
+        prog = self.compile()
+        if isinstance(prog, _Program):
+            prog.run(state)
+            return
+        if not isinstance(rng, np.random.Generator):
+            rng = np.random.default_rng(rng)
+        for step in prog:
+            if isinstance(step, _Program):
+                step.run(state)
+            else:
+                step.apply(state, rng)
 
 
 class ParametricCircuit(Circuit):

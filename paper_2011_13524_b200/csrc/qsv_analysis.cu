@@ -101,6 +101,75 @@ __global__ void k_sum_partials(const double* __restrict__ partials, int nblocks,
   if (threadIdx.x == 0) *out = s[0];
 }
 
+// ------------------------------------------------------------ branch norm
+// ||E psi||^2 for a 2^K x 2^K matrix E on K qubits without materialising
+// E psi: per coset, u = E v and accumulate |u|^2 (CptpMap branch
+// probabilities, maps.py:55-73, where the reference copies the whole state
+// per Kraus operator).  E and the coset offsets live in shared memory.
+template <int K>
+__global__ void __launch_bounds__(kThreads)
+    k_branch_norm(const double2* __restrict__ a, FixedBits fb, const double2* __restrict__ E,
+                  const uint64_t* __restrict__ offs, uint64_t units,
+                  double* __restrict__ partials) {
+  constexpr int D = 1 << K;
+  __shared__ double2 sE[D * D];
+  __shared__ uint64_t sO[D];
+  for (int i = threadIdx.x; i < D * D; i += kThreads) sE[i] = E[i];
+  if (threadIdx.x < D) sO[threadIdx.x] = offs[threadIdx.x];
+  __syncthreads();
+  double acc = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t u = (uint64_t)blockIdx.x * kThreads + threadIdx.x; u < units; u += stride) {
+    const uint64_t x0 = widen(u, fb);
+    double2 v[D];
+#pragma unroll
+    for (int w = 0; w < D; ++w) v[w] = __ldg(a + (x0 | sO[w]));
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double2 t = cmul(sE[r * D], v[0]);
+#pragma unroll
+      for (int w = 1; w < D; ++w) t = cfma(sE[r * D + w], v[w], t);
+      acc = fma(t.x, t.x, fma(t.y, t.y, acc));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
+// scratch: E (4^k double2) followed by 2^k offsets, already on the device
+int launch_branch_norm(const double2* a, int n, const int* targets, int k, const double2* dE,
+                       const uint64_t* dOffs, double* partials, double* dev_out, cudaStream_t s) {
+  int pos[8];
+  for (int j = 0; j < k; ++j) pos[j] = targets[j];
+  std::sort(pos, pos + k);
+  FixedBits fb = make_fixed(pos, k, 0);
+  const uint64_t units = 1ULL << (n - k);
+  const unsigned grid = (unsigned)std::min<uint64_t>(kRedBlocks, std::max<uint64_t>(
+                                                          1, (units + kThreads - 1) / kThreads));
+  switch (k) {
+    case 1: k_branch_norm<1><<<grid, kThreads, 0, s>>>(a, fb, dE, dOffs, units, partials); break;
+    case 2: k_branch_norm<2><<<grid, kThreads, 0, s>>>(a, fb, dE, dOffs, units, partials); break;
+    case 3: k_branch_norm<3><<<grid, kThreads, 0, s>>>(a, fb, dE, dOffs, units, partials); break;
+    case 4: k_branch_norm<4><<<grid, kThreads, 0, s>>>(a, fb, dE, dOffs, units, partials); break;
+    case 5: k_branch_norm<5><<<grid, kThreads, 0, s>>>(a, fb, dE, dOffs, units, partials); break;
+    default:
+      set_error("branch norm supports 1..5 qubits, got %d", k);
+      return QSV_EINVAL;
+  }
+  QSV_CHECK_LAUNCH("k_branch_norm");
+  k_sum_partials<<<1, kThreads, 0, s>>>(partials, (int)grid, dev_out);
+  QSV_CHECK_LAUNCH("k_sum_partials");
+  return QSV_OK;
+}
+
 // ---------------------------------------------------------------- sampling
 // The cumulative distribution is defined blockwise: block b holds amplitudes
 // [b*BS, (b+1)*BS); cum(j) = P[b] + r_j where r_j is the sequential running

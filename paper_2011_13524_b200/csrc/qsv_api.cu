@@ -38,6 +38,8 @@ int launch_marginal(const double2* a, int n, uint64_t mask, uint64_t value, doub
 int launch_sampling(const double2* a, int n, const double* dev_u, int count, double* scratch,
                     uint64_t* dev_out, cudaStream_t s);
 size_t sampling_scratch_doubles(int n);
+int launch_branch_norm(const double2* a, int n, const int* targets, int k, const double2* dE,
+                       const uint64_t* dOffs, double* partials, double* dev_out, cudaStream_t s);
 int launch_mul_elementwise(double2* a, const double2* f, uint64_t dim, cudaStream_t s);
 int launch_kron(const double2* first, int n1, const double2* second, int n2, double2* out,
                 cudaStream_t s);
@@ -701,6 +703,48 @@ int qsv_drop_qubit(const qsv_state* src, const int* targets, const int* values, 
   DeviceGuard dg(out->device);
   if (src->stream != out->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
   return launch_drop(src->amps, src->n, targets, values, k, out->amps, out->stream);
+}
+
+int qsv_branch_norm2(const qsv_state* st, const int* targets, int k, const double* matrix,
+                     double* out) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (k < 1 || k > 5 || k > st->n) {
+    set_error("branch norm supports 1..5 target qubits, got %d", k);
+    return QSV_EINVAL;
+  }
+  uint64_t seen = 0;
+  for (int j = 0; j < k; ++j) {
+    if (targets[j] < 0 || targets[j] >= st->n || ((seen >> targets[j]) & 1ULL)) {
+      set_error("targets must be distinct qubits of the state");
+      return QSV_EINVAL;
+    }
+    seen |= 1ULL << targets[j];
+  }
+  DeviceGuard dg(st->device);
+  const size_t D = (size_t)1 << k;
+  std::vector<char> host(D * D * sizeof(double2) + D * sizeof(uint64_t) + 2 * sizeof(double));
+  memcpy(host.data(), matrix, D * D * sizeof(double2));
+  uint64_t* offs = reinterpret_cast<uint64_t*>(host.data() + D * D * sizeof(double2));
+  for (size_t w = 0; w < D; ++w) {
+    uint64_t o = 0;
+    for (int j = 0; j < k; ++j)
+      if ((w >> j) & 1) o |= 1ULL << targets[j];
+    offs[w] = o;
+  }
+  Scratch& sc = g_payload[st];
+  int rc = ensure(sc, host.size(), st->stream);
+  if (rc) return rc;
+  char* dev = reinterpret_cast<char*>(sc.ptr);
+  QSV_TRY(cudaMemcpyAsync(dev, host.data(), host.size() - 2 * sizeof(double),
+                          cudaMemcpyHostToDevice, st->stream));
+  double* dout = reinterpret_cast<double*>(dev + host.size() - 2 * sizeof(double));
+  rc = launch_branch_norm(st->amps, st->n, targets, k, reinterpret_cast<const double2*>(dev),
+                          reinterpret_cast<const uint64_t*>(dev + D * D * sizeof(double2)),
+                          st->partials, dout, st->stream);
+  if (rc) return rc;
+  QSV_TRY(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+  QSV_TRY(cudaStreamSynchronize(st->stream));
+  return QSV_OK;
 }
 
 }  // extern "C"

@@ -341,6 +341,29 @@ def make_analysis():
     np.savez_compressed(os.path.join(HERE, "analysis.npz"), **outs)
 
 
+def make_maps():
+    """Noise / measurement circuits run by the reference bindings with a
+    seed: final states and classical registers."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    import qsimbind as qb
+    from qsimbind import gate as qbg
+    from golden_util import build_map_circuit, map_circuit_specs
+    meta, outs = [], {}
+    for name, n, hseed, seeds, spec in map_circuit_specs():
+        for rs in seeds:
+            c = build_map_circuit(n, spec, qb.QuantumCircuit, qbg)
+            st = qb.StateVector(n)
+            st.set_Haar_random_state(hseed)
+            c.update_quantum_state(st, seed=rs)
+            key = f"{name}_r{rs}"
+            outs[key] = st.get_vector()
+            meta.append({"name": name, "seed": rs, "key": key,
+                         "cregs": [st.get_classical_value(i) for i in range(6)]})
+    with open(os.path.join(HERE, "maps.json"), "w") as fh:
+        json.dump(meta, fh)
+    np.savez_compressed(os.path.join(HERE, "maps.npz"), **outs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-cfg3", action="store_true",
@@ -352,8 +375,12 @@ def main():
     if args.only == "analysis":
         make_analysis()
         return
+    if args.only == "maps":
+        make_maps()
+        return
     make_haar()
     make_analysis()
+    make_maps()
     make_gates()
     make_circuits()
     make_observables(args.with_cfg3)

@@ -63,3 +63,58 @@ def load_observables():
 
 def load_haar():
     return np.load(os.path.join(GOLDEN, "haar.npz"))
+
+
+# ------------------------------------------------------------ quantum maps
+def map_circuit_specs():
+    """Noise / measurement circuits (shared by make_golden.py, which builds
+    them with the reference bindings, and the tests, which build them with
+    ours): (name, n, haar_seed, run_seeds, spec).  A spec item is
+    (factory, args); "Adaptive" args are (inner_item, register, value)."""
+    import math
+    s = math.sqrt
+    kraus_bitflip = [("DenseMatrix", [[1], [[s(0.7), 0], [0, s(0.7)]]]),
+                     ("DenseMatrix", [[1], [[0, s(0.3)], [s(0.3), 0]]])]
+    kraus_ctl = [("DenseMatrix", [[0, 2], [[1, 0, 0, 0], [0, s(0.5), 0, 0],
+                                           [0, 0, 1, 0], [0, 0, 0, s(0.5)]]]),
+                 ("DenseMatrix", [[0, 2], [[0, s(0.5), 0, 0], [0, 0, 0, 0],
+                                           [0, 0, 0, s(0.5)], [0, 0, 0, 0]]])]
+    noisy = [("H", [0]), ("RX", [1, 0.7]), ("CNOT", [0, 2]),
+             ("AmplitudeDampingNoise", [0, 0.35]), ("DepolarizingNoise", [1, 0.4]),
+             ("Measurement", [2, 0]), ("BitFlipNoise", [3, 0.5]), ("DephasingNoise", [0, 0.5]),
+             ("Adaptive", [("X", [1]), 0, 1]), ("TwoQubitDepolarizingNoise", [1, 3, 0.6]),
+             ("CPTP", [kraus_bitflip]), ("Instrument", [kraus_ctl, 1]), ("RY", [2, 1.1]),
+             ("Measurement", [0, 2]), ("Probabilistic", [[0.2, 0.5], [("Y", [3]), ("S", [1])]]),
+             ("Adaptive", [("Z", [3]), 2, 0])]
+    meas = [("H", [q]) for q in range(5)] + [("CZ", [0, 1]), ("CZ", [2, 3])] + \
+           [("Measurement", [q, q]) for q in range(5)]
+    return [("noisy4", 4, 3, [0, 1, 2, 3, 11, 12, 13, 14], noisy),
+            ("measure5", 5, 8, [0, 5, 6, 7], meas)]
+
+
+def build_map_gate(item, gm):
+    fac, args = item
+    if fac == "Adaptive":
+        inner, reg, val = args
+        return gm.Adaptive(build_map_gate(inner, gm),
+                           lambda regs, r=reg, v=val: len(regs) > r and regs[r] == v)
+    if fac in ("CPTP",):
+        return gm.CPTP([build_map_gate(k, gm) for k in args[0]])
+    if fac == "Instrument":
+        return gm.Instrument([build_map_gate(k, gm) for k in args[0]], args[1])
+    if fac == "Probabilistic":
+        return gm.Probabilistic(args[0], [build_map_gate(k, gm) for k in args[1]])
+    return getattr(gm, fac)(*args)
+
+
+def build_map_circuit(n, spec, circuit_cls, gm):
+    c = circuit_cls(n)
+    for item in spec:
+        c.add_gate(build_map_gate(item, gm))
+    return c
+
+
+def load_maps():
+    with open(os.path.join(GOLDEN, "maps.json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(GOLDEN, "maps.npz"))
