@@ -152,6 +152,15 @@ int qsv_drop_qubit(const qsv_state* src, const int* targets, const int* values, 
 int qsv_branch_norm2(const qsv_state* st, const int* targets, int k, const double* matrix,
                      double* out);
 
+/* Density matrices (state.py:195-222) are held as 2h-qubit vectors,
+ * element (r, c) at index (r << h) | c; U rho U^dag is U on qubits h + t and
+ * conj(U) on qubits t (two ordinary gate calls).
+ * qsv_conj         amps <- conj(amps) (density_from_pure, state.py:219-222)
+ * qsv_trace_pairs  <- DensityMatrix.get_trace (state.py:216-217):
+ *                     sum_i amps[(i << h) | i] for a 2h-qubit state. */
+int qsv_conj(qsv_state* st);
+int qsv_trace_pairs(const qsv_state* st, double out_re_im[2]);
+
 /* ------------------------------------------------------------ programs
  * A program is a compiled gate list: the replacement for the per-gate loop
  * of Circuit.update_state (circuit.py:48-55).  qsv_program_create copies the

@@ -17,12 +17,14 @@ from ._handles import QuantumGateBase, unwrap
 from ._state import QuantumState, StateVector
 from ._circuit import ParametricQuantumCircuit, QuantumCircuit
 from ._observable import GeneralQuantumOperator, Observable, PauliOperator
+from ._density import DensityMatrix, density_from_pure
 from . import circuit, gate, quantum_operator, state  # noqa: F401
 
 __all__ = [
     "QuantumState", "StateVector", "QuantumCircuit", "ParametricQuantumCircuit",
     "Observable", "PauliOperator", "GeneralQuantumOperator", "QuantumGateBase",
     "unwrap", "gate", "circuit", "state", "quantum_operator", "device_count",
+    "DensityMatrix", "density_from_pure",
 ]
 
 __version__ = "0.1.0"

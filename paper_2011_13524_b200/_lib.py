@@ -112,6 +112,8 @@ _SIGS = {
     "qsv_permutate_qubit": ([_P, _IP, _I, _P], _I),
     "qsv_drop_qubit": ([_P, _IP, _IP, _I, _P], _I),
     "qsv_branch_norm2": ([_P, _IP, _I, _DP, C.POINTER(C.c_double)], _I),
+    "qsv_conj": ([_P], _I),
+    "qsv_trace_pairs": ([_P, C.POINTER(C.c_double)], _I),
     "qsv_program_create": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts), C.POINTER(_P)], _I),
     "qsv_program_run": ([_P, _P], _I),
     "qsv_program_stats_get": ([_P, C.POINTER(QsvProgramStats)], _I),

@@ -19,6 +19,11 @@
 
 namespace qsv {
 
+static unsigned stream_grid(uint64_t units) {
+  return (unsigned)std::min<uint64_t>(std::max<uint64_t>(1, (units + kThreads - 1) / kThreads),
+                                      148ULL * 16);
+}
+
 // Index with the free bits of u deposited at pos[0..nf) over a fixed value:
 // used instead of widen() when more than kMaxFixed qubits are fixed.
 struct Deposit {
@@ -166,6 +171,73 @@ int launch_branch_norm(const double2* a, int n, const int* targets, int k, const
   }
   QSV_CHECK_LAUNCH("k_branch_norm");
   k_sum_partials<<<1, kThreads, 0, s>>>(partials, (int)grid, dev_out);
+  QSV_CHECK_LAUNCH("k_sum_partials");
+  return QSV_OK;
+}
+
+// ------------------------------------------------ density-matrix helpers
+// A density matrix rho (2^h x 2^h, row-major) is held as a 2h-qubit vector:
+// element (r, c) at index (r << h) | c, so U rho U^dag is U on the row
+// qubits (h + t) and conj(U) on the column qubits (t).
+__global__ void __launch_bounds__(kThreads)
+    k_conj(double2* __restrict__ a, uint64_t dim) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t x = (uint64_t)blockIdx.x * kThreads + threadIdx.x; x < dim; x += stride) {
+    double2 v = a[x];
+    v.y = -v.y;
+    a[x] = v;
+  }
+}
+
+// sum_i rho[i][i] = sum_i a[(i << h) | i]; per-block partials (re, im)
+__global__ void __launch_bounds__(kThreads)
+    k_trace_pairs(const double2* __restrict__ a, int h, double* __restrict__ partials) {
+  double re = 0.0, im = 0.0;
+  const uint64_t count = 1ULL << h;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < count; i += stride) {
+    const double2 v = __ldg(a + ((i << h) | i));
+    re += v.x;
+    im += v.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, o);
+    im += __shfl_xor_sync(0xffffffffu, im, o);
+  }
+  __shared__ double red[2][kThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = re;
+    red[1][threadIdx.x >> 5] = im;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sr = 0, si = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      sr += red[0][w];
+      si += red[1][w];
+    }
+    partials[blockIdx.x] = sr;
+    partials[gridDim.x + blockIdx.x] = si;
+  }
+}
+
+int launch_conj(double2* a, uint64_t dim, cudaStream_t s) {
+  k_conj<<<stream_grid(dim), kThreads, 0, s>>>(a, dim);
+  QSV_CHECK_LAUNCH("k_conj");
+  return QSV_OK;
+}
+
+int launch_trace_pairs(const double2* a, int h, double* partials, double* dev_out,
+                       cudaStream_t s) {
+  const uint64_t count = 1ULL << h;
+  const unsigned grid = (unsigned)std::min<uint64_t>(
+      kRedBlocks / 2, std::max<uint64_t>(1, (count + kThreads - 1) / kThreads));
+  k_trace_pairs<<<grid, kThreads, 0, s>>>(a, h, partials);
+  QSV_CHECK_LAUNCH("k_trace_pairs");
+  k_sum_partials<<<1, kThreads, 0, s>>>(partials, (int)grid, dev_out);
+  QSV_CHECK_LAUNCH("k_sum_partials");
+  k_sum_partials<<<1, kThreads, 0, s>>>(partials + grid, (int)grid, dev_out + 1);
   QSV_CHECK_LAUNCH("k_sum_partials");
   return QSV_OK;
 }
@@ -378,10 +450,6 @@ __global__ void __launch_bounds__(kThreads)
     st1(out + k, __ldg(in + widen(k, fb)));
 }
 
-static unsigned stream_grid(uint64_t units) {
-  return (unsigned)std::min<uint64_t>(std::max<uint64_t>(1, (units + kThreads - 1) / kThreads),
-                                      148ULL * 16);
-}
 
 int launch_marginal(const double2* a, int n, uint64_t mask, uint64_t value, double* partials,
                     double* dev_out, cudaStream_t s) {

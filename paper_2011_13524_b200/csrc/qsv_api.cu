@@ -38,6 +38,9 @@ int launch_marginal(const double2* a, int n, uint64_t mask, uint64_t value, doub
 int launch_sampling(const double2* a, int n, const double* dev_u, int count, double* scratch,
                     uint64_t* dev_out, cudaStream_t s);
 size_t sampling_scratch_doubles(int n);
+int launch_conj(double2* a, uint64_t dim, cudaStream_t s);
+int launch_trace_pairs(const double2* a, int h, double* partials, double* dev_out,
+                       cudaStream_t s);
 int launch_branch_norm(const double2* a, int n, const int* targets, int k, const double2* dE,
                        const uint64_t* dOffs, double* partials, double* dev_out, cudaStream_t s);
 int launch_mul_elementwise(double2* a, const double2* f, uint64_t dim, cudaStream_t s);
@@ -743,6 +746,30 @@ int qsv_branch_norm2(const qsv_state* st, const int* targets, int k, const doubl
                           st->partials, dout, st->stream);
   if (rc) return rc;
   QSV_TRY(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+  QSV_TRY(cudaStreamSynchronize(st->stream));
+  return QSV_OK;
+}
+
+int qsv_conj(qsv_state* st) {
+  if (bad_state(st)) return QSV_EINVAL;
+  DeviceGuard dg(st->device);
+  return launch_conj(st->amps, st->dim, st->stream);
+}
+
+int qsv_trace_pairs(const qsv_state* st, double out[2]) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (st->n % 2) {
+    set_error("a vectorised density matrix has an even qubit count, got %d", st->n);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(st->device);
+  Scratch& sc = g_results[st];
+  int rc = ensure(sc, sizeof(double) * 2 * kMaxTerms, st->stream);
+  if (rc) return rc;
+  double* dout = reinterpret_cast<double*>(sc.ptr);
+  rc = launch_trace_pairs(st->amps, st->n / 2, st->partials, dout, st->stream);
+  if (rc) return rc;
+  QSV_TRY(cudaMemcpyAsync(out, dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
   QSV_TRY(cudaStreamSynchronize(st->stream));
   return QSV_OK;
 }

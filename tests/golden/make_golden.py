@@ -364,6 +364,28 @@ def make_maps():
     np.savez_compressed(os.path.join(HERE, "maps.npz"), **outs)
 
 
+def make_density():
+    """Density-matrix evolution through apply_density (reference core)."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from golden_util import core_factory, density_specs
+    meta, outs = [], {}
+    for name, n, hseed, ops in density_specs():
+        if hseed is None:
+            rho = core.DensityMatrix(n)
+        else:
+            st = core.StateVector(n)
+            st.set_haar_random(hseed)
+            rho = core.density_from_pure(st)
+        for fac, args in ops:
+            core_factory(fac, core)(*args).apply_density(rho)
+        outs[name] = rho.elements
+        tr = rho.get_trace()
+        meta.append({"name": name, "trace": [tr.real, tr.imag]})
+    with open(os.path.join(HERE, "density.json"), "w") as fh:
+        json.dump(meta, fh)
+    np.savez_compressed(os.path.join(HERE, "density.npz"), **outs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-cfg3", action="store_true",
@@ -378,9 +400,13 @@ def main():
     if args.only == "maps":
         make_maps()
         return
+    if args.only == "density":
+        make_density()
+        return
     make_haar()
     make_analysis()
     make_maps()
+    make_density()
     make_gates()
     make_circuits()
     make_observables(args.with_cfg3)

@@ -118,3 +118,28 @@ def load_maps():
     with open(os.path.join(GOLDEN, "maps.json")) as fh:
         meta = json.load(fh)
     return meta, np.load(os.path.join(GOLDEN, "maps.npz"))
+
+
+# ---------------------------------------------------------- density matrices
+def density_specs():
+    """(name, n, haar_seed or None, [(core factory, args), ...]) applied with
+    ``apply_density``; None starts from DensityMatrix(n) = |0><0|."""
+    ops = [("H", [0]), ("CNOT", [0, 2]), ("RX", [1, 0.4]), ("AmplitudeDampingNoise", [0, 0.3]),
+           ("DepolarizingNoise", [1, 0.2]), ("TwoQubitDepolarizingNoise", [0, 2, 0.1]),
+           ("RZ", [2, -1.3]), ("BitFlipNoise", [2, 0.25]), ("T", [1]), ("DephasingNoise", [0, 0.4])]
+    return [("mixed3", 3, 5, ops),
+            ("zero2", 2, None, [("X", [1]), ("H", [0]), ("AmplitudeDampingNoise", [1, 0.6])]),
+            ("mixed5", 5, 9, ops + [("CZ", [3, 4]), ("DepolarizingNoise", [4, 0.5])])]
+
+
+def core_factory(name, gates_mod, maps_mod=None):
+    f = getattr(gates_mod, name, None)
+    if f is None and maps_mod is not None:
+        f = getattr(maps_mod, name)
+    return f
+
+
+def load_density():
+    with open(os.path.join(GOLDEN, "density.json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(GOLDEN, "density.npz"))
