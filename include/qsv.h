@@ -50,6 +50,8 @@ typedef struct qsv_program qsv_program;
 const char* qsv_last_error(void);
 int qsv_version(void);
 int qsv_device_count(int* out);
+/* name (NUL-terminated, truncated to name_len), SM count, global memory */
+int qsv_device_info(int device, char* name, int name_len, int* sm_count, uint64_t* total_mem);
 
 /* --------------------------------------------------------------- state
  * qsv_state_create        <- StateVector.__init__ (state.py:25-30):

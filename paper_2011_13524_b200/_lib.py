@@ -81,6 +81,7 @@ _SIGS = {
     "qsv_last_error": ([], C.c_char_p),
     "qsv_version": ([], _I),
     "qsv_device_count": ([_IP], _I),
+    "qsv_device_info": ([_I, C.c_char_p, _I, _IP, C.POINTER(_U64)], _I),
     "qsv_state_create": ([_I, _I, C.POINTER(_P)], _I),
     "qsv_state_destroy": ([_P], _I),
     "qsv_state_num_qubits": ([_P, _IP], _I),
@@ -149,6 +150,17 @@ def int_array(values):
     for i, v in enumerate(values):
         arr[i] = int(v)
     return arr
+
+
+def device_info(device: int = 0) -> dict:
+    """Name, SM count and memory of a CUDA device (empty if none)."""
+    buf = C.create_string_buffer(256)
+    sms = C.c_int(0)
+    mem = C.c_uint64(0)
+    if lib.qsv_device_info(int(device), buf, 256, C.byref(sms), C.byref(mem)) != QSV_OK:
+        return {}
+    return {"name": buf.value.decode(errors="replace"), "sm_count": sms.value,
+            "memory_bytes": mem.value}
 
 
 def device_count() -> int:

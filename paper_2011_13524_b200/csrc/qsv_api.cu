@@ -169,6 +169,18 @@ int qsv_device_count(int* out) {
   return QSV_OK;
 }
 
+int qsv_device_info(int device, char* name, int name_len, int* sm_count, uint64_t* total_mem) {
+  cudaDeviceProp p;
+  QSV_TRY(cudaGetDeviceProperties(&p, device));
+  if (name && name_len > 0) {
+    strncpy(name, p.name, (size_t)name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (total_mem) *total_mem = (uint64_t)p.totalGlobalMem;
+  return QSV_OK;
+}
+
 int qsv_state_create(int num_qubits, int device, qsv_state** out) {
   if (!out) {
     set_error("null output pointer");

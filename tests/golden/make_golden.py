@@ -386,6 +386,51 @@ def make_density():
     np.savez_compressed(os.path.join(HERE, "density.npz"), **outs)
 
 
+def make_serialize():
+    """A circuit touching every serialisable kind, written by the reference
+    serializer, plus its run result (zero state, default_rng(7)) and the
+    optimizer gate counts of the reference CLI passes."""
+    from qsimcore import maps as M
+    from qsimcore import serialize as S
+    from qsimcore.optimizer import optimize_heavy, optimize_light
+    c = core.Circuit(5)
+    c.add_gate(core.H(0))
+    c.add_gate(core.RX(1, 0.3))
+    c.add_gate(core.U3(2, 0.1, 0.2, 0.3))
+    c.add_gate(core.CNOT(0, 1))
+    c.add_gate(core.TOFFOLI(0, 1, 3))
+    c.add_gate(core.FREDKIN(4, 2, 3))
+    c.add_gate(core.DenseGate([1, 3], np.linalg.qr(np.arange(16).reshape(4, 4) + 1j)[0],
+                              [(0, 1)]))
+    c.add_gate(core.SparseGate([2], [(0, 1, 1.0), (1, 0, 1j)]))
+    c.add_gate(core.DiagonalGate([3, 4], [1, 1j, -1, -1j]))
+    c.add_gate(core.PermutationGate([0, 2], [3, 0, 1, 2]))
+    c.add_gate(core.PauliGate([1, 4], [2, 3]))
+    c.add_gate(core.PauliRotationGate([0, 2, 3], [1, 2, 3], 0.77))
+    c.add_gate(M.AmplitudeDampingNoise(2, 0.4))
+    c.add_gate(M.Measurement(3, 1))
+    c.add_gate(M.DepolarizingNoise(0, 0.3))
+    c.add_gate(M.CptpMap([core.DenseGate([4], [[np.sqrt(0.5), 0], [0, np.sqrt(0.5)]]),
+                          core.DenseGate([4], [[0, np.sqrt(0.5)], [np.sqrt(0.5), 0]])]))
+    c.add_gate(core.RZ(4, -0.4))
+    for q in range(5):
+        c.add_gate(core.H(q))
+    S.dump_circuit(c, os.path.join(HERE, "circuit_doc.json"))
+    st = core.StateVector(5)
+    c.update_state(st, rng=np.random.default_rng(7))
+    counts = {}
+    for label in ("light", "heavy2", "heavy3"):
+        d = S.load_circuit(os.path.join(HERE, "circuit_doc.json"))
+        if label == "light":
+            optimize_light(d)
+        else:
+            optimize_heavy(d, int(label[-1]))
+        counts[label] = d.get_gate_count()
+    np.savez_compressed(os.path.join(HERE, "serialize.npz"), amplitudes=st.get_vector())
+    with open(os.path.join(HERE, "serialize.json"), "w") as fh:
+        json.dump({"cregs": list(st.classical_registers), "optimizer_counts": counts}, fh)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-cfg3", action="store_true",
@@ -403,10 +448,14 @@ def main():
     if args.only == "density":
         make_density()
         return
+    if args.only == "serialize":
+        make_serialize()
+        return
     make_haar()
     make_analysis()
     make_maps()
     make_density()
+    make_serialize()
     make_gates()
     make_circuits()
     make_observables(args.with_cfg3)
