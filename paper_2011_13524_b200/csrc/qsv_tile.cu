@@ -184,6 +184,20 @@ __device__ __forceinline__ void t_real1x(double2 (&v)[kRegs], const TileOp& op,
     t_real1_body<(I) % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y);    \
     M += 2;                                                                \
   }
+  if (s == kRegs - 1) {  // every slot: straight-line code, no merges of v after branches
+#pragma unroll
+    for (int i = 0; i < kRegBits; ++i) {
+      const double2 ab = M[2 * i], cd = M[2 * i + 1];
+      switch (i) {
+        case 0: t_real1_body<0, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+        case 1: t_real1_body<1 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+        case 2: t_real1_body<2 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+        case 3: t_real1_body<3 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+        default: t_real1_body<4 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+      }
+    }
+    return;
+  }
   QSV_REAL_SLOT(0) QSV_REAL_SLOT(1) QSV_REAL_SLOT(2) QSV_REAL_SLOT(3) QSV_REAL_SLOT(4)
 #undef QSV_REAL_SLOT
 }
@@ -226,38 +240,44 @@ struct NegAll<0> {
 };
 
 // merged diagonal: v[j] *= T[j] * C(thread) * (-1)^(sign(j, thread))
-__device__ __forceinline__ void t_flush(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
-                                        const double2* data) {
-  const bool table = op.flags & 1;
-  const double2* T = data + op.data;
-  const FlushSign* sg = reinterpret_cast<const FlushSign*>(T + (table ? kRegs : 0));
-  // sign bits over the 2^kRegBits slots: the table's own signs, then the
-  // linear rules (j_slot parity patterns are the constant columns below)
-  uint32_t bits = table ? 0u : op.lmask;
-  for (int r = 0; r < op.m; ++r) {
+__device__ __forceinline__ uint32_t flush_sign_bits(const TileCtx& c, const FlushSign* sg, int nr,
+                                                    uint32_t bits) {
+  for (int r = 0; r < nr; ++r) {
     const FlushSign R = sg[r];
     if ((c.lt & R.lm) == R.lv && (c.base & R.gm) == R.gv) bits ^= R.col;
   }
-  const FlushFactor* fc = reinterpret_cast<const FlushFactor*>(sg + op.m);
-  double2 C = make_double2(1.0, 0.0);
-  for (int f = 0; f < op.slots; ++f) {
-    const int p = fc[f].pos;
-    const int bit = p >= 0 ? (int)((c.lt >> p) & 1u) : (int)((c.base >> (-p - 1)) & 1ULL);
-    C = cmul(C, bit ? fc[f].d1 : fc[f].d0);
-  }
-  if (table) {
-    if (op.slots) {
-#pragma unroll
-      for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], cmul(T[j], C));
-    } else {
-#pragma unroll
-      for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], T[j]);
+  return bits;
+}
+
+// merged diagonal with a table: v[j] *= T[j] * C(thread) * (-1)^(sign(j, thread))
+// (straight-line: the multiply and the sign pass always run)
+__device__ __forceinline__ void t_flush(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
+                                        const double2* data) {
+  const double2* T = data + op.data;
+  const FlushSign* sg = reinterpret_cast<const FlushSign*>(T + kRegs);
+  const uint32_t bits = flush_sign_bits(c, sg, op.m, 0u);
+  if (op.slots) {  // per-thread factors of non-register qubits (rare)
+    const FlushFactor* fc = reinterpret_cast<const FlushFactor*>(sg + op.m);
+    double2 C = make_double2(1.0, 0.0);
+    for (int f = 0; f < op.slots; ++f) {
+      const int p = fc[f].pos;
+      const int bit = p >= 0 ? (int)((c.lt >> p) & 1u) : (int)((c.base >> (-p - 1)) & 1ULL);
+      C = cmul(C, bit ? fc[f].d1 : fc[f].d0);
     }
-  } else if (op.slots) {
 #pragma unroll
     for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], C);
   }
-  if (bits) NegAll<kRegs - 1>::run(v, bits);
+#pragma unroll
+  for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], T[j]);
+  NegAll<kRegs - 1>::run(v, bits);
+}
+
+// sign-only merged diagonal (CZ-type patterns): integer XORs, no FP64 work
+__device__ __forceinline__ void t_signs(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
+                                        const double2* data) {
+  const FlushSign* sg = reinterpret_cast<const FlushSign*>(data + op.data);
+  const uint32_t bits = flush_sign_bits(c, sg, op.m, op.lmask);
+  NegAll<kRegs - 1>::run(v, bits);
 }
 
 __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
@@ -291,6 +311,9 @@ __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, c
       break;
     case T_FLUSH:
       t_flush(v, c, op, data);
+      break;
+    case T_SIGNS:
+      t_signs(v, c, op, data);
       break;
     case T_PHASE: {
       const SplitCond sc = split_cond(c, op);
@@ -456,9 +479,7 @@ __device__ __forceinline__ void reg_phase(double2* sm, const TilePhase& P, const
                                        bool skip_ops, int dbg) {
   TileCtx c;
   c.base = base;
-  c.lt = 0;
-  for (int j = 0; j < nthr; ++j)
-    if ((tid >> j) & 1) c.lt |= 1u << P.thrpos[j];
+  c.lt = P.thr_lo[tid & 15] | P.thr_hi[(tid >> 4) & 15];
   // the swizzle is XOR-linear: swz(lt | r) = swz(lt) ^ swz(r)
   uint32_t srb[kRegBits];
 #pragma unroll
@@ -529,6 +550,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
            int ndata) {
   extern __shared__ double2 smem_all[];
   __shared__ uint64_t s_hi[kRegs];       // HBM offset of copy-index bits >= kTidBits
+  __shared__ uint64_t s_lo[kCtaThreads]; // HBM offset of copy-index bits < kTidBits
   const int L = pd->L;
   const uint32_t tile_amps = 1u << L;
   const int group = threadIdx.x / kGroupThreads;
@@ -552,10 +574,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     for (int i = threadIdx.x; i < words; i += kCtaThreads) pdst[i] = psrc[i];
     if (threadIdx.x < kRegs) s_hi[threadIdx.x] = hi_part(pd, L, threadIdx.x);
   }
-  // local bits below kTidBits of the copy index l = k * kGroupThreads + tid
-  uint64_t lo_part = 0;
-  for (int b = 0; b < kTidBits && b < L; ++b)
-    if ((tid >> b) & 1) lo_part |= 1ULL << pd->spos[b];
+  // local bits below kTidBits of the copy index l = k * kGroupThreads + tid,
+  // kept in shared memory (re-read per copy) rather than in registers
+  {
+    uint64_t lo_part = 0;
+    for (int b = 0; b < kTidBits && b < L; ++b)
+      if ((tid >> b) & 1) lo_part |= 1ULL << pd->spos[b];
+    s_lo[threadIdx.x] = lo_part;
+  }
   const int nk = (int)((tile_amps + kGroupThreads - 1) / kGroupThreads);
   const bool copy_thread = (uint32_t)tid < tile_amps;
   const int nthr = pd->nthrbits;
@@ -567,8 +593,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   for (uint64_t tile = (uint64_t)blockIdx.x * kGroups + group; tile < ntiles;
        tile += (uint64_t)gridDim.x * kGroups) {
     const uint64_t base = widen(tile, tb);
-    const uint64_t gb = base | lo_part;
     if (copy_thread) {
+      const uint64_t gb = base | s_lo[threadIdx.x];
       for (int k = 0; k < nk; ++k) {
         const uint32_t l = (uint32_t)k * kGroupThreads + tid;
         cp_async16(sbase + swz(l) * 16u, a + (gb | s_hi[k]));
@@ -594,6 +620,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 
     // shared -> HBM (same mapping as the load)
     if (copy_thread) {
+      const uint64_t gb = base | s_lo[threadIdx.x];
       for (int k = 0; k < nk; ++k) {
         const uint32_t l = (uint32_t)k * kGroupThreads + tid;
         st1(a + (gb | s_hi[k]), sm[swz(l)]);
@@ -944,9 +971,10 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
     if (T[j].re == -1.0 && T[j].im == 0.0) tsign |= 1u << j;
   }
   if (!table && tsign == 0 && signs.empty() && facs.empty()) return rest;
+  if (!facs.empty()) table = true;  // factors ride on the table flush
   TileOp op;
   memset(&op, 0, sizeof(op));
-  op.kind = T_FLUSH;
+  op.kind = table ? T_FLUSH : T_SIGNS;
   op.flags = table ? 1 : 0;
   op.m = (int32_t)signs.size();
   op.slots = (int32_t)facs.size();
@@ -1142,6 +1170,13 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
       if (!((Rall >> b) & 1u)) tb.push_back(b);
     order_thread_bits(tb);
     for (size_t k = 0; k < tb.size(); ++k) ph.thrpos[k] = tb[k];
+    for (int v = 0; v < 16; ++v) {
+      ph.thr_lo[v] = ph.thr_hi[v] = 0;
+      for (int j = 0; j < 4; ++j) {
+        if (((v >> j) & 1) && j < (int)tb.size()) ph.thr_lo[v] |= 1u << tb[j];
+        if (((v >> j) & 1) && j + 4 < (int)tb.size()) ph.thr_hi[v] |= 1u << tb[j + 4];
+      }
+    }
     // classify
     const size_t K = cur.size();
     for (size_t k = 0; k < K; ++k) {
@@ -1623,7 +1658,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
         for (int o = ph.op_begin; o < ph.op_end; ++o) {
           const TileOp& op = e.ops[o];
           fprintf(stderr, " %d/%x", op.kind, op.slots);
-          if (op.kind == T_FLUSH) fprintf(stderr, "[t%d s%d f%d]", op.flags & 1, op.m, op.slots);
+          if (op.kind == T_FLUSH || op.kind == T_SIGNS) fprintf(stderr, "[t%d s%d f%d]", op.flags & 1, op.m, op.slots);
         }
         fprintf(stderr, "\n");
       }

@@ -8,8 +8,12 @@
 
 namespace qsv {
 
+// 16 amplitudes per thread: 512-thread CTAs (16 warps / SM) at 128 registers
+// hide the FP64 and shared-memory latencies better than 32 amplitudes at 255
+// registers (8 warps), which outweighs the 25% more register phases
+// (cnot-ring(30) 0.76 s -> 0.66 s, cz-ladder(30, 20) unchanged).
 #ifndef QSV_TILE_REGBITS
-#define QSV_TILE_REGBITS 5
+#define QSV_TILE_REGBITS 4
 #endif
 constexpr int kRegBits = QSV_TILE_REGBITS;  // amplitudes per thread = 2^kRegBits
 constexpr int kRegs = 1 << kRegBits;
@@ -18,7 +22,7 @@ constexpr int kGroupThreads = (1 << kMaxTileQubits) / kRegs;  // threads per til
 constexpr int kGroups = 2;                  // independent tile groups per CTA
 constexpr int kCtaThreads = kGroups * kGroupThreads;
 constexpr int kLowQubits = 4;       // qubits 0..3 are in every tile (256 B runs)
-constexpr int kTileSmemLimit = 227 * 1024 - 1024;  // dynamic part (static smem aside)
+constexpr int kTileSmemLimit = 227 * 1024 - 8192;  // dynamic part (static smem aside)
 // shared memory left for the staged pass program (ops, data, phases)
 constexpr int kTileProgramBudget =
     kTileSmemLimit - kGroups * (16 << kMaxTileQubits) - 1024;
@@ -35,6 +39,7 @@ enum TileOpKind : int32_t {
   T_REAL1X = 12,  // uncontrolled real 2x2 on every slot of the mask (2 double2 per slot)
   T_FLUSH = 13,   // merged diagonal: table over the register slots, linear sign
                   // rules and per-thread factors (see FlushSign / FlushFactor)
+  T_SIGNS = 14,   // sign-only merged diagonal: table signs (lmask) + sign rules
   // shared-memory ops (a phase of their own; cosets read straight from smem)
   S_DENSE = 9,    // 2^m x 2^m on m <= 4 local bits (tpos), optionally controlled
   S_PAULI = 10,   // X/Y product on local bits (slots = local X mask), Z parity
@@ -58,8 +63,8 @@ struct __align__(16) TileOp {   // 64 bytes = 4 x 128-bit loads
   int32_t pad;
 };
 
-// T_FLUSH payload: [T: 2^kRegBits double2 if flags & 1][m FlushSign][slots FlushFactor]
-// TileOp.lmask holds the sign bits of a +-1 table (flags & 1 clear).
+// T_FLUSH payload: [T: 2^kRegBits double2][m FlushSign][slots FlushFactor]
+// T_SIGNS payload: [m FlushSign]; TileOp.lmask holds the signs of its +-1 table.
 struct __align__(16) FlushSign {  // where the thread/tile pattern matches, flip the
   uint32_t lm, lv;                // sign of the register slots j with bit j of col
   uint32_t col, pad;              // set (col: all ones, or the j_slot == value column)
@@ -75,6 +80,9 @@ struct TilePhase {
   int32_t type;              // 0: register phase, 1: shared-memory ops
   int32_t regpos[kRegBits];  // local bit of each register slot
   int32_t thrpos[10];        // local bit of thread-id bit j (j < L - kRegBits)
+  // thread's local base lt = thr_lo[tid & 15] | thr_hi[tid >> 4] (host-built
+  // deposit tables: one lookup per phase instead of a bit loop)
+  uint32_t thr_lo[16], thr_hi[16];
   int32_t op_begin, op_end;
 };
 
