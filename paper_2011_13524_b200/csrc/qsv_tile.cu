@@ -269,7 +269,7 @@ __device__ __forceinline__ void t_flush(double2 (&v)[kRegs], const TileCtx& c, c
   }
 #pragma unroll
   for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], T[j]);
-  NegAll<kRegs - 1>::run(v, bits);
+  if (bits) NegAll<kRegs - 1>::run(v, bits);
 }
 
 // sign-only merged diagonal (CZ-type patterns): integer XORs, no FP64 work
@@ -595,9 +595,17 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     const uint64_t base = widen(tile, tb);
     if (copy_thread) {
       const uint64_t gb = base | s_lo[threadIdx.x];
-      for (int k = 0; k < nk; ++k) {
-        const uint32_t l = (uint32_t)k * kGroupThreads + tid;
-        cp_async16(sbase + swz(l) * 16u, a + (gb | s_hi[k]));
+      if (L == kMaxTileQubits) {
+        // full tile: unrolled, swz(k * G + tid) = swz(k * G) ^ swz(tid) (XOR-linear)
+        const uint32_t st = swz((uint32_t)tid);
+#pragma unroll
+        for (int k = 0; k < kRegs; ++k)
+          cp_async16(sbase + ((swz((uint32_t)k * kGroupThreads) ^ st) << 4), a + (gb | s_hi[k]));
+      } else {
+        for (int k = 0; k < nk; ++k) {
+          const uint32_t l = (uint32_t)k * kGroupThreads + tid;
+          cp_async16(sbase + swz(l) * 16u, a + (gb | s_hi[k]));
+        }
       }
     }
     cp_async_commit();
@@ -621,9 +629,16 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     // shared -> HBM (same mapping as the load)
     if (copy_thread) {
       const uint64_t gb = base | s_lo[threadIdx.x];
-      for (int k = 0; k < nk; ++k) {
-        const uint32_t l = (uint32_t)k * kGroupThreads + tid;
-        st1(a + (gb | s_hi[k]), sm[swz(l)]);
+      if (L == kMaxTileQubits) {
+        const uint32_t st = swz((uint32_t)tid);
+#pragma unroll
+        for (int k = 0; k < kRegs; ++k)
+          st1(a + (gb | s_hi[k]), sm[swz((uint32_t)k * kGroupThreads) ^ st]);
+      } else {
+        for (int k = 0; k < nk; ++k) {
+          const uint32_t l = (uint32_t)k * kGroupThreads + tid;
+          st1(a + (gb | s_hi[k]), sm[swz(l)]);
+        }
       }
     }
     group_sync(group);  // the tile buffer is refilled next iteration
