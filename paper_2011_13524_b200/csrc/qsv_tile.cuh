@@ -8,19 +8,16 @@
 
 namespace qsv {
 
-// 16 amplitudes per thread: 512-thread CTAs (16 warps / SM) at 128 registers
-// hide the FP64 and shared-memory latencies better than 32 amplitudes at 255
-// registers (8 warps), which outweighs the 25% more register phases
-// (cnot-ring(30) 0.76 s -> 0.66 s, cz-ladder(30, 20) unchanged).
-#ifndef QSV_TILE_REGBITS
-#define QSV_TILE_REGBITS 4
-#endif
-constexpr int kRegBits = QSV_TILE_REGBITS;  // amplitudes per thread = 2^kRegBits
-constexpr int kRegs = 1 << kRegBits;
+// The tile engine is compiled twice from qsv_tile_impl.cuh, with 16 (r4) and
+// 32 (r5) amplitudes per thread.  r5 (8 warps / SM at 255 registers, five
+// register qubits per phase) is faster when a pass is mostly real-rotation
+// batches (cz-ladder(30, 20): 0.51 s vs 0.58 s: fewer shared-memory phases and
+// flushes); r4 (512-thread CTAs, 16 warps / SM at 128 registers) hides
+// latency better for complex / controlled ops (cnot-ring(30): 0.66 s vs
+// 0.69 s).  plan_program picks the variant per program (plan_select).
+constexpr int kMaxRegBits = 5;
 constexpr int kMaxTileQubits = 12;          // 2^12 amps = 64 KiB of shared memory
-constexpr int kGroupThreads = (1 << kMaxTileQubits) / kRegs;  // threads per tile group
 constexpr int kGroups = 2;                  // independent tile groups per CTA
-constexpr int kCtaThreads = kGroups * kGroupThreads;
 constexpr int kLowQubits = 4;       // qubits 0..3 are in every tile (256 B runs)
 constexpr int kTileSmemLimit = 227 * 1024 - 8192;  // dynamic part (static smem aside)
 // shared memory left for the staged pass program (ops, data, phases)
@@ -78,7 +75,7 @@ struct __align__(16) FlushFactor {  // factor d[bit] of one non-register qubit
 
 struct TilePhase {
   int32_t type;              // 0: register phase, 1: shared-memory ops
-  int32_t regpos[kRegBits];  // local bit of each register slot
+  int32_t regpos[kMaxRegBits];  // local bit of each register slot
   int32_t thrpos[10];        // local bit of thread-id bit j (j < L - kRegBits)
   // thread's local base lt = thr_lo[tid & 15] | thr_hi[tid >> 4] (host-built
   // deposit tables: one lookup per phase instead of a bit loop)
@@ -97,6 +94,7 @@ struct TilePassDev {
 
 // ---- host-side plan of one pass ----
 struct TilePlan {
+  int variant = 4;               // register bits of the kernel that runs it
   int L = 0;
   std::vector<int> qubits;       // sorted tile qubits (global positions)
   size_t dev_off = 0;            // payload offset of TilePassDev, then phases, ops
@@ -107,6 +105,23 @@ struct TilePlan {
   double hbm_bytes = 0;
 };
 
+// per-variant entry points (qsv_tile_r4.cu / qsv_tile_r5.cu)
+struct PlanMix {
+  int real_ops = 0, complex_ops = 0;  // register 2x2 ops after encoding
+};
+#define QSV_TILE_DECLARE(NS)                                                                 \
+  namespace NS {                                                                            \
+  int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts& opts,    \
+                   std::vector<Step>& steps, std::vector<TilePlan>& tiles,                  \
+                   std::vector<char>& payload, qsv_program_stats* stats, PlanMix* mix);     \
+  int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,   \
+                       cudaStream_t s);                                                     \
+  }
+QSV_TILE_DECLARE(r4)
+QSV_TILE_DECLARE(r5)
+#undef QSV_TILE_DECLARE
+
+// plan with the variant that suits the circuit (qsv_program.cu)
 int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts& opts,
                  std::vector<Step>& steps, std::vector<TilePlan>& tiles,
                  std::vector<char>& payload, qsv_program_stats* stats);

@@ -27,7 +27,17 @@
 
 #include "qsv_tile.cuh"
 
+#ifndef QSV_TILE_REGBITS
+#error "qsv_tile_impl.cuh is included by qsv_tile_r4.cu / qsv_tile_r5.cu"
+#endif
+
 namespace qsv {
+namespace QSV_TILE_NS {
+
+constexpr int kRegBits = QSV_TILE_REGBITS;  // amplitudes per thread = 2^kRegBits
+constexpr int kRegs = 1 << kRegBits;
+constexpr int kGroupThreads = (1 << kMaxTileQubits) / kRegs;  // threads per tile group
+constexpr int kCtaThreads = kGroups * kGroupThreads;
 
 // ===================================================================== device
 
@@ -1626,7 +1636,7 @@ void add_gate_step(int n, const GateDesc& g, std::vector<Step>& steps, std::vect
 
 int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_opts& opts,
                  std::vector<Step>& steps, std::vector<TilePlan>& tiles,
-                 std::vector<char>& payload, qsv_program_stats* stats) {
+                 std::vector<char>& payload, qsv_program_stats* stats, PlanMix* mix) {
   std::vector<GateDesc> gates = opts.fuse ? fuse_1q(n, gates_in) : gates_in;
   int L = opts.tile_qubits > 0 ? opts.tile_qubits : kMaxTileQubits;
   L = std::min(std::min(L, kMaxTileQubits), n);
@@ -1679,7 +1689,15 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       }
     }
     TilePlan tp;
+    tp.variant = kRegBits;
     tp.L = L;
+    if (mix) {
+      for (const TileOp& op : e.ops) {
+        const int cnt = __builtin_popcount((uint32_t)op.slots);
+        if (op.kind == T_REAL1 || op.kind == T_REAL1X) mix->real_ops += cnt;
+        if (op.kind == T_DENSE1 || op.kind == T_DENSE1X) mix->complex_ops += cnt;
+      }
+    }
     for (int q = 0; q < n; ++q)
       if ((ps.S >> q) & 1ULL) tp.qubits.push_back(q);
     tp.nphases = (int)e.phases.size();
@@ -1751,4 +1769,5 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
   return QSV_OK;
 }
 
+}  // namespace QSV_TILE_NS
 }  // namespace qsv

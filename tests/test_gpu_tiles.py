@@ -161,3 +161,19 @@ def test_real_frames_benchmark_circuits():
             st.set_Haar_random_state(9)
             circ.update_quantum_state(st)
             assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12, rf
+
+
+@pytest.mark.parametrize("variant", ["4", "5"])
+def test_both_kernel_variants(variant, monkeypatch):
+    """The planner picks the 16- or 32-amplitude tile kernel per program;
+    force each and check parity on circuits that exercise every op kind."""
+    monkeypatch.setenv("QSV_TILE_VARIANT", variant)
+    for n, L, seed in ((12, 10, 7), (17, 12, 8)):
+        for circ in (layered_circuit(n, 5, seed), random_circuit(n, 120, seed)):
+            circ.set_plan_options(tile_qubits=L)
+            st = qs.QuantumState(n)
+            st.set_Haar_random_state(seed)
+            circ.update_quantum_state(st)
+            ref = orc.haar_state(n, seed)
+            c_oracle.run_records(ref, n, circuit_records(circ))
+            assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12, (variant, n)
