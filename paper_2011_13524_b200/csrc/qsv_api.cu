@@ -29,6 +29,10 @@ int cuda_fail(cudaError_t e, const char* what) {
   return e == cudaErrorMemoryAllocation ? QSV_ENOMEM : QSV_ECUDA;
 }
 
+size_t expect_tile_scratch_bytes();
+int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
+                const std::vector<uint64_t>& zms, void* scratch, std::vector<double>& res,
+                cudaStream_t s);
 int launch_expect_sweep(const double2* bra, const double2* ket, int n, uint64_t xm,
                         const uint64_t* zm, int nt, double* partials, double* dev_out,
                         cudaStream_t s);
@@ -503,7 +507,7 @@ int qsv_expect(const qsv_state* bra, const qsv_state* ket, int nterms, const int
   }
   // group terms by flip mask (one sweep per <= kMaxTerms terms of a group)
   std::map<uint64_t, std::vector<int>> groups;
-  std::vector<uint64_t> zms(nterms);
+  std::vector<uint64_t> zms(nterms), xms(nterms);
   std::vector<int> nys(nterms);
   size_t pos = 0;
   for (int t = 0; t < nterms; ++t) {
@@ -529,10 +533,29 @@ int qsv_expect(const qsv_state* bra, const qsv_state* ket, int nterms, const int
       if (id == 2) ++ny;
     }
     zms[t] = zm;
+    xms[t] = xm;
     nys[t] = ny;
     groups[xm].push_back(t);
   }
+  // expectation values with many flip masks: tile passes (qsv_expect_tile.cu)
+  std::vector<Cplx> per_term(nterms, Cplx{0, 0});
+  bool done = false;
+  if (bra == ket && ket->n >= 12 && groups.size() > 2) {
+    DeviceGuard dg(ket->device);
+    Scratch& sc = g_analysis[ket];
+    int rc = ensure(sc, expect_tile_scratch_bytes(), ket->stream);
+    if (rc) return rc;
+    std::vector<double> tres;
+    rc = expect_tile(ket->amps, ket->n, xms, zms, sc.ptr, tres, ket->stream);
+    if (rc == QSV_OK) {
+      for (int t = 0; t < nterms; ++t) per_term[t] = {tres[2 * t], tres[2 * t + 1]};
+      done = true;
+    } else if (rc != QSV_EUNSUPPORTED) {
+      return rc;
+    }
+  }
   std::vector<Sweep> sweeps;
+  if (!done)
   for (auto& kv : groups) {
     for (size_t i = 0; i < kv.second.size(); i += kMaxTerms) {
       Sweep s;
@@ -545,10 +568,11 @@ int qsv_expect(const qsv_state* bra, const qsv_state* ket, int nterms, const int
     }
   }
   std::vector<double> res;
-  int rc = run_sweeps(bra, ket, sweeps, res);
-  if (rc) return rc;
+  if (!done) {
+    int rc = run_sweeps(bra, ket, sweeps, res);
+    if (rc) return rc;
+  }
   // sum_t coef_t * i^ny_t * S_t, accumulated in term order
-  std::vector<Cplx> per_term(nterms, Cplx{0, 0});
   for (size_t i = 0; i < sweeps.size(); ++i)
     for (size_t j = 0; j < sweeps[i].term.size(); ++j)
       per_term[sweeps[i].term[j]] = {res[2 * kMaxTerms * i + 2 * j],
