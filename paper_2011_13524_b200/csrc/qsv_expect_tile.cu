@@ -39,7 +39,9 @@ struct XGroup {
 
 struct XTerm {
   uint32_t zl;     // sign mask over local bits
-  uint32_t pad;
+  uint32_t kmask;  // bit k: parity of ((k * 256) ^ xl) & zl over the k-indexed local bits
+                   // (bits 8..11) and of the flip mask's low bits: the per-amplitude
+                   // sign is bit k of kmask ^ parity(tid & zl_lo & ~...) (see kernel)
   uint64_t zg;     // sign mask over the other (tile-constant) bits
 };
 
@@ -50,7 +52,7 @@ struct XPass {
   XTerm terms[kXMaxTerms];
 };
 
-__global__ void __launch_bounds__(kXThreads)
+__global__ void __launch_bounds__(kXThreads, 2)
     k_expect_tile(const double2* __restrict__ a, const XPass* __restrict__ gp, FixedBits tb,
                   uint64_t ntiles, double* __restrict__ partials) {
   extern __shared__ double2 sm[];  // 2^12 amplitudes (64 KiB, dynamic)
@@ -82,25 +84,28 @@ __global__ void __launch_bounds__(kXThreads)
 #pragma unroll
     for (int k = 0; k < kXPer; ++k) sm[k * kXThreads + tid] = ld1(a + (base | lo | s_hi[k]));
     __syncthreads();
+    double2 v[kXPer];  // this thread's amplitudes, shared by every group
+#pragma unroll
+    for (int k = 0; k < kXPer; ++k) v[k] = sm[k * kXThreads + tid];
     for (int g = 0; g < P.ngroups; ++g) {
       const uint32_t xl = P.groups[g].xl;
       double2 p[kXPer];
 #pragma unroll
       for (int k = 0; k < kXPer; ++k) {
-        const uint32_t l = (uint32_t)(k * kXThreads + tid);
-        const double2 v = sm[l];
-        const double2 w = xl ? sm[l ^ xl] : v;
-        p[k] = make_double2(fma(v.x, w.x, v.y * w.y), fma(v.x, w.y, -v.y * w.x));
+        const double2 w = xl ? sm[(uint32_t)(k * kXThreads + tid) ^ xl] : v[k];
+        p[k] = make_double2(fma(v[k].x, w.x, v[k].y * w.y), fma(v[k].x, w.y, -v[k].y * w.x));
       }
       const int t1 = P.groups[g].first + P.groups[g].count;
       for (int t = P.groups[g].first; t < t1; ++t) {
         const XTerm T = P.terms[t];
-        const int par0 = __popcll(base & T.zg) & 1;
+        // sign of x ^ xl for x = k * 256 + tid: tile part, thread part, k part
+        const uint32_t tpar =
+            (uint32_t)((__popcll(base & T.zg) ^ __popc((uint32_t)tid & T.zl & 0xffu)) & 1);
+        const uint32_t M = T.kmask ^ (0u - tpar);
         double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 0; k < kXPer; ++k) {
-          const uint32_t l = (uint32_t)(k * kXThreads + tid);
-          const bool neg = (__popc((l ^ xl) & T.zl) ^ par0) & 1;
+          const bool neg = (M >> k) & 1u;
           acc.x += neg ? -p[k].x : p[k].x;
           acc.y += neg ? -p[k].y : p[k].y;
         }
@@ -258,13 +263,19 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
         if (terms[k].xm == m) {
           XTerm T;
           T.zl = 0;
-          T.pad = 0;
+          T.kmask = 0;
           T.zg = 0;
           for (int q = 0; q < n; ++q)
             if ((terms[k].zm >> q) & 1ULL) {
               if (local_of[q] >= 0) T.zl |= 1u << local_of[q];
               else T.zg |= 1ULL << q;
             }
+          // parity((x ^ xl) & zl) = parity(tid & zl & 0xff) ^ parity((k << 8) & zl)
+          //                          ^ parity(xl & zl)
+          for (int kk = 0; kk < kXPer; ++kk)
+            if ((__builtin_popcount(((uint32_t)kk << 8) & T.zl) ^
+                 __builtin_popcount(G.xl & T.zl)) & 1)
+              T.kmask |= 1u << kk;
           P.terms[order.size()] = T;
           order.push_back(k);
           ++G.count;
