@@ -379,16 +379,22 @@ class ShardedQuantumState:
         return self._allreduce(complex(sum(s.norm2() for s in self.shards.values()))).real
 
     # -- gates ----------------------------------------------------------------
-    def plan(self, records):
-        """Split records into segments of local gates and swap lists.
+    def plan(self, records, lookahead=None):
+        """Split records into segments of local gates and qubit remaps.
 
-        Returns a list of ("swap", g_phys, l_phys) / ("seg", [records]) and
-        updates nothing (pure function of the current map)."""
+        Returns a list of ("swap", [g_phys...], [l_phys...]) / ("seg",
+        [records]); pure function of the current map.  When a gate needs
+        global qubits, every other global qubit needed within the next
+        ``lookahead`` gates (default 2n) is brought local in the same remap
+        (one exchange step moving (1 - 2^-k) of the shard instead of k steps
+        moving half of it each); the local qubits that become global are the
+        ones whose next use is furthest away (Belady), high positions first."""
         phys = list(self.phys)
         L = self.L
         steps = []
         seg = []
         act = [active_qubits(r) for r in records]
+        window = 2 * self.n if lookahead is None else int(lookahead)
 
         def next_use(q, start):
             for k in range(start, len(records)):
@@ -402,16 +408,21 @@ class ShardedQuantumState:
                 if seg:
                     steps.append(("seg", seg))
                     seg = []
-                busy = set(act[i])
-                for q in need:
-                    cands = [lq for lq in range(self.n) if phys[lq] < L and lq not in busy]
-                    if not cands:
-                        raise ValueError("gate needs more local qubits than the shard has")
-                    victim = max(cands, key=lambda lq: (next_use(lq, i + 1), phys[lq]))
-                    g, l = phys[q], phys[victim]
-                    steps.append(("swap", g, l))
-                    phys[q], phys[victim] = l, g
-                    busy.add(victim)
+                soon = sorted((next_use(q, i), q) for q in range(self.n)
+                              if phys[q] >= L and q not in need)
+                want = list(need) + [q for k, q in soon if k < i + window]
+                busy = set(act[i]) | set(want)
+                cands = [lq for lq in range(self.n) if phys[lq] < L and lq not in busy]
+                cands.sort(key=lambda lq: (next_use(lq, i + 1), phys[lq]), reverse=True)
+                if len(cands) < len(need):
+                    raise ValueError("gate needs more local qubits than the shard has")
+                want = want[:len(cands)]
+                victims = cands[:len(want)]
+                gs = [phys[q] for q in want]
+                ls = [phys[v] for v in victims]
+                steps.append(("swap", gs, ls))
+                for q, v, g, lp in zip(want, victims, gs, ls):
+                    phys[q], phys[v] = lp, g
             seg.append(rec)
         if seg:
             steps.append(("seg", seg))
@@ -420,7 +431,7 @@ class ShardedQuantumState:
     def apply_records(self, records):
         for step in self.plan(records):
             if step[0] == "swap":
-                self._swap(step[1], step[2])
+                self._remap(step[1], step[2])
             else:
                 self.stats["segments"] += 1
                 for r, s in self.shards.items():
@@ -452,7 +463,7 @@ class ShardedQuantumState:
             recs = [("dense", tuple(sorted(need)), None, ())]
             for step in self.plan(recs):
                 if step[0] == "swap":
-                    self._swap(step[1], step[2])
+                    self._remap(step[1], step[2])
         total = 0j
         for r, s in self.shards.items():
             loc = []
@@ -473,58 +484,100 @@ class ShardedQuantumState:
         return self._allreduce(total)
 
     # -- the exchange ---------------------------------------------------------
+    def _remap(self, gs, ls):
+        """Swap physical global qubits gs[j] with local qubits ls[j] in one
+        exchange step.  Amplitude (rank r, local x) moves to rank r with bit
+        g_j := x_{l_j} and local x with bit l_j := r_{g_j}: rank r trades its
+        slice {x : x_ls = d} with partner r[gs := d], the same slice index on
+        both sides, so the step is 2^k - 1 pairwise slice exchanges.  Round s
+        pairs every rank with r ^ spread(s) (a perfect matching per round, so
+        blocking send/recv pairs cannot deadlock).  Bytes sent per rank:
+        (1 - 2^-k) * 16 * 2^L."""
+        L = self.L
+        k = len(gs)
+        if k == 0:
+            return
+
+        def gbits(r):
+            return sum(((r >> (g - L)) & 1) << j for j, g in enumerate(gs))
+
+        for s in range(1, 1 << k):
+            m = 0
+            for j in range(k):
+                if (s >> j) & 1:
+                    m |= 1 << (gs[j] - L)
+            done = set()
+            for r in self.owned:
+                if r in done:
+                    continue
+                partner = r ^ m
+                mine = self._slice_view(r, ls, gbits(partner))
+                if partner in self.shards:
+                    theirs = self._slice_view(partner, ls, gbits(r))
+                    tmp = mine.clone()
+                    mine.copy_(theirs)
+                    theirs.copy_(tmp)
+                    done.add(partner)
+                else:
+                    self._exchange(mine, partner)
+                done.add(r)
+                self.stats["bytes_sent"] += 16 << (L - k)
+        # logical map: the qubits at gs[j] and ls[j] trade places
+        inv = self._logical_of()
+        for g, lp in zip(gs, ls):
+            qg, ql = inv[g], inv[lp]
+            self.phys[qg], self.phys[ql] = lp, g
+        self.stats["swaps"] += 1
+        self.stats["remapped_qubits"] = self.stats.get("remapped_qubits", 0) + k
+
     def _swap(self, g, l):
         """Exchange physical global qubit g with local qubit l."""
-        L = self.L
-        step = 1 << (g - L)
-        done = set()
-        for r in self.owned:
-            if r in done:
-                continue
-            partner = r ^ step
-            b = (r >> (g - L)) & 1
-            mine = self._half_view(r, l, 1 - b)
-            if partner in self.shards:
-                theirs = self._half_view(partner, l, b)
-                tmp = mine.clone()
-                mine.copy_(theirs)
-                theirs.copy_(tmp)
-                done.add(partner)
-            else:
-                self._exchange(mine, partner)
-            done.add(r)
-            self.stats["bytes_sent"] += 16 << (L - 1)
-        # logical map: whoever sat at g now sits at l and vice versa
-        inv = self._logical_of()
-        qg, ql = inv[g], inv[l]
-        self.phys[qg], self.phys[ql] = l, g
-        self.stats["swaps"] += 1
+        self._remap([g], [l])
 
-    def _half_view(self, r, l, v):
-        """Float64 view of shard r restricted to local bit l == v, shaped
-        (outer, 2^l * 2) (complex as float pairs)."""
+    def _slice_view(self, r, ls, d):
+        """Float64 view of shard r restricted to local bits ls[j] == bit j
+        of d (complex as float pairs): one strided N-d view, no copy."""
         t = self.shards[r].tensor()
-        L = self.L
-        return t.view(1 << (L - 1 - l), 2, 2 << l)[:, v, :]
+        order = sorted(range(len(ls)), key=lambda j: -ls[j])
+        shape, index, prev = [], [], self.L
+        for j in order:
+            p = ls[j]
+            shape += [1 << (prev - p - 1), 2]
+            index += [slice(None), (d >> j) & 1]
+            prev = p
+        shape.append(2 << prev)
+        index.append(slice(None))
+        return t.view(shape)[tuple(index)]
+
+    def _chunks(self, view):
+        """Split a strided view into sub-views of at most chunk_bytes."""
+        if view.numel() * 8 <= self.chunk_bytes:
+            yield view
+            return
+        if view.dim() == 1:
+            step = max(1, self.chunk_bytes // 8)
+            for a in range(0, view.shape[0], step):
+                yield view[a:a + step]
+            return
+        if view.shape[0] == 1:
+            yield from self._chunks(view[0])
+            return
+        row = (view.numel() // view.shape[0]) * 8
+        if row > self.chunk_bytes:
+            for a in range(view.shape[0]):
+                yield from self._chunks(view[a])
+            return
+        rows = max(1, self.chunk_bytes // row)
+        for a in range(0, view.shape[0], rows):
+            yield view[a:a + rows]
 
     def _exchange(self, view, partner):
         """Send ``view`` to partner and overwrite it with the partner's data,
-        chunked through staging buffers."""
+        chunked through staging buffers (NCCL send/recv over NVLink on the
+        GPU box, gloo in the CPU tests)."""
         import torch
         dist = self.dist
-        outer, inner = view.shape
-        row = inner * 8
-        rows = max(1, self.chunk_bytes // max(row, 1))
-        if rows >= outer:
-            chunks = [(0, outer, None)]
-        else:
-            chunks = [(a, min(a + rows, outer), None) for a in range(0, outer, rows)]
-        if inner * 8 > self.chunk_bytes and outer == 1:
-            # contiguous half larger than a chunk: split the inner axis
-            cols = self.chunk_bytes // 8
-            chunks = [(0, 1, (c, min(c + cols, inner))) for c in range(0, inner, cols)]
-        for a, b, cols in chunks:
-            part = view[a:b] if cols is None else view[a:b, cols[0]:cols[1]]
+        for part in self._chunks(view):
             send = part.contiguous() if not part.is_contiguous() else part.clone()
             recv = torch.empty_like(send)
             ops = [dist.P2POp(dist.isend, send, partner, group=self.group),
@@ -532,3 +585,19 @@ class ShardedQuantumState:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
             part.copy_(recv)
+
+
+def plan_exchange_bytes(num_qubits, world, records, lookahead=None):
+    """Host-only model of a sharded run (no shards allocated): number of
+    remap steps, qubits remapped and NVLink bytes sent per rank, for the
+    combined HBM + NVLink roofline."""
+    eng = ShardedQuantumState.__new__(ShardedQuantumState)
+    p = int(round(math.log2(world)))
+    eng.n, eng.p, eng.L = num_qubits, p, num_qubits - p
+    eng.phys = list(range(num_qubits))
+    steps = eng.plan(records, lookahead)
+    remaps = [s for s in steps if s[0] == "swap"]
+    sent = sum((16 << eng.L) - (16 << (eng.L - len(s[1]))) for s in remaps)
+    return {"remaps": len(remaps), "qubits_remapped": sum(len(s[1]) for s in remaps),
+            "bytes_sent_per_rank": float(sent),
+            "segments": sum(1 for s in steps if s[0] == "seg")}

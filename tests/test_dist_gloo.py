@@ -110,3 +110,60 @@ def test_gloo_processes_match_oracle(world):
         assert abs(norm - orc.squared_norm(ref)) <= 1e-12
         assert abs(e - e_ref) <= 1e-11
         assert stats["swaps"] > 0
+
+
+def test_multi_qubit_remaps_batch_global_qubits():
+    """cz-ladder needs every qubit non-diagonally in every layer: the planner
+    brings all global qubits local in one remap per layer (k = log2 P), which
+    moves (1 - 2^-k) of a shard instead of k/2 with one swap per qubit."""
+    from paper_2011_13524_b200.dist import plan_exchange_bytes
+    n, world = 36, 8
+    recs = orc.cz_ladder_records(n, 20, seed=1)
+    batched = plan_exchange_bytes(n, world, recs)
+    single = plan_exchange_bytes(n, world, recs, lookahead=0)
+    assert batched["qubits_remapped"] >= 3 * 20
+    assert batched["remaps"] <= 22
+    assert batched["bytes_sent_per_rank"] < 0.7 * single["bytes_sent_per_rank"]
+    # small instance, every virtual rank, chunked N-d slice exchanges
+    n = 9
+    recs = orc.cz_ladder_records(n, 3, seed=2)
+    st = ShardedQuantumState(n, world=8, owned=list(range(8)),
+                             backend=lambda L, r: OracleShard(L, r), chunk_bytes=64)
+    st.load(orc.haar_state(n, 4))
+    st.apply_records(recs)
+    ref = orc.run_records(orc.haar_state(n, 4), n, recs)
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+    assert st.stats["remapped_qubits"] > st.stats["swaps"]
+
+
+def _worker_k(rank, world, port, n, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        recs = orc.cz_ladder_records(n, 3, seed=3)
+        st = ShardedQuantumState(n, backend=lambda L, r: OracleShard(L, r), chunk_bytes=96)
+        st.load(orc.haar_state(n, 6))
+        st.apply_records(recs)
+        q.put((rank, st.get_vector(), dict(st.stats)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_multi_qubit_remap_processes():
+    n, world = 8, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_k, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = orc.run_records(orc.haar_state(n, 6), n, orc.cz_ladder_records(n, 3, seed=3))
+    for rank, vec, stats in res:
+        assert np.max(np.abs(vec - ref)) <= 1e-12, rank
+        assert stats["remapped_qubits"] > stats["swaps"]
