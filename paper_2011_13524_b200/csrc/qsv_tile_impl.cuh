@@ -182,6 +182,22 @@ __device__ __forceinline__ void t_real1(double2 (&v)[kRegs], const TileCtx& c, c
     t_real1_body<I, false>(v, sc, ab.x, ab.y, cd.x, cd.y);
 }
 
+template <int NS>
+__device__ __forceinline__ void t_real_prefix(double2 (&v)[kRegs], const double2* M) {
+  const SplitCond sc{true, 0, 0};
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    const double2 ab = M[2 * i], cd = M[2 * i + 1];
+    switch (i) {
+      case 0: t_real1_body<0, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+      case 1: t_real1_body<1 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+      case 2: t_real1_body<2 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+      case 3: t_real1_body<3 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+      default: t_real1_body<4 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
+    }
+  }
+}
+
 // batched uncontrolled 1-qubit ops on the slots of a mask (slot order)
 __device__ __forceinline__ void t_real1x(double2 (&v)[kRegs], const TileOp& op,
                                          const double2* data) {
@@ -194,19 +210,13 @@ __device__ __forceinline__ void t_real1x(double2 (&v)[kRegs], const TileOp& op,
     t_real1_body<(I) % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y);    \
     M += 2;                                                                \
   }
-  if (s == kRegs - 1) {  // every slot: straight-line code, no merges of v after branches
-#pragma unroll
-    for (int i = 0; i < kRegBits; ++i) {
-      const double2 ab = M[2 * i], cd = M[2 * i + 1];
-      switch (i) {
-        case 0: t_real1_body<0, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
-        case 1: t_real1_body<1 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
-        case 2: t_real1_body<2 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
-        case 3: t_real1_body<3 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
-        default: t_real1_body<4 % kRegBits, false>(v, sc, ab.x, ab.y, cd.x, cd.y); break;
-      }
-    }
-    return;
+  // prefix masks (slots 0..m-1, the usual shape: slots are assigned in order
+  // of first use) run as straight-line code, no merges of v after branches
+  switch (s) {
+    case (1 << kRegBits) - 1: t_real_prefix<kRegBits>(v, M); return;
+    case (1 << (kRegBits - 1)) - 1: t_real_prefix<kRegBits - 1>(v, M); return;
+    case (1 << (kRegBits - 2)) - 1: t_real_prefix<kRegBits - 2>(v, M); return;
+    default: break;
   }
   QSV_REAL_SLOT(0) QSV_REAL_SLOT(1) QSV_REAL_SLOT(2) QSV_REAL_SLOT(3) QSV_REAL_SLOT(4)
 #undef QSV_REAL_SLOT
