@@ -101,6 +101,16 @@ int qsv_apply_pauli(qsv_state* st, const int* targets, const int* ids, int m,
 int qsv_apply_pauli_rot(qsv_state* st, const int* targets, const int* ids, int m,
                         double angle, const int* control_qubits,
                         const int* control_values, int nc);
+/* qsv_apply_sparse  <- kernels.apply_sparse / apply_permutation
+ *                      (kernels.py:141-152, 176-185): per coset of the
+ *                      targets, out[r] = sum over entries (r, c, v) of
+ *                      v * in[c]; rows without entries become 0 (sparse
+ *                      matrix product semantics).  A permutation table t is
+ *                      the entries (t[s], s, 1).  Cost is O(nnz) per coset
+ *                      instead of the dense 4^m. */
+int qsv_apply_sparse(qsv_state* st, const int* targets, int m, int nnz, const int* rows,
+                     const int* cols, const double* values, const int* control_qubits,
+                     const int* control_values, int nc);
 
 /* ------------------------------------------------------- state algebra
  * qsv_norm2   <- get_squared_norm (state.py:75-76)
@@ -174,6 +184,7 @@ int qsv_trace_pairs(const qsv_state* st, double out_re_im[2]);
 #define QSV_OP_DIAG 2
 #define QSV_OP_PAULI 3
 #define QSV_OP_PAULI_ROT 4
+#define QSV_OP_SPARSE 5       /* data: nnz complex values; sp_rows / sp_cols */
 
 typedef struct qsv_op {
   int32_t kind;                            /* QSV_OP_*                     */
@@ -184,7 +195,10 @@ typedef struct qsv_op {
   int32_t control_qubits[QSV_MAX_CONTROLS];
   int32_t control_values[QSV_MAX_CONTROLS];
   double angle;                            /* PAULI_ROT                    */
-  const double* data;                      /* DENSE: 4^m, DIAG: 2^m complex */
+  const double* data;                      /* DENSE: 4^m, DIAG: 2^m complex, SPARSE: nnz */
+  int32_t nnz;                             /* SPARSE: entry count          */
+  const int32_t* sp_rows;                  /* SPARSE: row of each entry    */
+  const int32_t* sp_cols;                  /* SPARSE: column of each entry */
 } qsv_op;
 
 typedef struct qsv_plan_opts {

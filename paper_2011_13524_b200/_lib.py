@@ -27,6 +27,7 @@ OP_DENSE = 1
 OP_DIAG = 2
 OP_PAULI = 3
 OP_PAULI_ROT = 4
+OP_SPARSE = 5
 
 
 class QsvOp(C.Structure):
@@ -40,6 +41,9 @@ class QsvOp(C.Structure):
         ("control_values", C.c_int32 * MAX_CONTROLS),
         ("angle", C.c_double),
         ("data", C.c_void_p),
+        ("nnz", C.c_int32),
+        ("sp_rows", C.c_void_p),
+        ("sp_cols", C.c_void_p),
     ]
 
 
@@ -101,6 +105,7 @@ _SIGS = {
     "qsv_apply_diag": ([_P, _IP, _I, _DP, _IP, _IP, _I], _I),
     "qsv_apply_pauli": ([_P, _IP, _IP, _I, _IP, _IP, _I], _I),
     "qsv_apply_pauli_rot": ([_P, _IP, _IP, _I, C.c_double, _IP, _IP, _I], _I),
+    "qsv_apply_sparse": ([_P, _IP, _I, _I, _IP, _IP, _DP, _IP, _IP, _I], _I),
     "qsv_norm2": ([_P, C.POINTER(C.c_double)], _I),
     "qsv_scale": ([_P, C.c_double, C.c_double], _I),
     "qsv_add": ([_P, _P], _I),

@@ -96,6 +96,31 @@ std::vector<char> make_payload(const GateDesc& g) {
   } else if (g.kind == QSV_OP_DIAG && g.m > 5) {
     out.resize(((size_t)1 << g.m) * sizeof(double2));
     memcpy(out.data(), g.data.data(), out.size());
+  } else if (g.kind == QSV_OP_SPARSE) {
+    // [values (CSR order)][coset offsets][row pointers][columns]
+    const size_t D = (size_t)1 << g.m, nnz = g.data.size();
+    std::vector<size_t> order(nnz);
+    for (size_t e = 0; e < nnz; ++e) order[e] = e;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](size_t x, size_t y) { return g.sp_rows[x] < g.sp_rows[y]; });
+    out.resize(nnz * sizeof(double2) + D * sizeof(uint64_t) + (D + 1 + nnz) * sizeof(int32_t));
+    double2* vals = reinterpret_cast<double2*>(out.data());
+    uint64_t* offs = reinterpret_cast<uint64_t*>(out.data() + nnz * sizeof(double2));
+    int32_t* rptr = reinterpret_cast<int32_t*>(offs + D);
+    int32_t* cols = rptr + D + 1;
+    for (size_t e = 0; e < nnz; ++e) {
+      vals[e] = make_double2(g.data[order[e]].re, g.data[order[e]].im);
+      cols[e] = g.sp_cols[order[e]];
+    }
+    for (size_t z = 0; z <= D; ++z) rptr[z] = 0;
+    for (size_t e = 0; e < nnz; ++e) ++rptr[g.sp_rows[e] + 1];
+    for (size_t z = 0; z < D; ++z) rptr[z + 1] += rptr[z];
+    for (size_t z = 0; z < D; ++z) {
+      uint64_t o = 0;
+      for (int j = 0; j < g.m; ++j)
+        if ((z >> j) & 1) o |= 1ULL << g.targets[j];
+      offs[z] = o;
+    }
   }
   return out;
 }
@@ -416,6 +441,21 @@ int qsv_apply_pauli(qsv_state* st, const int* targets, const int* ids, int m, co
     return QSV_EINVAL;
   }
   GateDesc g = make_desc(QSV_OP_PAULI, targets, ids, m, cq, cv, nc);
+  return apply_desc(st, g);
+}
+
+int qsv_apply_sparse(qsv_state* st, const int* targets, int m, int nnz, const int* rows,
+                     const int* cols, const double* values, const int* cq, const int* cv, int nc) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (m < 0 || m > QSV_MAX_TARGETS || nc < 0 || nc > QSV_MAX_CONTROLS || nnz < 0) {
+    set_error("unsupported target/control/entry count (%d, %d, %d)", m, nc, nnz);
+    return QSV_EINVAL;
+  }
+  GateDesc g = make_desc(QSV_OP_SPARSE, targets, nullptr, m, cq, cv, nc);
+  g.data.resize(nnz);
+  if (nnz) memcpy(g.data.data(), values, nnz * sizeof(Cplx));
+  g.sp_rows.assign(rows, rows + nnz);
+  g.sp_cols.assign(cols, cols + nnz);
   return apply_desc(st, g);
 }
 

@@ -289,6 +289,38 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Sparse / permutation (kernels.py:141-152, 176-185): cosets staged in shared
+// memory like k_dense_smem, each output row summed over its CSR entries
+// (O(nnz) per coset instead of 4^K).  Payload: values, coset offsets,
+// row pointers, columns.
+__global__ void __launch_bounds__(kThreads)
+    k_sparse_smem(double2* __restrict__ a, FixedBits fb, int K, const double2* __restrict__ vals,
+                  const uint64_t* __restrict__ offs, const int32_t* __restrict__ rptr,
+                  const int32_t* __restrict__ cols, uint64_t ncos) {
+  extern __shared__ double2 sm[];
+  const int D = 1 << K;
+  const int per_block = max(1, kThreads / D);  // cosets per block
+  for (uint64_t c0 = (uint64_t)blockIdx.x * per_block; c0 < ncos;
+       c0 += (uint64_t)gridDim.x * per_block) {
+    const uint64_t rem = ncos - c0;
+    const int nco = rem < (uint64_t)per_block ? (int)rem : per_block;
+    for (int i = threadIdx.x; i < nco * D; i += blockDim.x) {
+      const int c = i / D, w = i % D;
+      sm[i] = a[widen(c0 + c, fb) + offs[w]];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nco * D; i += blockDim.x) {
+      const int c = i / D, z = i % D;
+      const double2* in = sm + c * D;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int e = __ldg(rptr + z); e < __ldg(rptr + z + 1); ++e)
+        acc = cfma(__ldg(vals + e), in[__ldg(cols + e)], acc);
+      a[widen(c0 + c, fb) + offs[z]] = acc;
+    }
+    __syncthreads();
+  }
+}
+
 // --------------------------------------------------------------------------
 // Pauli product on pairs (i, j = i ^ xmask) (kernels.py:202-235):
 //   new_i = alpha psi_i + beta phi(j) psi_j,  new_j = alpha psi_j + beta phi(i) psi_i
@@ -571,6 +603,19 @@ int validate_gate(int n, const GateDesc& g) {
     }
     used |= 1ULL << q;
   }
+  if (g.kind == QSV_OP_SPARSE) {
+    const int D = 1 << g.m;
+    if (g.sp_rows.size() != g.data.size() || g.sp_cols.size() != g.data.size()) {
+      set_error("sparse entries: rows, columns and values differ in length");
+      return QSV_EINVAL;
+    }
+    for (size_t e = 0; e < g.data.size(); ++e)
+      if (g.sp_rows[e] < 0 || g.sp_rows[e] >= D || g.sp_cols[e] < 0 || g.sp_cols[e] >= D) {
+        set_error("sparse entry (%d, %d) outside a %dx%d matrix", g.sp_rows[e], g.sp_cols[e], D,
+                  D);
+        return QSV_EINVAL;
+      }
+  }
   if (g.kind == QSV_OP_PAULI || g.kind == QSV_OP_PAULI_ROT) {
     for (int j = 0; j < g.m; ++j)
       if (g.ids[j] < 0 || g.ids[j] > 3) {
@@ -591,7 +636,7 @@ int validate_gate(int n, const GateDesc& g) {
       set_error("diagonal length does not match %d targets", g.m);
       return QSV_EINVAL;
     }
-  } else {
+  } else if (g.kind != QSV_OP_SPARSE) {  // sparse entries checked above
     set_error("unknown op kind %d", g.kind);
     return QSV_EINVAL;
   }
@@ -634,6 +679,37 @@ int launch_gate(double2* a, int n, const GateDesc& g0, const Cplx* dev_data, cud
   }
   int lowest_ctl = 64;
   for (int j = 0; j < g.nc; ++j) lowest_ctl = std::min(lowest_ctl, g.cq[j]);
+
+  if (g.kind == QSV_OP_SPARSE) {
+    if (!dev_data) {
+      set_error("internal: sparse gate needs a device payload");
+      return QSV_EINVAL;
+    }
+    int fixed2[kMaxFixed];
+    for (int j = 0; j < g.nc; ++j) fixed2[j] = g.cq[j];
+    for (int j = 0; j < g.m; ++j) fixed2[g.nc + j] = g.targets[j];
+    FixedBits fb2 = make_fixed(fixed2, g.nc + g.m, cval);
+    const int D = 1 << g.m;
+    const size_t nnz = g.data.size();
+    const char* base = reinterpret_cast<const char*>(dev_data);
+    const double2* vals = reinterpret_cast<const double2*>(base);
+    const uint64_t* offs = reinterpret_cast<const uint64_t*>(base + nnz * sizeof(double2));
+    const int32_t* rptr = reinterpret_cast<const int32_t*>(offs + D);
+    const int32_t* cols = rptr + D + 1;
+    const uint64_t ncos = dim >> (g.nc + g.m);
+    const int per_block = std::max(1, kThreads / D);
+    const size_t smem = sizeof(double2) * (size_t)per_block * D;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_sparse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set = true;
+    }
+    uint64_t nblk = (ncos + per_block - 1) / per_block;
+    nblk = std::max<uint64_t>(1, std::min<uint64_t>(nblk, 148ULL * 64));
+    k_sparse_smem<<<(unsigned)nblk, kThreads, smem, s>>>(a, fb2, g.m, vals, offs, rptr, cols, ncos);
+    QSV_CHECK_LAUNCH("k_sparse_smem");
+    return QSV_OK;
+  }
 
   if (g.kind == QSV_OP_DIAG) {
     if (g.m == 1 && g.nc == 0) {

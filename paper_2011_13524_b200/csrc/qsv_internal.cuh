@@ -154,7 +154,8 @@ struct GateDesc {
   int cq[QSV_MAX_CONTROLS];
   int cv[QSV_MAX_CONTROLS];
   double angle;
-  std::vector<Cplx> data;  // DENSE: 4^m, DIAG: 2^m
+  std::vector<Cplx> data;  // DENSE: 4^m, DIAG: 2^m, SPARSE: nnz values
+  std::vector<int32_t> sp_rows, sp_cols;  // SPARSE entries (row, column)
   // real-frame form of an uncontrolled 1-qubit dense gate (tile planner):
   // data = R diag(rf_b) with R = rf_r real; the tile encoder applies
   // diag(rf_b) inside a merged diagonal flush and R as real arithmetic

@@ -92,6 +92,15 @@ static int convert_ops(int n, const qsv_op* ops, int nops, std::vector<GateDesc>
       }
       g.data.resize(D * D);
       memcpy(g.data.data(), op.data, D * D * sizeof(Cplx));
+    } else if (op.kind == QSV_OP_SPARSE) {
+      if (op.nnz < 0 || (op.nnz > 0 && (!op.data || !op.sp_rows || !op.sp_cols))) {
+        set_error("op %d: sparse gate without entries", i);
+        return QSV_EINVAL;
+      }
+      g.data.resize(op.nnz);
+      if (op.nnz) memcpy(g.data.data(), op.data, op.nnz * sizeof(Cplx));
+      g.sp_rows.assign(op.sp_rows, op.sp_rows + op.nnz);
+      g.sp_cols.assign(op.sp_cols, op.sp_cols + op.nnz);
     } else if (op.kind == QSV_OP_DIAG) {
       const size_t D = (size_t)1 << op.m;
       if (!op.data) {

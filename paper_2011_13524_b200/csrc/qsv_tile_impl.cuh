@@ -1478,7 +1478,7 @@ bool euler_real(const M2& U, Cplx a[2], Cplx b[2], double R[4]) {
 // qubits a gate acts on non-diagonally
 uint64_t nondiag_mask(const GateDesc& g) {
   uint64_t m = 0;
-  if (g.kind == QSV_OP_DENSE) {
+  if (g.kind == QSV_OP_DENSE || g.kind == QSV_OP_SPARSE) {
     for (int j = 0; j < g.m; ++j) m |= 1ULL << g.targets[j];
   } else if (g.kind == QSV_OP_PAULI || g.kind == QSV_OP_PAULI_ROT) {
     for (int j = 0; j < g.m; ++j)
@@ -1614,6 +1614,7 @@ std::vector<GateDesc> realify(int n, const std::vector<GateDesc>& in) {
 double gate_fp64_flops(int n, const GateDesc& g) {
   const double amps = std::ldexp(1.0, n - g.nc);
   if (g.kind == QSV_OP_DENSE) return amps * 8.0 * (double)(1 << g.m);
+  if (g.kind == QSV_OP_SPARSE) return amps * 8.0 * (double)g.data.size() / (double)(1 << g.m);
   if (g.kind == QSV_OP_DIAG) {
     if (g.m == 0 && g.data.size() == 1 && g.data[0].re == -1.0 && g.data[0].im == 0.0) return 0.0;
     return amps * 6.0;

@@ -337,3 +337,37 @@ def test_program_stats_and_reuse():
     circ.update_quantum_state(a)
     circ.update_quantum_state(b)
     assert np.array_equal(a.get_vector(), b.get_vector())
+
+
+@pytest.mark.parametrize("m,nc", [(1, 0), (2, 1), (5, 0), (7, 2), (10, 0)])
+def test_sparse_and_permutation_gates(m, nc):
+    """SparseMatrix / ReversibleBoolean / SWAP / FREDKIN run the O(nnz) sparse
+    kernel (kernels.py:141-152, 176-185), directly and inside circuits."""
+    n = 14
+    rng = np.random.default_rng(m * 7 + nc)
+    perm = [int(v) for v in rng.permutation(n)]
+    tg, ctl = perm[:m], perm[m:m + nc]
+    dim = 1 << m
+    table = [int(v) for v in rng.permutation(dim)]
+    ents = [(int(r), int(c), complex(*rng.normal(size=2)))
+            for r, c in zip(rng.integers(0, dim, 3 * dim), rng.integers(0, dim, 3 * dim))]
+    ents = list({(r, c): (r, c, v) for r, c, v in ents}.values())
+    gates = [qg.ReversibleBoolean(tg, lambda z, d, t=table: t[z]), qg.SparseMatrix(tg, ents)]
+    for g in gates:
+        for q in ctl:
+            g.add_control_qubit(q, 1)
+    recs = [g._core.record() for g in gates]
+    ref = orc.run_records(orc.haar_state(n, 2), n, recs)
+    st = haar(n, 2)
+    for g in gates:
+        g.update_quantum_state(st)
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+    c = qs.QuantumCircuit(n)
+    for g in gates:
+        c.add_gate(g)
+    c.add_gate(qg.SWAP(perm[0], perm[-1]))
+    c.add_gate(qg.FREDKIN(perm[1], perm[2], perm[3]))
+    st2 = haar(n, 2)
+    c.update_quantum_state(st2)
+    ref2 = orc.run_records(orc.haar_state(n, 2), n, circuit_records(c))
+    assert np.max(np.abs(st2.get_vector() - ref2)) <= 1e-12
