@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
            const double2* __restrict__ g_data, FixedBits tb, uint64_t ntiles, int nops,
            int ndata) {
   extern __shared__ double2 smem_all[];
-  __shared__ uint64_t s_hi[kRegs];       // HBM offset of copy-index bits >= kTidBits
+  __shared__ uint64_t s_hi[kRegs + 1];   // HBM offset of copy-index bits >= kTidBits (+ flag)
   __shared__ uint64_t s_lo[kCtaThreads]; // HBM offset of copy-index bits < kTidBits
   const int L = pd->L;
   const uint32_t tile_amps = 1u << L;
@@ -608,7 +608,18 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   const bool active = tid < (1 << nthr);
   double2* sm = smem_all + (size_t)group * tile_amps;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+  // Stagger: the two groups run identical work, so started together they
+  // stay in lockstep and load / store their tiles at the same time, leaving
+  // the FP64 pipe idle meanwhile.  Group 1 starts once group 0 is half way
+  // through its first tile, so one group's HBM traffic overlaps the other's
+  // math from then on.
+  volatile int* s_go = reinterpret_cast<volatile int*>(&s_hi[kRegs]);
+  if (threadIdx.x == 0) *s_go = (kGroups < 2 || (pd->debug & 16)) ? 1 : 0;
   __syncthreads();
+  if (group == 1)
+    while (*s_go == 0) __nanosleep(256);
+  const int half_phase = nphases / 2;
+  bool first = true;
 
   for (uint64_t tile = (uint64_t)blockIdx.x * kGroups + group; tile < ntiles;
        tile += (uint64_t)gridDim.x * kGroups) {
@@ -633,6 +644,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     group_sync(group);
 
     for (int ph = 0; ph < nphases; ++ph) {
+      if (group == 0 && first && ph == half_phase && tid == 0) *s_go = 1;
       const TilePhase& P = s_ph[ph];
       const int ob = P.op_begin, oe = P.op_end;
       if (P.type != 0) {
@@ -662,7 +674,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       }
     }
     group_sync(group);  // the tile buffer is refilled next iteration
+    if (group == 0 && first && tid == 0) *s_go = 1;
+    first = false;
   }
+  if (group == 0 && tid == 0) *s_go = 1;  // no tile / no phase: release group 1
 }
 
 // ======================================================================= host
