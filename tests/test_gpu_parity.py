@@ -14,7 +14,7 @@ import pytest
 import paper_2011_13524_b200 as qs
 from paper_2011_13524_b200 import gate as qg
 from paper_2011_13524_b200 import workloads
-from paper_2011_13524_b200 import _optimizer
+from paper_2011_13524_b200 import _gates, _optimizer
 from paper_2011_13524_b200._circuit import circuit_records
 from paper_2011_13524_b200.circuit import QuantumCircuitOptimizer
 from paper_2011_13524_b200.quantum_operator import create_quantum_operator_from_openfermion_text
@@ -371,3 +371,27 @@ def test_sparse_and_permutation_gates(m, nc):
     c.update_quantum_state(st2)
     ref2 = orc.run_records(orc.haar_state(n, 2), n, circuit_records(c))
     assert np.max(np.abs(st2.get_vector() - ref2)) <= 1e-12
+
+
+def test_cfg4_full_size_mirror_n30():
+    """BASELINE cfg4 at its full size: cz-ladder(30, depth 20, seed 1) through
+    the planner's default path (fusion, real frames, tile passes), then its
+    inverse; size-independent checks on the device (no 16 GiB host copies):
+    |U^dag U psi - psi|^2 and the norm."""
+    n = 30
+    circ = workloads.generate_cz_ladder(n, 20, seed=1)
+    inv = qs.QuantumCircuit(n)
+    for g in reversed(circ._core.gates):
+        if isinstance(g, _gates.PauliRotationGate):
+            inv.add_gate(qg.PauliRotation(list(g.targets), list(g.pauli_ids), -g.angle))
+        else:
+            inv.add_gate(g.copy())  # CZ is its own inverse
+    st = qs.QuantumState(n)
+    st.set_random_state_device(11)
+    start = st.copy()
+    circ.update_quantum_state(st)
+    assert abs(st.get_squared_norm() - 1.0) <= 1e-12
+    inv.update_quantum_state(st)
+    start.multiply_coef(-1.0)
+    st.add_state(start)
+    assert st.get_squared_norm() <= 1e-20
