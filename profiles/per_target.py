@@ -13,6 +13,17 @@ import paper_2011_13524_b200 as qs  # noqa: E402
 from paper_2011_13524_b200 import gate as qg  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 28
+if os.environ.get("L2_FETCH"):
+    # experiment: cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity = 0x05, bytes)
+    import ctypes
+    torch.cuda.init()
+    rt = ctypes.CDLL("libcudart.so.12")
+    v = ctypes.c_size_t()
+    rt.cudaDeviceGetLimit(ctypes.byref(v), 0x05)
+    print("L2 fetch granularity was", v.value, flush=True)
+    print("set rc", rt.cudaDeviceSetLimit(0x05, ctypes.c_size_t(int(os.environ["L2_FETCH"]))))
+    rt.cudaDeviceGetLimit(ctypes.byref(v), 0x05)
+    print("now", v.value, flush=True)
 kinds = sys.argv[2:] or ["CZ", "CNOT"]
 st = qs.QuantumState(n)
 st.set_random_state_device(3)
