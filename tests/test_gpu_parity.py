@@ -395,3 +395,37 @@ def test_cfg4_full_size_mirror_n30():
     start.multiply_coef(-1.0)
     st.add_state(start)
     assert st.get_squared_norm() <= 1e-20
+
+
+def test_n32_indexing_beyond_2_31():
+    """A 32-qubit state (64 GiB, indices past 2^31 and 2^32 bytes): layers of
+    H / RX / CZ / CNOT through tile passes and per-gate kernels, then the
+    mirror circuit; checked through device reductions only."""
+    n = 32
+    c = qs.QuantumCircuit(n)
+    for q in range(n):
+        c.add_gate(qg.H(q))
+    for q in range(0, n - 1, 2):
+        c.add_gate(qg.CZ(q, q + 1))
+    for q in range(n):
+        c.add_gate(qg.RX(q, 0.1 * (q + 1)))
+    c.add_gate(qg.CNOT(31, 0))
+    c.add_gate(qg.CNOT(0, 31))
+    inv = qs.QuantumCircuit(n)
+    for g in reversed(c._core.gates):
+        if isinstance(g, _gates.PauliRotationGate):
+            inv.add_gate(qg.PauliRotation(list(g.targets), list(g.pauli_ids), -g.angle))
+        else:
+            inv.add_gate(g.copy())  # H, CZ, CNOT are self-inverse
+    st = qs.QuantumState(n)
+    c.update_quantum_state(st)
+    assert abs(st.get_squared_norm() - 1.0) <= 1e-12
+    p31 = st.get_marginal_probability([2] * 31 + [1])
+    assert 0.0 < p31 < 1.0
+    st2 = qs.QuantumState(n)
+    for g in c._core.gates:  # the per-gate kernels on the same circuit
+        g.apply(st2)
+    assert abs(st2.get_marginal_probability([2] * 31 + [1]) - p31) <= 1e-12
+    del st2
+    inv.update_quantum_state(st)
+    assert abs(st.get_marginal_probability([0] * n) - 1.0) <= 1e-12
