@@ -37,6 +37,8 @@ enum TileOpKind : int32_t {
   T_FLUSH = 13,   // merged diagonal: table over the register slots, linear sign
                   // rules and per-thread factors (see FlushSign / FlushFactor)
   T_SIGNS = 14,   // sign-only merged diagonal: table signs (lmask) + sign rules
+  T_PHASES = 15,  // merged phase rules (controlled phases involving thread / tile
+                  // bits): per-thread scalar and per-slot factors (FlushPhase)
   // shared-memory ops (a phase of their own; cosets read straight from smem)
   S_DENSE = 9,    // 2^m x 2^m on m <= 4 local bits (tpos), optionally controlled
   S_PAULI = 10,   // X/Y product on local bits (slots = local X mask), Z parity
@@ -71,6 +73,15 @@ struct __align__(16) FlushFactor {  // factor d[bit] of one non-register qubit
   int32_t pos;                      // >= 0 local (thread) bit, < 0: -(global bit)-1
   int32_t pad[3];
   double2 d0, d1;
+};
+
+// T_PHASES payload: [m FlushPhase]; TileOp.slots = mask of slots with rules,
+// flags & 1: some rule is a scalar (slot < 0).
+struct __align__(16) FlushPhase {  // factor f where the thread/tile pattern matches,
+  uint32_t lm, lv;                 // on every amplitude (slot < 0) or on those with
+  int32_t slot, pad;               // register slot `slot` == 1
+  uint64_t gm, gv;
+  double2 f;
 };
 
 struct TilePhase {

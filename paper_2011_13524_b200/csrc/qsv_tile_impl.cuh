@@ -292,6 +292,41 @@ __device__ __forceinline__ void t_flush(double2 (&v)[kRegs], const TileCtx& c, c
   if (bits) NegAll<kRegs - 1>::run(v, bits);
 }
 
+// merged phase rules: per-thread scalar C and per-slot factors ph[i] (on the
+// amplitudes whose slot i is 1): 4 FP64 ops per amplitude for the scalar and
+// 2 per slot, however many controlled phases were merged
+__device__ __forceinline__ void t_phases(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
+                                         const double2* data) {
+  const FlushPhase* pr = reinterpret_cast<const FlushPhase*>(data + op.data);
+  double2 C = make_double2(1.0, 0.0);
+  double2 ph[kRegBits];
+#pragma unroll
+  for (int i = 0; i < kRegBits; ++i) ph[i] = make_double2(1.0, 0.0);
+  for (int r = 0; r < op.m; ++r) {
+    const FlushPhase R = pr[r];
+    if ((c.lt & R.lm) != R.lv || (c.base & R.gm) != R.gv) continue;
+    switch (R.slot) {
+      case 0: ph[0] = cmul(ph[0], R.f); break;
+      case 1: ph[1 % kRegBits] = cmul(ph[1 % kRegBits], R.f); break;
+      case 2: ph[2 % kRegBits] = cmul(ph[2 % kRegBits], R.f); break;
+      case 3: ph[3 % kRegBits] = cmul(ph[3 % kRegBits], R.f); break;
+      case 4: ph[4 % kRegBits] = cmul(ph[4 % kRegBits], R.f); break;
+      default: C = cmul(C, R.f); break;
+    }
+  }
+  if (op.flags & 1) {
+#pragma unroll
+    for (int j = 0; j < kRegs; ++j) v[j] = cmul(v[j], C);
+  }
+#pragma unroll
+  for (int i = 0; i < kRegBits; ++i) {
+    if (!((op.slots >> i) & 1)) continue;
+#pragma unroll
+    for (int j = 0; j < kRegs; ++j)
+      if ((j >> i) & 1) v[j] = cmul(v[j], ph[i]);
+  }
+}
+
 // sign-only merged diagonal (CZ-type patterns): integer XORs, no FP64 work
 __device__ __forceinline__ void t_signs(double2 (&v)[kRegs], const TileCtx& c, const TileOp& op,
                                         const double2* data) {
@@ -334,6 +369,9 @@ __device__ __forceinline__ void t_apply(double2 (&v)[kRegs], const TileCtx& c, c
       break;
     case T_SIGNS:
       t_signs(v, c, op, data);
+      break;
+    case T_PHASES:
+      t_phases(v, c, op, data);
       break;
     case T_PHASE: {
       const SplitCond sc = split_cond(c, op);
@@ -934,6 +972,13 @@ void emit_op(Encoded& e, TileOp op, const std::vector<Cplx>& data) {
   e.ops.push_back(op);
 }
 
+double d_op_cost(const TileOp& op) {
+  if (op.kind == T_PHASE) return (op.flags & 2) ? 0.0 : 4.0;
+  if (op.kind == T_PHASES)
+    return ((op.flags & 1) ? 4.0 : 0.0) + 2.0 * __builtin_popcount((uint32_t)op.slots);
+  return 4.0;  // T_DIAG / T_PARITY: one complex multiply per amplitude
+}
+
 // Merge a layer of D ops: returns the ops that could not be merged.
 std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, const int* regpos) {
   uint32_t Rall = 0;
@@ -946,6 +991,38 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
   std::vector<Cplx> T(kRegs, Cplx{1, 0});
   std::vector<FlushSign> signs;
   std::vector<FlushFactor> facs;
+  std::vector<FlushPhase> phrules;
+  auto unit = [](Cplx f) { return std::fabs(std::hypot(f.re, f.im) - 1.0) <= 1e-14; };
+  // factor f where (thread pattern lm/lv, tile pattern gm/gv) holds and, if
+  // jm has a bit, where that register slot equals the bit of jv
+  auto add_phase = [&](uint32_t lm, uint32_t lv, uint64_t gm, uint64_t gv, uint32_t jm,
+                       uint32_t jv, Cplx f) {
+    FlushPhase r;
+    memset(&r, 0, sizeof(r));
+    r.lm = lm;
+    r.lv = lv;
+    r.gm = gm;
+    r.gv = gv;
+    if (!jm) {
+      r.slot = -1;
+      r.f = make_double2(f.re, f.im);
+      phrules.push_back(r);
+      return;
+    }
+    const int sl = __builtin_ctz(jm);
+    if (jv & jm) {
+      r.slot = sl;
+      r.f = make_double2(f.re, f.im);
+      phrules.push_back(r);
+    } else {  // factor on slot == 0: f overall, conj(f) where the slot is 1
+      r.slot = -1;
+      r.f = make_double2(f.re, f.im);
+      phrules.push_back(r);
+      r.slot = sl;
+      r.f = make_double2(f.re, -f.im);
+      phrules.push_back(r);
+    }
+  };
   std::vector<PhaseOp> rest;
   bool changed = false;
   auto jpat = [&](uint32_t mask, uint32_t val, uint32_t* jm, uint32_t* jv) {
@@ -967,6 +1044,11 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
       if (op.gmask == 0 && tm == 0) {
         for (int j = 0; j < kRegs; ++j)
           if (((uint32_t)j & jm) == jv) T[j] = cm(T[j], f);
+        changed = true;
+        continue;
+      }
+      if (!(f.re == -1.0 && f.im == 0.0) && unit(f) && __builtin_popcount(jm) <= 1) {
+        add_phase(tm, op.lval & tm, op.gmask, op.gval, jm, jv, f);
         changed = true;
         continue;
       }
@@ -1000,6 +1082,27 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
         changed = true;
         continue;
       }
+      if (op.m == 1 && (op.lmask & Rall) == 0 && (op.lmask || op.gmask) &&
+          unit(po.data[0]) && unit(po.data[1])) {
+        // 1-qubit diagonal with controls on thread / tile bits
+        const int p = op.tpos[0];
+        const uint32_t tm = op.lmask, tv = op.lval;
+        if (p >= 0 && slot_of[p] >= 0) {
+          const uint32_t jm = 1u << slot_of[p];
+          add_phase(tm, tv, op.gmask, op.gval, 0, 0, po.data[0]);
+          const Cplx r = cm(po.data[1], cconj(po.data[0]));  // d1 / d0 for unit d0
+          add_phase(tm, tv, op.gmask, op.gval, jm, jm, r);
+        } else if (p >= 0) {  // target on a thread bit
+          add_phase(tm | (1u << p), tv, op.gmask, op.gval, 0, 0, po.data[0]);
+          add_phase(tm | (1u << p), tv | (1u << p), op.gmask, op.gval, 0, 0, po.data[1]);
+        } else {  // target on a tile bit
+          const uint64_t gb = 1ULL << (-p - 1);
+          add_phase(tm, tv, op.gmask | gb, op.gval, 0, 0, po.data[0]);
+          add_phase(tm, tv, op.gmask | gb, op.gval | gb, 0, 0, po.data[1]);
+        }
+        changed = true;
+        continue;
+      }
       if (op.m == 1 && op.lmask == 0 && op.gmask == 0) {  // non-register qubit
         FlushFactor f;
         memset(&f, 0, sizeof(f));
@@ -1014,6 +1117,25 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
     rest.push_back(po);
   }
   if (!changed) return rest;
+  if (!phrules.empty()) {  // one T_PHASES op after the flush (diagonals commute)
+    TileOp pop;
+    memset(&pop, 0, sizeof(pop));
+    pop.kind = T_PHASES;
+    pop.m = (int32_t)phrules.size();
+    std::vector<Cplx> pdata;
+    int scalar = 0;
+    for (const FlushPhase& r : phrules) {
+      if (r.slot < 0) scalar = 1;
+      else pop.slots |= 1 << r.slot;
+      Cplx w[3];
+      memcpy(w, &r, sizeof(r));
+      for (int k = 0; k < 3; ++k) pdata.push_back(w[k]);
+    }
+    pop.flags = scalar;
+    rest.insert(rest.begin(), PhaseOp{});
+    rest.front().op = pop;
+    rest.front().data = pdata;  // emitted (and costed) by the caller with the other `rest` ops
+  }
   bool table = false;
   uint32_t tsign = 0;
   for (int j = 0; j < kRegs; ++j) {
@@ -1047,10 +1169,6 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
   return rest;
 }
 
-double d_op_cost(const TileOp& op) {
-  if (op.kind == T_PHASE) return (op.flags & 2) ? 0.0 : 4.0;
-  return 4.0;  // T_DIAG / T_PARITY: one complex multiply per amplitude
-}
 
 void emit_rlayer(Encoded& e, const std::vector<PhaseOp>& rl) {
   // uncontrolled 1-qubit ops are collected into slot-mask batches; a batch

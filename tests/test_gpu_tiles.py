@@ -177,3 +177,30 @@ def test_both_kernel_variants(variant, monkeypatch):
             ref = orc.haar_state(n, seed)
             c_oracle.run_records(ref, n, circuit_records(circ))
             assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12, (variant, n)
+
+
+def qft_circuit(n, inverse_bits=0):
+    import math
+    c = qs.QuantumCircuit(n)
+    for i in range(n - 1, -1, -1):
+        c.add_gate(qg.H(i))
+        for j in range(i - 1, -1, -1):
+            g = qg.DiagonalMatrix([i], [1, np.exp(1j * math.pi / (1 << (i - j)))])
+            g.add_control_qubit(j, 1 if (j + inverse_bits) % 3 else 0)
+            c.add_gate(g)
+    return c
+
+
+@pytest.mark.parametrize("n,L", [(14, 12), (18, 10), (21, 12)])
+def test_qft_controlled_phases_merge(n, L):
+    """Controlled phases between register, thread and tile bits merge into
+    per-thread scalar / per-slot phase rules (T_PHASES); control value 0
+    included."""
+    circ = qft_circuit(n, inverse_bits=1)
+    circ.set_plan_options(tile_qubits=L)
+    st = qs.QuantumState(n)
+    st.set_Haar_random_state(n)
+    circ.update_quantum_state(st)
+    ref = orc.haar_state(n, n)
+    c_oracle.run_records(ref, n, circuit_records(circ))
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
