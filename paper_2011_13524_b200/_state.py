@@ -197,6 +197,22 @@ class StateVector:
             self._cregs.extend([0] * (index + 1 - len(self._cregs)))
         self._cregs[index] = int(value)
 
+    # -- qsimcore attribute names (state.py:22-31) ----------------------------
+    @property
+    def amplitudes(self) -> np.ndarray:
+        """Host copy of the amplitudes (qsimcore exposes its numpy buffer;
+        here the buffer is in HBM, so in-place edits of the returned array do
+        not reach the state -- assign to ``amplitudes`` or call ``load``)."""
+        return self.get_vector()
+
+    @amplitudes.setter
+    def amplitudes(self, value) -> None:
+        self.load(value)
+
+    @property
+    def classical_registers(self) -> list:
+        return self._cregs
+
     def synchronize(self) -> None:
         check(lib.qsv_sync(self._h))
 

@@ -429,3 +429,21 @@ def test_n32_indexing_beyond_2_31():
     del st2
     inv.update_quantum_state(st)
     assert abs(st.get_marginal_probability([0] * n) - 1.0) <= 1e-12
+
+
+def test_core_style_usage():
+    """Core-level script (qsimcore names): Circuit.update_state with a seed,
+    StateVector.amplitudes read / assign, classical registers."""
+    import paper_2011_13524_b200.core as core
+    c = core.Circuit(3)
+    c.add_gate(core.H(0))
+    c.add_gate(core.CNOT(0, 1))
+    c.add_gate(core.Measurement(1, 0))
+    st = core.StateVector(3)
+    c.update_state(st, rng=7)
+    a = st.amplitudes
+    assert abs(np.sum(np.abs(a) ** 2) - 1.0) <= 1e-14
+    bit = st.classical_registers[0]
+    assert abs(abs(a[3 * bit]) - 1.0) <= 1e-14
+    st.amplitudes = np.eye(8, dtype=np.complex128)[5]
+    assert st.get_vector()[5] == 1.0

@@ -162,3 +162,26 @@ def test_commutation_labels():
     assert not _optimizer.commutation_check(G.RX(0, 0.1), G.CZ(0, 1))
     assert _optimizer.commutation_check(G.CNOT(0, 1), G.RZ(0, 0.3))
     assert _optimizer.commutation_check(G.Identity(0), G.H(0))
+
+
+def test_core_module_exports_reference_core_names():
+    """paper_2011_13524_b200.core carries the reference's qsimcore names
+    (pkg/src/qsimcore/__init__.py) for scripts written against the core."""
+    import paper_2011_13524_b200.core as core
+    names = ["AdaptiveGate", "AmplitudeDampingNoise", "BasicGate", "BitFlipNoise", "CNOT", "CZ",
+             "Circuit", "CircuitFormatError", "CptpMap", "DenseGate", "DensityMatrix",
+             "DephasingNoise", "DepolarizingNoise", "DiagonalGate", "FREDKIN", "GeneralOperator",
+             "H", "Identity", "Instrument", "Measurement", "Observable", "P0", "P1",
+             "ParametricCircuit", "ParametricPauliRotation", "ParametricRX", "ParametricRY",
+             "ParametricRZ", "PauliGate", "PauliProduct", "PauliRotationGate", "PermutationGate",
+             "ProbabilisticMap", "QuantumGate", "RX", "RY", "RZ", "RandomUnitary", "S", "SWAP",
+             "Sdag", "SparseGate", "StateVector", "T", "TOFFOLI", "Tdag",
+             "TwoQubitDepolarizingNoise", "U1", "U2", "U3", "WILDCARD", "X", "Y", "Z",
+             "add_observable_rotation", "circuit_from_dict", "circuit_to_dict",
+             "commutation_check", "density_from_pure", "drop_qubit", "dump_circuit",
+             "gate_from_dict", "gate_to_dict", "inner_product", "load_circuit", "merge",
+             "merge_all", "optimize_heavy", "optimize_light", "parse_openfermion_text",
+             "parse_pauli_string", "permutate_qubit", "sqrtX", "sqrtXdag", "sqrtY", "sqrtYdag",
+             "tensor_product"]
+    missing = [n for n in names if not hasattr(core, n)]
+    assert not missing, missing
