@@ -1840,6 +1840,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
         const int cnt = __builtin_popcount((uint32_t)op.slots);
         if (op.kind == T_REAL1 || op.kind == T_REAL1X) mix->real_ops += cnt;
         if (op.kind == T_DENSE1 || op.kind == T_DENSE1X) mix->complex_ops += cnt;
+        if (op.kind == S_DENSE || op.kind == S_PAULI) mix->complex_ops += 1;
       }
     }
     for (int q = 0; q < n; ++q)

@@ -25,7 +25,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
     PlanMix mix;
     int rc = r5::plan_program(n, gates, opts, s5, t5, p5, &st5, &mix);
     if (rc) return rc;
-    if (force == 5 || mix.real_ops >= 2 * mix.complex_ops) {
+    if (force == 5 || (mix.real_ops > 0 && mix.real_ops >= 2 * mix.complex_ops)) {
       // the caller's vectors start empty, so offsets and indices carry over
       steps.swap(s5);
       tiles.swap(t5);
