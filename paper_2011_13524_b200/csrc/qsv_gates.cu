@@ -289,6 +289,35 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Dense K = 5 (fused blocks of optimize_heavy(5), kernels.py:100-106): the
+// 32x32 matrix is staged in shared memory once per block and read as
+// broadcasts; each thread holds one coset's 32 amplitudes in registers and
+// computes its 32 outputs (1024 complex FMA per coset, FP64-bound).
+__global__ void __launch_bounds__(kThreads)
+    k_dense5(double2* __restrict__ a, FixedBits fb, const double2* __restrict__ mat,
+             const uint64_t* __restrict__ offs, uint64_t ncos) {
+  constexpr int D = 32;
+  __shared__ double2 sM[D * D];
+  __shared__ uint64_t sO[D];
+  for (int i = threadIdx.x; i < D * D; i += kThreads) sM[i] = mat[i];
+  if (threadIdx.x < D) sO[threadIdx.x] = offs[threadIdx.x];
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t c = (uint64_t)blockIdx.x * kThreads + threadIdx.x; c < ncos; c += stride) {
+    const uint64_t x0 = widen(c, fb);
+    double2 in[D];
+#pragma unroll
+    for (int w = 0; w < D; ++w) in[w] = ld1(a + (x0 | sO[w]));
+#pragma unroll 4
+    for (int z = 0; z < D; ++z) {
+      double2 acc = cmul(sM[z * D], in[0]);
+#pragma unroll
+      for (int w = 1; w < D; ++w) acc = cfma(sM[z * D + w], in[w], acc);
+      st1(a + (x0 | sO[z]), acc);
+    }
+  }
+}
+
 // Sparse / permutation (kernels.py:141-152, 176-185): cosets staged in shared
 // memory like k_dense_smem, each output row summed over its CSR entries
 // (O(nnz) per coset instead of 4^K).  Payload: values, coset offsets,
@@ -832,6 +861,14 @@ int launch_gate(double2* a, int n, const GateDesc& g0, const Cplx* dev_data, cud
   }
   const int D = 1 << m;
   const uint64_t* offs = reinterpret_cast<const uint64_t*>(dev_data + (size_t)D * D);
+  if (m == 5) {
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((ncos + kThreads - 1) / kThreads, 148ULL * 8));
+    k_dense5<<<grid, kThreads, 0, s>>>(a, fb, reinterpret_cast<const double2*>(dev_data), offs,
+                                       ncos);
+    QSV_CHECK_LAUNCH("k_dense5");
+    return QSV_OK;
+  }
   const int per_block = std::max(1, kThreads / D);
   const size_t smem = sizeof(double2) * (size_t)per_block * D;
   if (smem > 48 * 1024) {

@@ -57,9 +57,8 @@ struct __align__(16) TileOp {   // 64 bytes = 4 x 128-bit loads
   uint64_t gmask;     // control pattern over global (non-tile) bits
   uint64_t gval;
   uint64_t zg;        // PARITY/PAULI: sign mask over global bits
-  int8_t tpos[4];     // DIAG: target position; >= 0 local bit, < 0: -(global bit)-1
-                      // S_DENSE: local bit of matrix index bit j
-  int32_t pad;
+  int8_t tpos[8];     // DIAG: target position; >= 0 local bit, < 0: -(global bit)-1
+                      // S_DENSE: local bit of matrix index bit j (up to 5 targets)
 };
 
 // T_FLUSH payload: [T: 2^kRegBits double2][m FlushSign][slots FlushFactor]
@@ -118,7 +117,8 @@ struct TilePlan {
 
 // per-variant entry points (qsv_tile_r4.cu / qsv_tile_r5.cu)
 struct PlanMix {
-  int real_ops = 0, complex_ops = 0;  // register 2x2 ops after encoding
+  int real_ops = 0, complex_ops = 0;  // register 2x2 ops after encoding (+ narrow smem ops)
+  int wide_dense = 0;                 // 5-target shared-memory dense ops
 };
 #define QSV_TILE_DECLARE(NS)                                                                 \
   namespace NS {                                                                            \

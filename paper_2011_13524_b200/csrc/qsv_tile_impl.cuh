@@ -481,7 +481,7 @@ __device__ __forceinline__ void s_dense(double2* sm, int L, const TileOp& op,
         if ((w >> j) & 1) l |= 1u << op.tpos[j];
       in[w] = sm[swz(l)];
     }
-#pragma unroll
+#pragma unroll(K >= 5 ? 1 : D)  // 5 targets: keep the 32 inputs + one row live only
     for (int z = 0; z < D; ++z) {
       double2 acc = cmul((data[op.data + z * D]), in[0]);
 #pragma unroll
@@ -527,6 +527,7 @@ __device__ __noinline__ void s_apply(double2* sm, int L, const TileOp& op,
     case 2: s_dense<2>(sm, L, op, data, tid); break;
     case 3: s_dense<3>(sm, L, op, data, tid); break;
     case 4: s_dense<4>(sm, L, op, data, tid); break;
+    case 5: s_dense<5>(sm, L, op, data, tid); break;
   }
 }
 
@@ -838,7 +839,7 @@ std::vector<GateDesc> fuse_1q(int n, const std::vector<GateDesc>& in) {
 bool active_qubits(const GateDesc& g, uint64_t* act) {
   *act = 0;
   if (g.kind == QSV_OP_DENSE) {
-    if (g.m > 4) return false;
+    if (g.m > 5) return false;  // up to 5 targets run as shared-memory phases
     for (int j = 0; j < g.m; ++j) *act |= 1ULL << g.targets[j];
     return true;
   }
@@ -1793,7 +1794,10 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
   const size_t G = gates.size();
   std::vector<uint64_t> act(G, 0);
   std::vector<char> ok(G, 0), done(G, 0);
-  for (size_t i = 0; i < G; ++i) ok[i] = active_qubits(gates[i], &act[i]) && popc64(act[i]) <= L;
+  // a gate fits a tile only together with the always-present low qubits
+  const uint64_t lowq = (n >= 64) ? ~0ULL : ((1ULL << std::min(kLowQubits, n)) - 1);
+  for (size_t i = 0; i < G; ++i)
+    ok[i] = active_qubits(gates[i], &act[i]) && popc64(act[i] | lowq) <= L;
   size_t first = 0;
   while (true) {
     while (first < G && done[first]) ++first;
@@ -1804,7 +1808,8 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       continue;
     }
     PassSel ps = select_pass(n, L, gates, act, ok, done, first);
-    if (ps.taken.size() == 1) {
+    if (ps.taken.size() <= 1) {
+      if (ps.taken.empty()) ps.taken.push_back((int)first);  // cannot happen (ok[] checks fit)
       // a lone gate is cheaper as its own streaming kernel
       add_gate_step(n, gates[ps.taken[0]], steps, payload, stats);
       done[ps.taken[0]] = 1;
@@ -1840,7 +1845,8 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
         const int cnt = __builtin_popcount((uint32_t)op.slots);
         if (op.kind == T_REAL1 || op.kind == T_REAL1X) mix->real_ops += cnt;
         if (op.kind == T_DENSE1 || op.kind == T_DENSE1X) mix->complex_ops += cnt;
-        if (op.kind == S_DENSE || op.kind == S_PAULI) mix->complex_ops += 1;
+        if (op.kind == S_DENSE && op.m >= 5) mix->wide_dense += 1;
+        else if (op.kind == S_DENSE || op.kind == S_PAULI) mix->complex_ops += 1;
       }
     }
     for (int q = 0; q < n; ++q)

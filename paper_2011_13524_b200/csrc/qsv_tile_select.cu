@@ -1,6 +1,8 @@
 // Variant selection for the tile engine (see qsv_tile.cuh): plan with the
 // 32-amplitude kernel (r5) and keep it when the encoded passes are mostly
-// real-rotation batches; otherwise re-plan for the 16-amplitude kernel (r4).
+// real-rotation batches or 5-target dense blocks; otherwise re-plan for the
+// 16-amplitude kernel (r4).  Measured (profiles/variant_ab.py, time_fused.py):
+// cz-ladder r5, cnot-ring / QV / QFT / heavy(2..4) r4, heavy(5) r5 (2x).
 // QSV_TILE_VARIANT=4|5 forces one (A/B experiments).
 #include <cstdlib>
 
@@ -25,7 +27,10 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
     PlanMix mix;
     int rc = r5::plan_program(n, gates, opts, s5, t5, p5, &st5, &mix);
     if (rc) return rc;
-    if (force == 5 || (mix.real_ops > 0 && mix.real_ops >= 2 * mix.complex_ops)) {
+    // r5 for real-rotation batches (fewer phases / flushes) and for 5-target
+    // dense blocks (their 32-amplitude cosets need the larger register file)
+    const int r5_score = mix.real_ops / 2 + 4 * mix.wide_dense;
+    if (force == 5 || (r5_score > 0 && r5_score >= mix.complex_ops)) {
       // the caller's vectors start empty, so offsets and indices carry over
       steps.swap(s5);
       tiles.swap(t5);
