@@ -17,12 +17,8 @@ namespace qsv {
 // 0.69 s).  plan_program picks the variant per program (plan_select).
 constexpr int kMaxRegBits = 5;
 constexpr int kMaxTileQubits = 12;          // 2^12 amps = 64 KiB of shared memory
-constexpr int kGroups = 2;                  // independent tile groups per CTA
 constexpr int kLowQubits = 4;       // qubits 0..3 are in every tile (256 B runs)
 constexpr int kTileSmemLimit = 227 * 1024 - 8192;  // dynamic part (static smem aside)
-// shared memory left for the staged pass program (ops, data, phases)
-constexpr int kTileProgramBudget =
-    kTileSmemLimit - kGroups * (16 << kMaxTileQubits) - 1024;
 
 // ---- device-side program records (all POD, stored in the payload) ----
 enum TileOpKind : int32_t {

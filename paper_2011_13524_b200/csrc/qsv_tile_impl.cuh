@@ -37,7 +37,20 @@ namespace QSV_TILE_NS {
 constexpr int kRegBits = QSV_TILE_REGBITS;  // amplitudes per thread = 2^kRegBits
 constexpr int kRegs = 1 << kRegBits;
 constexpr int kGroupThreads = (1 << kMaxTileQubits) / kRegs;  // threads per tile group
+#ifndef QSV_TILE_GROUPS
+#define QSV_TILE_GROUPS 2
+#endif
+// widest dense gate run inside a tile pass (shared-memory phase).  5-target
+// blocks stay standalone (k_dense5 is FP64-bound either way, and a 32-input
+// s_dense in the same kernel raises the interpreter's register spills).
+#ifndef QSV_TILE_MAX_DENSE
+#define QSV_TILE_MAX_DENSE 4
+#endif
+constexpr int kGroups = QSV_TILE_GROUPS;  // independent tile groups per CTA
 constexpr int kCtaThreads = kGroups * kGroupThreads;
+// shared memory left for the staged pass program (ops, data, phases)
+constexpr int kTileProgramBudget =
+    kTileSmemLimit - kGroups * (16 << kMaxTileQubits) - 1024;
 
 // ===================================================================== device
 
@@ -527,7 +540,9 @@ __device__ __noinline__ void s_apply(double2* sm, int L, const TileOp& op,
     case 2: s_dense<2>(sm, L, op, data, tid); break;
     case 3: s_dense<3>(sm, L, op, data, tid); break;
     case 4: s_dense<4>(sm, L, op, data, tid); break;
+#if QSV_TILE_MAX_DENSE >= 5
     case 5: s_dense<5>(sm, L, op, data, tid); break;
+#endif
   }
 }
 
@@ -653,11 +668,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   // through its first tile, so one group's HBM traffic overlaps the other's
   // math from then on.
   volatile int* s_go = reinterpret_cast<volatile int*>(&s_hi[kRegs]);
-  if (threadIdx.x == 0) *s_go = (kGroups < 2 || (pd->debug & 16)) ? 1 : 0;
+  if (threadIdx.x == 0) *s_go = (kGroups < 2 || (pd->debug & 16)) ? kGroups : 0;
   __syncthreads();
-  if (group == 1)
-    while (*s_go == 0) __nanosleep(256);
-  const int half_phase = nphases / 2;
+  if (group > 0)
+    while (*s_go < group) __nanosleep(256);
   bool first = true;
 
   for (uint64_t tile = (uint64_t)blockIdx.x * kGroups + group; tile < ntiles;
@@ -683,7 +697,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     group_sync(group);
 
     for (int ph = 0; ph < nphases; ++ph) {
-      if (group == 0 && first && ph == half_phase && tid == 0) *s_go = 1;
+      // release group k once group 0 is k / kGroups of the way through its first tile
+      if (group == 0 && first && tid == 0 && ph * kGroups >= (*s_go + 1) * nphases &&
+          *s_go < kGroups - 1)
+        *s_go = *s_go + 1;
       const TilePhase& P = s_ph[ph];
       const int ob = P.op_begin, oe = P.op_end;
       if (P.type != 0) {
@@ -713,10 +730,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       }
     }
     group_sync(group);  // the tile buffer is refilled next iteration
-    if (group == 0 && first && tid == 0) *s_go = 1;
+    if (group == 0 && first && tid == 0) *s_go = kGroups;
     first = false;
   }
-  if (group == 0 && tid == 0) *s_go = 1;  // no tile / no phase: release group 1
+  if (group == 0 && tid == 0) *s_go = kGroups;  // no tile / no phase: release the others
 }
 
 // ======================================================================= host
@@ -839,7 +856,7 @@ std::vector<GateDesc> fuse_1q(int n, const std::vector<GateDesc>& in) {
 bool active_qubits(const GateDesc& g, uint64_t* act) {
   *act = 0;
   if (g.kind == QSV_OP_DENSE) {
-    if (g.m > 5) return false;  // up to 5 targets run as shared-memory phases
+    if (g.m > QSV_TILE_MAX_DENSE) return false;  // wider blocks run as k_dense5 / k_dense_smem
     for (int j = 0; j < g.m; ++j) *act |= 1ULL << g.targets[j];
     return true;
   }
