@@ -65,6 +65,48 @@ struct Scratch {
 static std::map<const qsv_state*, Scratch> g_payload;
 static std::map<const qsv_state*, Scratch> g_results;
 static std::map<const qsv_state*, Scratch> g_analysis;
+static constexpr size_t kPartialBytes = sizeof(double) * 2 * kRedBlocks * kMaxTerms;
+
+// ------------------------------------------------------------ allocator
+// State vectors up to kPoolMaxBytes come from the device's stream-ordered
+// memory pool (cudaMallocAsync / cudaFreeAsync): freed blocks stay cached up
+// to kPoolKeepBytes, so the many short-lived states of copies, channel
+// branches, density-matrix terms and benchmark repeats cost neither a
+// cudaMalloc nor the implicit device synchronisation of cudaFree.  Larger
+// states (the 16-128 GiB shards) use plain cudaMalloc: allocated once, never
+// kept in a cache, and peer-accessible for NVLink copies.  An allocation that
+// fails trims the pool and retries once.
+constexpr size_t kPoolMaxBytes = 1ULL << 30;
+constexpr uint64_t kPoolKeepBytes = 4ULL << 30;
+
+static cudaError_t dev_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
+  if (bytes > kPoolMaxBytes) return cudaMalloc(p, bytes);
+  static std::vector<char> configured(64, 0);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+    cudaGetLastError();
+    return cudaMalloc(p, bytes);
+  }
+  if (device >= 0 && device < 64 && !configured[device]) {
+    uint64_t keep = kPoolKeepBytes;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    configured[device] = 1;
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(p, bytes, s);
+  }
+  return e;
+}
+
+static void dev_free(void* p, size_t bytes, cudaStream_t s) {
+  if (!p) return;
+  if (bytes > kPoolMaxBytes) cudaFree(p);
+  else cudaFreeAsync(p, s);
+}
 
 static int ensure(Scratch& s, size_t bytes, cudaStream_t stream) {
   if (s.cap >= bytes) return QSV_OK;
@@ -235,8 +277,8 @@ int qsv_state_create(int num_qubits, int device, qsv_state** out) {
   st->amps = nullptr;
   st->partials = nullptr;
   st->host_res = nullptr;
-  const size_t bytes = st->dim * sizeof(double2);
-  cudaError_t e = cudaMalloc(&st->amps, std::max<size_t>(bytes, 32));
+  const size_t bytes = std::max<size_t>(st->dim * sizeof(double2), 32);
+  cudaError_t e = dev_alloc(reinterpret_cast<void**>(&st->amps), bytes, device, st->stream);
   if (e != cudaSuccess) {
     delete st;
     set_error("cannot allocate %zu bytes for a %d-qubit state: %s", bytes, num_qubits,
@@ -244,9 +286,9 @@ int qsv_state_create(int num_qubits, int device, qsv_state** out) {
     cudaGetLastError();
     return QSV_ENOMEM;
   }
-  e = cudaMalloc(&st->partials, sizeof(double) * 2 * kRedBlocks * kMaxTerms);
+  e = dev_alloc(reinterpret_cast<void**>(&st->partials), kPartialBytes, device, st->stream);
   if (e != cudaSuccess) {
-    cudaFree(st->amps);
+    dev_free(st->amps, bytes, st->stream);
     delete st;
     return cuda_fail(e, "cudaMalloc(partials)");
   }
@@ -257,9 +299,10 @@ int qsv_state_create(int num_qubits, int device, qsv_state** out) {
 int qsv_state_destroy(qsv_state* st) {
   if (!st) return QSV_OK;
   DeviceGuard dg(st->device);
-  cudaStreamSynchronize(st->stream);
-  cudaFree(st->amps);
-  cudaFree(st->partials);
+  // stream-ordered release: the pool reuses the blocks after the work queued
+  // on this stream (no host synchronisation for pooled blocks)
+  dev_free(st->amps, std::max<size_t>(st->dim * sizeof(double2), 32), st->stream);
+  dev_free(st->partials, kPartialBytes, st->stream);
   for (auto* mp : {&g_payload, &g_results, &g_analysis}) {
     auto it = mp->find(st);
     if (it != mp->end()) {
@@ -285,6 +328,10 @@ int qsv_state_device_ptr(const qsv_state* st, void** out) {
 
 int qsv_set_stream(qsv_state* st, void* stream) {
   if (bad_state(st)) return QSV_EINVAL;
+  // work (and the stream-ordered allocation) queued on the old stream must be
+  // complete before the new stream touches the state
+  DeviceGuard dg(st->device);
+  QSV_TRY(cudaStreamSynchronize(st->stream));
   st->stream = reinterpret_cast<cudaStream_t>(stream);
   return QSV_OK;
 }
