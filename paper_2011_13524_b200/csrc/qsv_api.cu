@@ -79,7 +79,7 @@ static constexpr size_t kPartialBytes = sizeof(double) * 2 * kRedBlocks * kMaxTe
 constexpr size_t kPoolMaxBytes = 1ULL << 30;
 constexpr uint64_t kPoolKeepBytes = 4ULL << 30;
 
-static cudaError_t dev_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
+cudaError_t dev_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
   if (bytes > kPoolMaxBytes) return cudaMalloc(p, bytes);
   static std::vector<char> configured(64, 0);
   cudaMemPool_t pool;
@@ -102,7 +102,7 @@ static cudaError_t dev_alloc(void** p, size_t bytes, int device, cudaStream_t s)
   return e;
 }
 
-static void dev_free(void* p, size_t bytes, cudaStream_t s) {
+void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!p) return;
   if (bytes > kPoolMaxBytes) cudaFree(p);
   else cudaFreeAsync(p, s);

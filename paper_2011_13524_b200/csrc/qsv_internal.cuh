@@ -21,6 +21,9 @@ constexpr int kMaxTerms = 8;          // Pauli terms evaluated per sweep
 constexpr int kMaxFixed = QSV_MAX_TARGETS + QSV_MAX_CONTROLS;
 
 void set_error(const char* fmt, ...);
+// pooled stream-ordered device memory for blocks up to 1 GiB (qsv_api.cu)
+cudaError_t dev_alloc(void** p, size_t bytes, int device, cudaStream_t s);
+void dev_free(void* p, size_t bytes, cudaStream_t s);
 int cuda_fail(cudaError_t e, const char* what);
 
 #define QSV_TRY(call)                                   \

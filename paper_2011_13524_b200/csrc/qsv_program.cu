@@ -28,6 +28,7 @@ struct qsv_program {
   cudaGraph_t graph = nullptr;
   double2* graph_amps = nullptr;
   cudaStream_t graph_stream = nullptr;
+  cudaStream_t last_stream = 0;  // the payload is released in this stream's order
   int device = -1;
 };
 
@@ -175,7 +176,9 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
   }
   p->payload_bytes = host_payload.size();
   if (!host_payload.empty()) {
-    cudaError_t e = cudaMalloc(&p->dev_payload, host_payload.size());
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = dev_alloc(&p->dev_payload, host_payload.size(), dev, 0);
     if (e != cudaSuccess) {
       delete p;
       return cuda_fail(e, "cudaMalloc(program payload)");
@@ -183,7 +186,7 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
     e = cudaMemcpy(p->dev_payload, host_payload.data(), host_payload.size(),
                    cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-      cudaFree(p->dev_payload);
+      dev_free(p->dev_payload, host_payload.size(), 0);
       delete p;
       return cuda_fail(e, "cudaMemcpy(program payload)");
     }
@@ -203,6 +206,7 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
     return QSV_EINVAL;
   }
   DeviceGuard dg(st->device);
+  p->last_stream = st->stream;
   if (!p->opts.use_graph || p->steps.empty()) return launch_steps(p, st->amps, st->stream);
   if (!(p->gexec && p->graph_amps == st->amps && p->graph_stream == st->stream &&
         p->device == st->device)) {
@@ -250,7 +254,8 @@ int qsv_program_stats_get(const qsv_program* p, qsv_program_stats* out) {
 int qsv_program_destroy(qsv_program* p) {
   if (!p) return QSV_OK;
   drop_graph(p);
-  if (p->dev_payload) cudaFree(p->dev_payload);
+  // freed in the order of the stream the program last ran on (pooled block)
+  if (p->dev_payload) dev_free(p->dev_payload, p->payload_bytes, p->last_stream);
   delete p;
   return QSV_OK;
 }
