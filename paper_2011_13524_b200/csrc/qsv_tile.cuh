@@ -120,7 +120,11 @@ struct PlanMix {
   namespace NS {                                                                            \
   int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts& opts,    \
                    std::vector<Step>& steps, std::vector<TilePlan>& tiles,                  \
-                   std::vector<char>& payload, qsv_program_stats* stats, PlanMix* mix);     \
+                   std::vector<char>& payload, qsv_program_stats* stats, PlanMix* mix,      \
+                   bool preprocessed);                                                      \
+  bool tiles_enabled(int n, const qsv_plan_opts& opts);                                     \
+  std::vector<GateDesc> preprocess(int n, const std::vector<GateDesc>& gates,              \
+                                   const qsv_plan_opts& opts);                              \
   int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,   \
                        cudaStream_t s);                                                     \
   }

@@ -1796,14 +1796,29 @@ void add_gate_step(int n, const GateDesc& g, std::vector<Step>& steps, std::vect
 
 }  // namespace
 
-int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_opts& opts,
-                 std::vector<Step>& steps, std::vector<TilePlan>& tiles,
-                 std::vector<char>& payload, qsv_program_stats* stats, PlanMix* mix) {
-  std::vector<GateDesc> gates = opts.fuse ? fuse_1q(n, gates_in) : gates_in;
+bool tiles_enabled(int n, const qsv_plan_opts& opts) {
   int L = opts.tile_qubits > 0 ? opts.tile_qubits : kMaxTileQubits;
   L = std::min(std::min(L, kMaxTileQubits), n);
-  const bool tiles_on = opts.use_tiles && n >= kRegBits + 1 && L >= kRegBits + 1;
-  if (tiles_on && opts.real_frames) gates = realify(n, gates);
+  return opts.use_tiles && n >= kRegBits + 1 && L >= kRegBits + 1;
+}
+
+// host-side gate-list passes shared by both variants: 1-qubit fusion and
+// real frames (the latter only when tile passes run)
+std::vector<GateDesc> preprocess(int n, const std::vector<GateDesc>& gates_in,
+                                 const qsv_plan_opts& opts) {
+  std::vector<GateDesc> gates = opts.fuse ? fuse_1q(n, gates_in) : gates_in;
+  if (tiles_enabled(n, opts) && opts.real_frames) gates = realify(n, gates);
+  return gates;
+}
+
+int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_opts& opts,
+                 std::vector<Step>& steps, std::vector<TilePlan>& tiles,
+                 std::vector<char>& payload, qsv_program_stats* stats, PlanMix* mix,
+                 bool preprocessed) {
+  std::vector<GateDesc> gates = preprocessed ? gates_in : preprocess(n, gates_in, opts);
+  int L = opts.tile_qubits > 0 ? opts.tile_qubits : kMaxTileQubits;
+  L = std::min(std::min(L, kMaxTileQubits), n);
+  const bool tiles_on = tiles_enabled(n, opts);
   if (!tiles_on) {
     for (const GateDesc& g : gates) add_gate_step(n, g, steps, payload, stats);
     return QSV_OK;

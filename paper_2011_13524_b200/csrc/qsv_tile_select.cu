@@ -1,7 +1,6 @@
-// Variant selection for the tile engine (see qsv_tile.cuh): plan with the
-// 32-amplitude kernel (r5) and keep it when the encoded passes are mostly
-// real-rotation batches or 5-target dense blocks; otherwise re-plan for the
-// 16-amplitude kernel (r4).  Measured (profiles/variant_ab.py, time_fused.py):
+// Variant selection for the tile engine (see qsv_tile.cuh): the 32-amplitude
+// kernel (r5) when the preprocessed gate list is mostly real-rotation
+// batches, otherwise the 16-amplitude kernel (r4); one plan per program.  Measured (profiles/variant_ab.py, time_fused.py):
 // cz-ladder r5, cnot-ring / QV / QFT / heavy(2..4) r4, heavy(5) r5 (2x).
 // QSV_TILE_VARIANT=4|5 forces one (A/B experiments).
 #include <cstdlib>
@@ -9,6 +8,34 @@
 #include "qsv_tile.cuh"
 
 namespace qsv {
+
+// Cheap estimate of the encoded op mix from the preprocessed gate list:
+// real-matrix 1-qubit gates (split rotations, X / CNOT) become real register
+// batches, other 1-qubit gates complex ones, 2..4-target dense / X-Y Paulis
+// shared-memory phases.
+static PlanMix estimate_mix(const std::vector<GateDesc>& gates) {
+  PlanMix m;
+  for (const GateDesc& g : gates) {
+    if (g.kind == QSV_OP_DENSE && g.m == 1) {
+      bool real = g.rf != 0;
+      if (!real) {
+        real = true;
+        for (const Cplx& c : g.data) real = real && c.im == 0.0;
+      }
+      if (real) ++m.real_ops;
+      else ++m.complex_ops;
+    } else if (g.kind == QSV_OP_DENSE && g.m >= 2 && g.m <= 4) {
+      ++m.complex_ops;
+    } else if (g.kind == QSV_OP_PAULI || g.kind == QSV_OP_PAULI_ROT) {
+      for (int j = 0; j < g.m; ++j)
+        if (g.ids[j] == 1 || g.ids[j] == 2) {
+          ++m.complex_ops;
+          break;
+        }
+    }
+  }
+  return m;
+}
 
 int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts& opts,
                  std::vector<Step>& steps, std::vector<TilePlan>& tiles,
@@ -19,27 +46,20 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
   }
   int force = 0;
   if (const char* v = getenv("QSV_TILE_VARIANT")) force = atoi(v);
-  if (force != 4) {
-    std::vector<Step> s5;
-    std::vector<TilePlan> t5;
-    std::vector<char> p5;
-    qsv_program_stats st5 = *stats;
-    PlanMix mix;
-    int rc = r5::plan_program(n, gates, opts, s5, t5, p5, &st5, &mix);
-    if (rc) return rc;
-    // r5 for real-rotation batches (fewer phases / flushes) and for 5-target
-    // dense blocks (their 32-amplitude cosets need the larger register file)
+  const bool on4 = r4::tiles_enabled(n, opts), on5 = r5::tiles_enabled(n, opts);
+  if (on4 != on5) force = 4;  // tiny states: only the 16-amplitude kernel tiles them
+  // fusion and real frames once (identical in both variants), then one plan
+  std::vector<GateDesc> pre = r5::preprocess(n, gates, opts);
+  bool use5 = force == 5;
+  if (!force) {
+    const PlanMix mix = estimate_mix(pre);
     const int r5_score = mix.real_ops / 2 + 4 * mix.wide_dense;
-    if (force == 5 || (r5_score > 0 && r5_score >= mix.complex_ops)) {
-      // the caller's vectors start empty, so offsets and indices carry over
-      steps.swap(s5);
-      tiles.swap(t5);
-      payload.swap(p5);
-      *stats = st5;
-      return QSV_OK;
-    }
+    use5 = r5_score > 0 && r5_score >= mix.complex_ops;
   }
-  return r4::plan_program(n, gates, opts, steps, tiles, payload, stats, nullptr);
+  if (force == 4 && on4 != on5)
+    return r4::plan_program(n, gates, opts, steps, tiles, payload, stats, nullptr, false);
+  return use5 ? r5::plan_program(n, pre, opts, steps, tiles, payload, stats, nullptr, true)
+              : r4::plan_program(n, pre, opts, steps, tiles, payload, stats, nullptr, true);
 }
 
 int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,
