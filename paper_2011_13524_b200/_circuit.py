@@ -21,16 +21,66 @@ from ._handles import QuantumGateBase, unwrap
 from ._lib import check, lib
 
 
+_OP_SIZE = C.sizeof(_lib.QsvOp)
+
+
+class _OpsCache:
+    """qsv_op array of one gate list, kept with the arrays it points to;
+    a recompile after ParametricCircuit.set_parameter copies it and patches
+    only the rotation angles."""
+
+    __slots__ = ("ids", "gates", "blob", "rot")
+
+    def __init__(self, gates):
+        self.gates = list(gates)  # keeps the gates (and their cached arrays) alive
+        self.ids = tuple(id(g) for g in gates)
+        self.blob = bytes(_fill_ops_uncached(gates))
+        self.rot = [(i, g) for i, g in enumerate(gates) if isinstance(g, PauliRotationGate)]
+
+    def ops(self):
+        ops = (_lib.QsvOp * max(1, len(self.gates))).from_buffer_copy(self.blob)
+        for i, g in self.rot:
+            ops[i].angle = g.angle
+        return ops
+
+
+def fill_ops(gates, cache_owner=None):
+    """qsv_op array for a gate list (cached on ``cache_owner`` when given)."""
+    if cache_owner is None:
+        return _fill_ops_uncached(gates)
+    c = getattr(cache_owner, "_ops_cache", None)
+    if c is None or c.ids != tuple(id(g) for g in gates):
+        c = _OpsCache(gates)
+        cache_owner._ops_cache = c
+    return c.ops()
+
+
+def _fill_ops_uncached(gates):
+    """qsv_op array for a gate list.  Each gate's op is built once and cached
+    on the gate (with the arrays it points to); only angles are re-read."""
+    ops = (_lib.QsvOp * max(1, len(gates)))()
+    base = C.addressof(ops)
+    for i, g in enumerate(gates):
+        cached = getattr(g, "_op_cache", None)
+        if cached is None:
+            tmp = _lib.QsvOp()
+            keep = []
+            g.fill_op(tmp, keep)
+            cached = (bytes(tmp), keep)
+            g._op_cache = cached
+        C.memmove(base + i * _OP_SIZE, cached[0], _OP_SIZE)
+        if isinstance(g, PauliRotationGate):
+            ops[i].angle = g.angle
+    return ops
+
+
 class _Program:
     """Owner of one native program handle."""
 
     __slots__ = ("h", "stats")
 
-    def __init__(self, n, gates, opts):
-        ops = (_lib.QsvOp * max(1, len(gates)))()
-        keep = []
-        for i, g in enumerate(gates):
-            g.fill_op(ops[i], keep)
+    def __init__(self, n, gates, opts, cache_owner=None):
+        ops = fill_ops(gates, cache_owner)
         h = C.c_void_p()
         check(lib.qsv_program_create(n, ops, len(gates), C.byref(opts), C.byref(h)))
         self.h = h
@@ -68,6 +118,7 @@ class Circuit:
         self.gates: list[QuantumGate] = []
         self._prog = None
         self._prog_key = None
+        self._ops_cache = None
         self._plan = default_plan_opts()
 
     # -- editing -------------------------------------------------------------
@@ -139,7 +190,7 @@ class Circuit:
         key = self._key()
         if self._prog is None or self._prog_key != key:
             if all(isinstance(g, BasicGate) for g in self.gates):
-                self._prog = _Program(self.num_qubits, self.gates, self._plan)
+                self._prog = _Program(self.num_qubits, self.gates, self._plan, self)
             else:
                 steps, run = [], []
                 for g in self.gates:
@@ -172,10 +223,7 @@ class Circuit:
         """Host-only planning statistics (no GPU needed)."""
         opts = default_plan_opts(**kw) if kw else self._plan
         basic = [g for g in self.gates if isinstance(g, BasicGate)]  # maps run on the host
-        ops = (_lib.QsvOp * max(1, len(basic)))()
-        keep = []
-        for i, g in enumerate(basic):
-            g.fill_op(ops[i], keep)
+        ops = fill_ops(basic)
         st = _lib.QsvProgramStats()
         check(lib.qsv_plan_stats(self.num_qubits, ops, len(basic), C.byref(opts),
                                  C.byref(st)))
