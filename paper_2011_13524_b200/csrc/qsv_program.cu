@@ -29,6 +29,7 @@ struct qsv_program {
   double2* graph_amps = nullptr;
   cudaStream_t graph_stream = nullptr;
   cudaStream_t last_stream = 0;  // the payload is released in this stream's order
+  uint64_t runs = 0;
   int device = -1;
 };
 
@@ -207,7 +208,10 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
   }
   DeviceGuard dg(st->device);
   p->last_stream = st->stream;
-  if (!p->opts.use_graph || p->steps.empty()) return launch_steps(p, st->amps, st->stream);
+  // the first run launches directly: a program that runs once (a recompile
+  // after set_parameter) never pays for graph capture + instantiation
+  if (!p->opts.use_graph || p->steps.empty() || p->runs++ == 0)
+    return launch_steps(p, st->amps, st->stream);
   if (!(p->gexec && p->graph_amps == st->amps && p->graph_stream == st->stream &&
         p->device == st->device)) {
     drop_graph(p);
