@@ -10,7 +10,7 @@ namespace qsv {
 std::vector<char> make_payload(const GateDesc& g);
 
 // One step of a program: either a single gate kernel or a tile pass that
-// applies several gates per HBM sweep (qsv_tile.cu).
+// applies several gates per HBM sweep (qsv_tile_impl.cuh).
 struct TilePass;
 
 struct Step {

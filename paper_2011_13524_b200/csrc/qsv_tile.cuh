@@ -1,4 +1,5 @@
-// Tile passes: several gates applied per HBM sweep (see qsv_tile.cu).
+// Tile passes: several gates applied per HBM sweep (implementation in
+// qsv_tile_impl.cuh, compiled as qsv_tile_r4.cu / qsv_tile_r5.cu).
 #pragma once
 
 #include <vector>
