@@ -209,8 +209,11 @@ static bool pack_passes(int n, const std::vector<XTermIn>& terms,
 // land in res[2 * index].  Returns QSV_EUNSUPPORTED when the masks do not
 // fit tiles.  scratch must hold sizeof(XPass) + 2 * grid * kXMaxTerms doubles
 // + 2 * kXMaxTerms doubles.
+constexpr int kXBatch = 32;  // passes launched back to back before one synchronisation
+
 size_t expect_tile_scratch_bytes() {
-  return sizeof(XPass) + sizeof(double) * (2 * (size_t)148 * 2 * kXMaxTerms + 2 * kXMaxTerms) + 256;
+  return ((sizeof(XPass) * kXBatch + 255) / 256) * 256 +
+         sizeof(double) * (2 * (size_t)296 * kXMaxTerms + 2 * kXMaxTerms * kXBatch);
 }
 
 int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
@@ -230,11 +233,35 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
   const uint64_t ntiles = 1ULL << (n - kXTileQubits);
   const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)std::min(num_sms * 2, 296));
   char* base = reinterpret_cast<char*>(scratch);
-  XPass* dpass = reinterpret_cast<XPass*>(base);
-  double* partials = reinterpret_cast<double*>(base + ((sizeof(XPass) + 255) / 256) * 256);
-  double* dout = partials + 2 * (size_t)296 * kXMaxTerms;
+  XPass* dpass0 = reinterpret_cast<XPass*>(base);
+  double* partials = reinterpret_cast<double*>(base + ((sizeof(XPass) * kXBatch + 255) / 256) * 256);
+  double* dout0 = partials + 2 * (size_t)296 * kXMaxTerms;
   res.assign(2 * xms.size(), 0.0);
+  // passes run back to back (stream order protects the shared partials);
+  // results come back with one copy and one synchronisation per batch
+  std::vector<std::vector<int>> orders;
+  std::vector<double> hout;
+  auto drain = [&]() -> int {
+    if (orders.empty()) return QSV_OK;
+    hout.resize(2 * kXMaxTerms * orders.size());
+    QSV_TRY(cudaMemcpyAsync(hout.data(), dout0, hout.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    QSV_TRY(cudaStreamSynchronize(s));
+    for (size_t b = 0; b < orders.size(); ++b)
+      for (size_t k = 0; k < orders[b].size(); ++k) {
+        res[2 * terms[orders[b][k]].index] = hout[2 * kXMaxTerms * b + 2 * k];
+        res[2 * terms[orders[b][k]].index + 1] = hout[2 * kXMaxTerms * b + 2 * k + 1];
+      }
+    orders.clear();
+    return QSV_OK;
+  };
   for (auto& ps : passes) {
+    if ((int)orders.size() == kXBatch) {
+      const int rc = drain();
+      if (rc) return rc;
+    }
+    XPass* dpass = dpass0 + orders.size();
+    double* dout = dout0 + 2 * kXMaxTerms * orders.size();
     XPass P;
     memset(&P, 0, sizeof(P));
     const uint64_t S = ps.first;
@@ -300,15 +327,9 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
     QSV_CHECK_LAUNCH("k_expect_tile");
     k_expect_tile_final<<<P.nterms, kXThreads, 0, s>>>(partials, (int)grid, dout);
     QSV_CHECK_LAUNCH("k_expect_tile_final");
-    std::vector<double> h(2 * P.nterms);
-    QSV_TRY(cudaMemcpyAsync(h.data(), dout, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    QSV_TRY(cudaStreamSynchronize(s));  // dpass / partials are reused by the next pass
-    for (size_t k = 0; k < order.size(); ++k) {
-      res[2 * terms[order[k]].index] = h[2 * k];
-      res[2 * terms[order[k]].index + 1] = h[2 * k + 1];
-    }
+    orders.push_back(order);
   }
-  return QSV_OK;
+  return drain();
 }
 
 }  // namespace qsv

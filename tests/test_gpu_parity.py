@@ -447,3 +447,24 @@ def test_core_style_usage():
     assert abs(abs(a[3 * bit]) - 1.0) <= 1e-14
     st.amplitudes = np.eye(8, dtype=np.complex128)[5]
     assert st.get_vector()[5] == 1.0
+
+
+def test_many_term_observable_tile_batches():
+    """150 random Pauli strings on 16 qubits: dozens of tile passes (more
+    than one launch batch) in the tile expectation path, vs the oracle."""
+    n = 16
+    rng = np.random.default_rng(21)
+    obs = qs.Observable(n)
+    terms = []
+    for _ in range(150):
+        k = int(rng.integers(1, 6))
+        qsel = [int(q) for q in rng.choice(n, size=k, replace=False)]
+        axes = [int(a) for a in rng.integers(1, 4, size=k)]
+        coef = float(rng.normal())
+        obs.add_operator(coef, " ".join(f"{'XYZ'[a - 1]} {q}" for q, a in zip(qsel, axes)))
+        terms.append((coef, tuple(zip(qsel, axes))))
+    st = haar(n, 4)
+    got = obs.get_expectation_value(st)
+    a = orc.haar_state(n, 4)
+    ref = orc.expectation(a, a, n, terms).real
+    assert close_expect(got, ref, sum(abs(c) for c, _ in terms)), (got, ref)
