@@ -578,8 +578,10 @@ class ShardedQuantumState:
         import torch
         dist = self.dist
         for part in self._chunks(view):
-            send = part.contiguous() if not part.is_contiguous() else part.clone()
-            recv = torch.empty_like(send)
+            # a contiguous slice is sent in place (only the received data is
+            # staged); a strided one is packed first
+            send = part if part.is_contiguous() else part.contiguous()
+            recv = torch.empty(send.shape, dtype=send.dtype, device=send.device)
             ops = [dist.P2POp(dist.isend, send, partner, group=self.group),
                    dist.P2POp(dist.irecv, recv, partner, group=self.group)]
             for w in dist.batch_isend_irecv(ops):
