@@ -315,14 +315,8 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
     for (int b = 0; b < kXTileQubits; ++b) pos[b] = P.spos[b];
     FixedBits tb = make_fixed(pos, kXTileQubits, 0);
     const size_t smem = sizeof(double2) << kXTileQubits;
-    static int attr_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (attr_dev != dev) {
-      QSV_TRY(cudaFuncSetAttribute(k_expect_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      attr_dev = dev;
-    }
+    static uint64_t attr_done = 0;
+    QSV_TRY(ensure_smem_attr(k_expect_tile, (int)smem, attr_done));
     k_expect_tile<<<grid, kXThreads, smem, s>>>(a, dpass, tb, ntiles, partials);
     QSV_CHECK_LAUNCH("k_expect_tile");
     k_expect_tile_final<<<P.nterms, kXThreads, 0, s>>>(partials, (int)grid, dout);

@@ -728,11 +728,8 @@ int launch_gate(double2* a, int n, const GateDesc& g0, const Cplx* dev_data, cud
     const uint64_t ncos = dim >> (g.nc + g.m);
     const int per_block = std::max(1, kThreads / D);
     const size_t smem = sizeof(double2) * (size_t)per_block * D;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_sparse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set = true;
-    }
+    static uint64_t attr_done = 0;
+    QSV_TRY(ensure_smem_attr(k_sparse_smem, 200 * 1024, attr_done));
     uint64_t nblk = (ncos + per_block - 1) / per_block;
     nblk = std::max<uint64_t>(1, std::min<uint64_t>(nblk, 148ULL * 64));
     k_sparse_smem<<<(unsigned)nblk, kThreads, smem, s>>>(a, fb2, g.m, vals, offs, rptr, cols, ncos);
@@ -872,11 +869,8 @@ int launch_gate(double2* a, int n, const GateDesc& g0, const Cplx* dev_data, cud
   const int per_block = std::max(1, kThreads / D);
   const size_t smem = sizeof(double2) * (size_t)per_block * D;
   if (smem > 48 * 1024) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_dense_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set = true;
-    }
+    static uint64_t attr_done = 0;
+    QSV_TRY(ensure_smem_attr(k_dense_smem, 200 * 1024, attr_done));
   }
   uint64_t nblk = (ncos + per_block - 1) / per_block;
   nblk = std::min<uint64_t>(nblk, 148ULL * 64);

@@ -111,6 +111,18 @@ __device__ __forceinline__ void st1(double2* p, double2 v) {
                : "memory");
 }
 
+// cudaFuncSetAttribute acts on the current device: remember per device
+// (bit d of done_mask) whether the dynamic shared-memory limit is raised.
+template <typename F>
+inline cudaError_t ensure_smem_attr(F* func, int bytes, uint64_t& done_mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && ((done_mask >> dev) & 1ULL)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && dev < 64) done_mask |= 1ULL << dev;
+  return e;
+}
+
 inline unsigned grid_for(uint64_t units, int per_thread) {
   uint64_t per_block = (uint64_t)kThreads * per_thread;
   uint64_t b = (units + per_block - 1) / per_block;
