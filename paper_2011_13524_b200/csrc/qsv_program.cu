@@ -21,6 +21,8 @@ struct qsv_program {
   std::vector<TilePlan> tiles;
   void* dev_payload = nullptr;
   size_t payload_bytes = 0;
+  int payload_device = -1;       // device holding dev_payload
+  std::vector<char> host_payload;  // re-uploaded when a state on another device runs it
   qsv_program_stats stats;
   qsv_plan_opts opts;
   // CUDA graph cache (valid for one amps pointer / stream / device)
@@ -48,6 +50,26 @@ int launch_steps(qsv_program* p, double2* amps, cudaStream_t s) {
     }
     if (rc) return rc;
   }
+  return QSV_OK;
+}
+
+// payload on `dev` (programs are built on the current device; a state on
+// another device triggers a re-upload there)
+int upload_payload(qsv_program* p, int dev) {
+  if (p->host_payload.empty() || p->payload_device == dev) return QSV_OK;
+  if (p->dev_payload) {
+    DeviceGuard old(p->payload_device);
+    dev_free(p->dev_payload, p->payload_bytes, p->last_stream);
+    p->dev_payload = nullptr;
+  }
+  DeviceGuard dg(dev);
+  cudaError_t e = dev_alloc(&p->dev_payload, p->payload_bytes, dev, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(program payload)");
+  e = cudaMemcpy(p->dev_payload, p->host_payload.data(), p->payload_bytes,
+                 cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(program payload)");
+  p->payload_device = dev;
+  p->last_stream = 0;
   return QSV_OK;
 }
 
@@ -169,30 +191,20 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
   memset(&p->stats, 0, sizeof(p->stats));
   p->stats.num_ops_in = nops;
 
-  std::vector<char> host_payload;
-  int rc = plan_program(n, gates, o, p->steps, p->tiles, host_payload, &p->stats);
+  int rc = plan_program(n, gates, o, p->steps, p->tiles, p->host_payload, &p->stats);
   if (rc) {
     delete p;
     return rc;
   }
-  p->payload_bytes = host_payload.size();
-  if (!host_payload.empty()) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaError_t e = dev_alloc(&p->dev_payload, host_payload.size(), dev, 0);
-    if (e != cudaSuccess) {
-      delete p;
-      return cuda_fail(e, "cudaMalloc(program payload)");
-    }
-    e = cudaMemcpy(p->dev_payload, host_payload.data(), host_payload.size(),
-                   cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      dev_free(p->dev_payload, host_payload.size(), 0);
-      delete p;
-      return cuda_fail(e, "cudaMemcpy(program payload)");
-    }
+  p->payload_bytes = p->host_payload.size();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  rc = upload_payload(p, dev);
+  if (rc) {
+    delete p;
+    return rc;
   }
-  cudaGetDevice(&p->device);
+  p->device = dev;
   *out = p;
   return QSV_OK;
 }
@@ -207,6 +219,11 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
     return QSV_EINVAL;
   }
   DeviceGuard dg(st->device);
+  if (p->payload_device != st->device && !p->host_payload.empty()) {
+    drop_graph(p);
+    const int rc = upload_payload(p, st->device);
+    if (rc) return rc;
+  }
   p->last_stream = st->stream;
   // the first run launches directly: a program that runs once (a recompile
   // after set_parameter) never pays for graph capture + instantiation
@@ -259,7 +276,10 @@ int qsv_program_destroy(qsv_program* p) {
   if (!p) return QSV_OK;
   drop_graph(p);
   // freed in the order of the stream the program last ran on (pooled block)
-  if (p->dev_payload) dev_free(p->dev_payload, p->payload_bytes, p->last_stream);
+  if (p->dev_payload) {
+    DeviceGuard dg(p->payload_device);
+    dev_free(p->dev_payload, p->payload_bytes, p->last_stream);
+  }
   delete p;
   return QSV_OK;
 }
