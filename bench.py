@@ -536,6 +536,25 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
             tb = min(tb, a.elapsed_time(b) / 1e3)
         curve[str(m)] = tb / (depth + 1)
         del s2
+    # beyond n = 30 on one GPU while the state fits in HBM (n = 33: 128 GiB)
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    for m in (32, 33):
+        if (16 << m) > free_b - (4 << 30):
+            break
+        c = workloads.generate_cz_ladder(m, depth, seed=1)
+        s2 = qs.QuantumState(m, device=dev)
+        s2.set_stream(stream.cuda_stream)
+        s2.set_random_state_device(7)
+        c.update_quantum_state(s2)  # plan + first run
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        c.update_quantum_state(s2)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        curve[str(m)] = a.elapsed_time(b) / 1e3 / (depth + 1)
+        del s2
+        free_b, _ = torch.cuda.mem_get_info(dev)
     out["sec_per_layer_vs_qubits"] = curve
     # the same circuit after the reference's own heavy(5) fusion
     # (QuantumCircuitOptimizer().optimize(c, 5), optimizer.py:73-107): 5-qubit
