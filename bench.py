@@ -452,6 +452,39 @@ def run_sharded(args, rank, world, local_rank):
         elapsed_ms = float(t.item())
     value = bytes_step * args.steps / (elapsed_ms / 1e3) / 1e9
     stats = dict(st.stats)
+    launches = len(seq) * args.steps  # one gate kernel per record and rank (use_tiles=0)
+
+    # e2e: the same sweep with each rank's shard loaded from pinned host memory
+    # and read back every step (host <-> device copies inside the timed region)
+    e2e = None
+    shard = next(iter(st.shards.values()))
+    host = torch.empty(2 << st.L, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    shard.state.get_vector(out=host)
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        shard.state.load(host)
+        sweep()
+        shard.state.get_vector(out=host)
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    if dist.is_initialized():
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": bytes_step * args.e2e_steps / e2e_s / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": 16 << st.L, "d2h_bytes_per_step": 16 << st.L,
+           "steps": args.e2e_steps, "note": "per rank; max over ranks of wall time"}
+    del host
+    del st, shard
+
+    circuit = None
+    try:
+        circuit = run_sharded_circuit(args, rank, world, dev, stream)
+    except Exception as exc:  # reported, never fatal for the headline line
+        circuit = {"error": f"{type(exc).__name__}: {exc}"}
     if rank != 0:
         return
     peak, peak_kind = measured_peaks()
@@ -472,11 +505,60 @@ def run_sharded(args, rank, world, local_rank):
                      "note": "per-GPU algorithmic HBM bytes / time; swaps add NVLink bytes"},
         "swaps": stats, "wall_s": wall,
         "cpu_baseline": None,
-        "e2e": None,
-        "gpu_launches": None,
+        "e2e": e2e,
+        "gpu_launches": launches,
         "clocks": clk.summary(),
+        "sharded_random_circuit": circuit,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_sharded_circuit(args, rank, world, dev, stream):
+    """cfg5 shape: cz-ladder(L + log2 P, depth 20) sharded over the ranks with
+    multi-qubit remaps over NVLink; device time, max over ranks.  On one GPU
+    (--sharded) it runs 4 virtual ranks (remaps become device copies)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2011_13524_b200 import workloads
+    from paper_2011_13524_b200._circuit import circuit_records
+    from paper_2011_13524_b200.dist import ShardedQuantumState, plan_exchange_bytes
+
+    virtual = world == 1
+    vworld = 4 if virtual else world
+    p = int(round(math.log2(vworld)))
+    L = args.shard_circuit_qubits if not virtual else min(args.shard_circuit_qubits, 26)
+    n = L + p
+    depth = 20
+    recs = circuit_records(workloads.generate_cz_ladder(n, depth, seed=1))
+    kw = dict(world=vworld, owned=list(range(vworld))) if virtual else {}
+    st = ShardedQuantumState(n, **kw)
+    for r, s in st.shards.items():
+        s.set_random(97 + r)          # each shard normalised to 1 ...
+        s.scale(1.0 / math.sqrt(vworld))  # ... so the whole state has norm 1
+    model = plan_exchange_bytes(n, vworld, recs)
+    st.apply_records(recs)  # warm-up: programs compiled per segment
+    torch.cuda.synchronize(dev)
+    if dist.is_initialized():
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    st.apply_records(recs)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b)
+    if dist.is_initialized():
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    norm = st.get_squared_norm()
+    del st
+    return {"metric": "random-circuit sec/layer (sharded)", "unit": "s/layer",
+            "value": ms / 1e3 / (depth + 1), "higher_is_better": False,
+            "workload": f"cz-ladder n={n} depth={depth} seed=1 over {vworld} "
+                        f"{'virtual ranks on one GPU' if virtual else 'GPUs'} "
+                        f"(2^{L} amplitudes per rank)",
+            "circuit_s": ms / 1e3, "norm_after": norm, "exchange_model": model,
+            "nvlink_roofline_s": model["bytes_sent_per_rank"] / 900e9}
 
 
 def run_random_circuit(args, dev, stream, qs, workloads, torch):
@@ -665,6 +747,8 @@ def main():
     ap.add_argument("--ref-gates-per-step", type=int, default=1)
     ap.add_argument("--skip-circuit", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--shard-circuit-qubits", type=int, default=30,
+                    help="local qubits per rank of the sharded random circuit extra")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded engine even on one GPU (tests the N>1 path)")
     args = ap.parse_args()
