@@ -334,10 +334,22 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        e2e = {"value": bytes_step * e2e_steps * world / e2e_s / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": 16 << n, "d2h_bytes_per_step": 16 << n,
-               "steps": e2e_steps}
+        serial = {"value": bytes_step * e2e_steps * world / e2e_s / 1e9, "unit": "GB/s",
+                  "h2d_bytes_per_step": 16 << n, "d2h_bytes_per_step": 16 << n,
+                  "steps": e2e_steps, "note": "one state: load, gates, read back in sequence"}
         del host, hv
+        # pipelined: three states on three streams; step i runs on state i % 3
+        # with its pinned input / output buffers, so one step's host <-> device
+        # copies (PCIe is full duplex) overlap the other steps' gates
+        pipe = None
+        try:
+            pipe = e2e_pipelined(qs, gates, n, dev, torch, bytes_step, world,
+                                 max(3, 2 * e2e_steps), barrier, dist)
+        except Exception as exc:  # noqa: BLE001  (reported, never fatal)
+            serial["pipelined_error"] = f"{type(exc).__name__}: {exc}"
+        e2e = pipe if pipe is not None else serial
+        if pipe is not None:
+            e2e["serial"] = serial
 
     extra = {}
     if rank == 0 and not args.skip_circuit:
@@ -559,6 +571,50 @@ def run_sharded_circuit(args, rank, world, dev, stream):
                         f"(2^{L} amplitudes per rank)",
             "circuit_s": ms / 1e3, "norm_after": norm, "exchange_model": model,
             "nvlink_roofline_s": model["bytes_sent_per_rank"] / 900e9}
+
+
+def e2e_pipelined(qs, gates, n, dev, torch, bytes_step, world, steps, barrier, dist, depth=3):
+    states, bufs = [], []
+    for k in range(depth):
+        s = qs.QuantumState(n, device=dev)
+        s.set_stream(torch.cuda.Stream(dev).cuda_stream)
+        s.set_random_state_device(123 + k)
+        states.append(s)
+        hin = torch.empty(2 << n, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
+        hout = torch.empty(2 << n, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
+        s.get_vector(out=hin)
+        bufs.append((hin, hout))
+
+    def step(i):
+        s = states[i % depth]
+        hin, hout = bufs[i % depth]
+        s.synchronize()  # step i - depth on this state is done: its buffers are free
+        s.load(hin)      # pinned -> asynchronous H2D on the state's stream
+        for _, _, g in gates:
+            g.update_quantum_state(s)
+        s.get_vector(out=hout, blocking=False)
+
+    for i in range(depth):  # warm-up
+        step(i)
+    for s in states:
+        s.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        step(i)
+    for s in states:
+        s.synchronize()
+    sec = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([sec], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    del states, bufs
+    return {"value": bytes_step * steps * world / sec / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": 16 << n, "d2h_bytes_per_step": 16 << n, "steps": steps,
+            "note": f"public API, {depth} states on {depth} streams: each step = H2D of its "
+                    "input state from pinned memory, the 140-gate sweep, D2H of the result; "
+                    "one step's copies overlap the other steps' gates"}
 
 
 def run_random_circuit(args, dev, stream, qs, workloads, torch):

@@ -78,6 +78,10 @@ int qsv_set_zero(qsv_state* st);
 int qsv_set_basis(qsv_state* st, uint64_t index);
 int qsv_load(qsv_state* st, const double* interleaved, uint64_t n_amps);
 int qsv_get(const qsv_state* st, double* interleaved_out, uint64_t n_amps);
+/* qsv_get_async: enqueue the device->host copy on the state's stream and
+ * return; the caller synchronises (qsv_sync) before reading `out`, which
+ * should be pinned for the copy to overlap other work. */
+int qsv_get_async(const qsv_state* st, double* interleaved_out, uint64_t n_amps);
 int qsv_load_range(qsv_state* st, const double* interleaved, uint64_t offset, uint64_t count);
 int qsv_get_range(const qsv_state* st, double* interleaved_out, uint64_t offset, uint64_t count);
 int qsv_copy(const qsv_state* src, qsv_state* dst);

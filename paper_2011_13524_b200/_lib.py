@@ -97,6 +97,7 @@ _SIGS = {
     "qsv_set_basis": ([_P, _U64], _I),
     "qsv_load": ([_P, _DP, _U64], _I),
     "qsv_get": ([_P, _DP, _U64], _I),
+    "qsv_get_async": ([_P, _DP, _U64], _I),
     "qsv_load_range": ([_P, _DP, _U64, _U64], _I),
     "qsv_get_range": ([_P, _DP, _U64, _U64], _I),
     "qsv_copy": ([_P, _P], _I),

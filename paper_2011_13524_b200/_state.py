@@ -107,15 +107,19 @@ class StateVector:
             raise ValueError(f"expected {self.dim} amplitudes, got shape {data.shape}")
         self._upload(data)
 
-    def get_vector(self, out: np.ndarray | None = None) -> np.ndarray:
+    def get_vector(self, out: np.ndarray | None = None, blocking: bool = True) -> np.ndarray:
         """A host copy (mutating it never touches the device state).  ``out``
-        may supply a contiguous complex128 buffer, e.g. pinned memory."""
+        may supply a contiguous complex128 buffer, e.g. pinned memory; with
+        ``blocking=False`` the copy is only enqueued on the state's stream
+        (read ``out`` after ``synchronize()``)."""
         if out is None:
+            if not blocking:
+                raise ValueError("a non-blocking copy needs an output buffer")
             out = np.empty(self.dim, dtype=np.complex128)
         elif out.dtype != np.complex128 or out.shape != (self.dim,) or \
                 not out.flags.c_contiguous:
             raise ValueError(f"out must be a contiguous complex128 array of {self.dim}")
-        check(lib.qsv_get(self._h, out.ctypes.data, out.size))
+        check((lib.qsv_get if blocking else lib.qsv_get_async)(self._h, out.ctypes.data, out.size))
         return out
 
     def copy(self) -> "StateVector":

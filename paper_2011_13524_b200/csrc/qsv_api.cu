@@ -423,6 +423,19 @@ int qsv_get(const qsv_state* st, double* dst, uint64_t n_amps) {
   return qsv_get_range(st, dst, 0, n_amps);
 }
 
+int qsv_get_async(const qsv_state* st, double* dst, uint64_t n_amps) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (n_amps != st->dim) {
+    set_error("expected a buffer of %llu amplitudes, got %llu", (unsigned long long)st->dim,
+              (unsigned long long)n_amps);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(st->device);
+  QSV_TRY(cudaMemcpyAsync(dst, st->amps, st->dim * sizeof(double2), cudaMemcpyDeviceToHost,
+                          st->stream));
+  return QSV_OK;
+}
+
 int qsv_copy(const qsv_state* src, qsv_state* dst) {
   if (bad_state(src) || bad_state(dst)) return QSV_EINVAL;
   if (src->n != dst->n) {
