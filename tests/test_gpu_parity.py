@@ -468,3 +468,19 @@ def test_many_term_observable_tile_batches():
     a = orc.haar_state(n, 4)
     ref = orc.expectation(a, a, n, terms).real
     assert close_expect(got, ref, sum(abs(c) for c, _ in terms)), (got, ref)
+
+
+def test_async_readback_on_own_stream():
+    """get_vector(blocking=False) enqueues the copy on the state's stream;
+    after synchronize() the buffer equals a blocking read."""
+    import torch
+    st = haar(18, 3)
+    s = torch.cuda.Stream()
+    st.set_stream(s.cuda_stream)
+    qg.H(17).update_quantum_state(st)
+    out = torch.empty(2 << 18, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
+    st.get_vector(out=out, blocking=False)
+    st.synchronize()
+    assert np.array_equal(out, st.get_vector())
+    with pytest.raises(ValueError):
+        st.get_vector(blocking=False)
