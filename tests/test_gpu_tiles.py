@@ -204,3 +204,36 @@ def test_qft_controlled_phases_merge(n, L):
     ref = orc.haar_state(n, n)
     c_oracle.run_records(ref, n, circuit_records(circ))
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+
+
+def test_planner_fuzz():
+    """Random circuits (every gate kind, random widths) under random plan
+    options and forced kernel variants, against the C oracle."""
+    import os
+    rng = np.random.default_rng(2024)
+    for case in range(int(os.environ.get("QSV_FUZZ_CASES", "40"))):
+        n = int(rng.integers(6, 19))
+        L = int(rng.integers(6, 13))
+        ng = int(rng.integers(20, 200))
+        seed = int(rng.integers(1 << 30))
+        circ = random_circuit(n, ng, seed, max_k=int(rng.integers(2, 5))) if case % 2 \
+            else layered_circuit(n, int(rng.integers(2, 8)), seed)
+        opts = dict(tile_qubits=L, real_frames=int(rng.integers(2)), fuse=int(rng.integers(2)),
+                    use_graph=int(rng.integers(2)))
+        variant = ("", "4", "5")[int(rng.integers(3))]
+        if variant:
+            os.environ["QSV_TILE_VARIANT"] = variant
+        try:
+            circ.set_plan_options(**opts)
+            st = qs.QuantumState(n)
+            st.set_Haar_random_state(seed % 1000)
+            circ.update_quantum_state(st)
+            circ.update_quantum_state(st)  # second run: CUDA graph replay
+        finally:
+            os.environ.pop("QSV_TILE_VARIANT", None)
+        ref = orc.haar_state(n, seed % 1000)
+        recs = circuit_records(circ)
+        c_oracle.run_records(ref, n, recs)
+        c_oracle.run_records(ref, n, recs)
+        err = np.max(np.abs(st.get_vector() - ref))
+        assert err <= 1e-12, (case, n, L, ng, opts, variant, err)
