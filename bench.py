@@ -419,7 +419,8 @@ def sweep_records(n):
 def run_sharded(args, rank, world, local_rank):
     """N GPUs: the sweep on n = qubits + log2(N) qubits sharded over the
     ranks by the top qubits (weak scaling: 2^qubits amplitudes per GPU);
-    gates on global qubits trigger NVLink swaps (NCCL send/recv)."""
+    gates on global qubits trigger NVLink swaps (qsv_slice_swap on the
+    peers' IPC-mapped shards; NCCL only for the barriers)."""
     import torch
     import torch.distributed as dist
     from paper_2011_13524_b200.dist import ShardedQuantumState
@@ -490,6 +491,7 @@ def run_sharded(args, rank, world, local_rank):
            "h2d_bytes_per_step": 16 << st.L, "d2h_bytes_per_step": 16 << st.L,
            "steps": args.e2e_steps, "note": "per rank; max over ranks of wall time"}
     del host
+    st.close()
     del st, shard
 
     circuit = None
@@ -563,8 +565,10 @@ def run_sharded_circuit(args, rank, world, dev, stream):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     norm = st.get_squared_norm()
+    mode = st.exchange
+    st.close()
     del st
-    return {"metric": "random-circuit sec/layer (sharded)", "unit": "s/layer",
+    return {"metric": "random-circuit sec/layer (sharded)", "exchange": mode, "unit": "s/layer",
             "value": ms / 1e3 / (depth + 1), "higher_is_better": False,
             "workload": f"cz-ladder n={n} depth={depth} seed=1 over {vworld} "
                         f"{'virtual ranks on one GPU' if virtual else 'GPUs'} "

@@ -232,6 +232,28 @@ int qsv_program_destroy(qsv_program* prog);
 int qsv_plan_stats(int num_qubits, const qsv_op* ops, int nops, const qsv_plan_opts* opts,
                    qsv_program_stats* out);
 
+/* --------------------------------------------------------------- sharding
+ * Exchange primitives of the sharded engine (dist.py; no reference
+ * counterpart -- the reference is single-process).  A shard that
+ * takes part in peer exchanges is allocated with qsv_state_create_shared
+ * (plain cudaMalloc, so its buffer can be exported with CUDA IPC); a peer
+ * process maps it with qsv_ipc_open and passes the mapped pointer to
+ * qsv_slice_swap, which exchanges the slice {x : bits ls of x == d_mine} of
+ * the local shard with the slice {x : bits ls == d_peer} of the peer buffer
+ * in place, one kernel over NVLink (loads and stores to peer memory; no
+ * staging buffers, no pack/unpack).  Only slice elements j0 <= j < j1 (in
+ * slice order) are touched, so the two owners of a pair can each swap half.
+ * The caller orders it against the peer's own work (a barrier before and
+ * after an exchange step).  QSV_IPC_HANDLE_BYTES bytes per handle. */
+#define QSV_IPC_HANDLE_BYTES 64
+#define QSV_MAX_SLICE_BITS 16
+int qsv_state_create_shared(int num_qubits, int device, qsv_state** out);
+int qsv_ipc_export(const qsv_state* st, void* handle_out);
+int qsv_ipc_open(const void* handle, int device, void** peer_amps);
+int qsv_ipc_close(int device, void* peer_amps);
+int qsv_slice_swap(qsv_state* st, void* peer_amps, const int* ls, int k, uint64_t d_mine,
+                   uint64_t d_peer, uint64_t j0, uint64_t j1);
+
 #ifdef __cplusplus
 }
 #endif

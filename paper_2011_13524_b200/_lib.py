@@ -87,6 +87,11 @@ _SIGS = {
     "qsv_device_count": ([_IP], _I),
     "qsv_device_info": ([_I, C.c_char_p, _I, _IP, C.POINTER(_U64)], _I),
     "qsv_state_create": ([_I, _I, C.POINTER(_P)], _I),
+    "qsv_state_create_shared": ([_I, _I, C.POINTER(_P)], _I),
+    "qsv_ipc_export": ([_P, _P], _I),
+    "qsv_ipc_open": ([_P, _I, C.POINTER(_P)], _I),
+    "qsv_ipc_close": ([_I, _P], _I),
+    "qsv_slice_swap": ([_P, _P, _IP, _I, _U64, _U64, _U64, _U64], _I),
     "qsv_state_destroy": ([_P], _I),
     "qsv_state_num_qubits": ([_P, _IP], _I),
     "qsv_state_device_ptr": ([_P, C.POINTER(_P)], _I),

@@ -29,14 +29,15 @@ class StateVector:
 
     __slots__ = ("_h", "_n", "_device", "_cregs", "__weakref__")
 
-    def __init__(self, qubit_count: int, device: int = 0):
+    def __init__(self, qubit_count: int, device: int = 0, shared: bool = False):
         n = _check_count(qubit_count)
         self._h = None
         self._n = n
         self._device = int(device)
         self._cregs: list[int] = []
         h = C.c_void_p()
-        check(lib.qsv_state_create(n, self._device, C.byref(h)))
+        create = lib.qsv_state_create_shared if shared else lib.qsv_state_create
+        check(create(n, self._device, C.byref(h)))
         self._h = h
 
     def __del__(self):

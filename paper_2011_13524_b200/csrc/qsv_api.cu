@@ -252,7 +252,7 @@ int qsv_device_info(int device, char* name, int name_len, int* sm_count, uint64_
   return QSV_OK;
 }
 
-int qsv_state_create(int num_qubits, int device, qsv_state** out) {
+static int state_create(int num_qubits, int device, bool plain, qsv_state** out) {
   if (!out) {
     set_error("null output pointer");
     return QSV_EINVAL;
@@ -277,8 +277,10 @@ int qsv_state_create(int num_qubits, int device, qsv_state** out) {
   st->amps = nullptr;
   st->partials = nullptr;
   st->host_res = nullptr;
+  st->plain = plain ? 1 : 0;
   const size_t bytes = std::max<size_t>(st->dim * sizeof(double2), 32);
-  cudaError_t e = dev_alloc(reinterpret_cast<void**>(&st->amps), bytes, device, st->stream);
+  cudaError_t e = plain ? cudaMalloc(reinterpret_cast<void**>(&st->amps), bytes)
+                        : dev_alloc(reinterpret_cast<void**>(&st->amps), bytes, device, st->stream);
   if (e != cudaSuccess) {
     delete st;
     set_error("cannot allocate %zu bytes for a %d-qubit state: %s", bytes, num_qubits,
@@ -288,7 +290,8 @@ int qsv_state_create(int num_qubits, int device, qsv_state** out) {
   }
   e = dev_alloc(reinterpret_cast<void**>(&st->partials), kPartialBytes, device, st->stream);
   if (e != cudaSuccess) {
-    dev_free(st->amps, bytes, st->stream);
+    if (plain) cudaFree(st->amps);
+    else dev_free(st->amps, bytes, st->stream);
     delete st;
     return cuda_fail(e, "cudaMalloc(partials)");
   }
@@ -296,12 +299,25 @@ int qsv_state_create(int num_qubits, int device, qsv_state** out) {
   return qsv_set_zero(st);
 }
 
+int qsv_state_create(int num_qubits, int device, qsv_state** out) {
+  return state_create(num_qubits, device, false, out);
+}
+
+int qsv_state_create_shared(int num_qubits, int device, qsv_state** out) {
+  return state_create(num_qubits, device, true, out);
+}
+
 int qsv_state_destroy(qsv_state* st) {
   if (!st) return QSV_OK;
   DeviceGuard dg(st->device);
   // stream-ordered release: the pool reuses the blocks after the work queued
   // on this stream (no host synchronisation for pooled blocks)
-  dev_free(st->amps, std::max<size_t>(st->dim * sizeof(double2), 32), st->stream);
+  if (st->plain) {
+    cudaStreamSynchronize(st->stream);
+    cudaFree(st->amps);
+  } else {
+    dev_free(st->amps, std::max<size_t>(st->dim * sizeof(double2), 32), st->stream);
+  }
   dev_free(st->partials, kPartialBytes, st->stream);
   for (auto* mp : {&g_payload, &g_results, &g_analysis}) {
     auto it = mp->find(st);

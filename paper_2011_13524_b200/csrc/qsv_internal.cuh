@@ -154,6 +154,7 @@ struct qsv_state {
   cudaStream_t stream;
   double* partials;   // device reduction scratch
   double* host_res;   // pinned result slots
+  int plain;          // amps from cudaMalloc (IPC-exportable shard), not the pool
 };
 
 // ----------------------------------------------------------------------

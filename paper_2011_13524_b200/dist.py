@@ -12,11 +12,18 @@ map is kept on the host and is never undone eagerly.
   gates are compiled per rank into one libqsv program (fused + tiled).
 * A non-diagonal target on a global qubit triggers a global<->local swap:
   rank r and its partner r ^ 2^(g-L) exchange the half of their shard whose
-  local bit l differs from r's bit g (16 * 2^(L-1) bytes each way), in chunks
-  through a staging buffer with NCCL send/recv over NVLink
-  (torch.distributed).  The victim local qubit is the one whose next
-  non-diagonal use is furthest away (Belady), preferring high positions so
-  the exchanged half is contiguous.
+  local bit l differs from r's bit g (16 * 2^(L-1) bytes each way).  The
+  victim local qubit is the one whose next non-diagonal use is furthest away
+  (Belady), preferring high positions so the exchanged half is contiguous.
+  Two exchange paths (``exchange=``):
+  - "p2p" (default when every shard is a CudaShard and all GPUs can reach
+    each other): the shards are mapped into each other's address space (CUDA
+    IPC across processes) and each pair trades its slices in place with one
+    libqsv kernel over NVLink (qsv_slice_swap: loads and stores to peer
+    memory, each owner swapping half the slice), bracketed by a device-side
+    barrier (a one-element NCCL all_reduce on the shard stream);
+  - "nccl": chunked send/recv through staging buffers (torch.distributed
+    batch_isend_irecv; gloo in the CPU tests).
 * Reductions (norm, expectation) are local partial sums + all_reduce.
 
 The engine is SPMD over the shards a process owns: normally one (its rank),
@@ -185,10 +192,10 @@ def records_to_ops(records):
 class CudaShard:
     """A shard held by libqsv on one GPU (the product backend)."""
 
-    def __init__(self, L, device=0, stream_ptr=None, **plan):
+    def __init__(self, L, device=0, stream_ptr=None, shared=False, **plan):
         from ._state import StateVector
         self.L = L
-        self.state = StateVector(L, device=device)
+        self.state = StateVector(L, device=device, shared=shared)
         if stream_ptr is not None:
             self.state.set_stream(stream_ptr)
         plan.setdefault("use_graph", 0)
@@ -276,6 +283,38 @@ class CudaShard:
     def sync(self):
         self.state.synchronize()
 
+    # -- peer exchange (qsv_slice_swap) ----------------------------------------
+    def ptr(self) -> int:
+        ptr = C.c_void_p()
+        check(lib.qsv_state_device_ptr(self.state._handle(), C.byref(ptr)))
+        return ptr.value
+
+    def device_id(self) -> int:
+        return self.state.get_device()
+
+    def can_reach(self, device) -> bool:
+        import torch
+        me = self.state.get_device()
+        return device == me or torch.cuda.can_device_access_peer(me, device)
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        check(lib.qsv_ipc_export(self.state._handle(), buf))
+        return buf.raw
+
+    def open_peer(self, handle: bytes) -> int:
+        ptr = C.c_void_p()
+        check(lib.qsv_ipc_open(handle, self.state.get_device(), C.byref(ptr)))
+        return ptr.value
+
+    def close_peer(self, ptr: int):
+        check(lib.qsv_ipc_close(self.state.get_device(), C.c_void_p(ptr)))
+
+    def slice_swap(self, peer_ptr, ls, d_mine, d_peer, j0, j1):
+        from ._lib import int_array
+        check(lib.qsv_slice_swap(self.state._handle(), C.c_void_p(peer_ptr), int_array(ls),
+                                 len(ls), d_mine, d_peer, j0, j1))
+
 
 # --------------------------------------------------------------------- engine
 class ShardedQuantumState:
@@ -285,7 +324,7 @@ class ShardedQuantumState:
     ``backend``: callable (L, rank) -> shard backend (default CudaShard)."""
 
     def __init__(self, num_qubits, world=None, rank=None, owned=None, backend=None,
-                 group=None, chunk_bytes=1 << 30, plan=None):
+                 group=None, chunk_bytes=1 << 30, plan=None, exchange="auto"):
         import torch.distributed as dist
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
         if world is None:
@@ -301,16 +340,88 @@ class ShardedQuantumState:
         self.world, self.group = world, group
         self.owned = list(owned) if owned is not None else [rank]
         self.chunk_bytes = int(chunk_bytes)
+        if exchange not in ("auto", "p2p", "nccl"):
+            raise ValueError(f"unknown exchange mode {exchange!r}")
+        self._stream = None
         if backend is None:
             import torch
             dev = torch.cuda.current_device()
-            stream = torch.cuda.current_stream().cuda_stream
+            self._stream = torch.cuda.current_stream()
+            stream = self._stream.cuda_stream
             plan = dict(plan or {})
-            backend = lambda L, r: CudaShard(L, dev, stream, **plan)  # noqa: E731
+            shared = exchange != "nccl" and len(self.owned) < world
+            backend = lambda L, r: CudaShard(L, dev, stream, shared=shared, **plan)  # noqa: E731
         self.shards = {r: backend(self.L, r) for r in self.owned}
         self.phys = list(range(num_qubits))  # logical -> physical
         self.stats = {"swaps": 0, "bytes_sent": 0, "segments": 0}
+        self._peer_ptr = {}
+        self._peer_open = None
+        self.exchange = self._setup_exchange(exchange)
         self.set_zero_state()
+
+    def _setup_exchange(self, mode):
+        """Pick the exchange path; for "p2p" with remote ranks, map every
+        remote shard into this process (CUDA IPC handles swapped with
+        all_gather_object).  All ranks reach the same decision."""
+        capable = all(hasattr(s, "slice_swap") for s in self.shards.values())
+        remote = self.dist is not None and len(self.owned) < self.world
+        if mode == "nccl" or not capable:
+            if mode == "p2p":
+                raise ValueError("p2p exchange needs CudaShard shards")
+            return "nccl"
+        if not remote:
+            return "p2p"
+        shard0 = next(iter(self.shards.values()))
+        dev = shard0.device_id()
+        try:
+            mine = {r: sh.ipc_handle() for r, sh in self.shards.items()}
+        except Exception:  # pooled (non-exportable) shards from a custom backend
+            mine = None
+        procs = self.dist.get_world_size(self.group)
+        info = [None] * procs
+        self.dist.all_gather_object(info, (dev, mine), group=self.group)
+        ok = all(h is not None and shard0.can_reach(d) for d, h in info)
+        votes = [None] * procs
+        self.dist.all_gather_object(votes, ok, group=self.group)
+        if not all(votes):
+            if mode == "p2p":
+                raise RuntimeError("p2p exchange: shards not exportable or GPUs not peers")
+            return "nccl"
+        self._peer_open = shard0
+        for d, handles in info:
+            for r, h in handles.items():
+                if r not in self.shards:
+                    self._peer_ptr[r] = shard0.open_peer(h)
+        if self._stream is None and dev is not None:
+            import torch
+            self._stream = torch.cuda.current_stream()
+        return "p2p"
+
+    def close(self):
+        """Unmap the peers' shards (after a final barrier)."""
+        if self._peer_ptr:
+            self._device_barrier()
+            for s in self.shards.values():
+                s.sync()
+            for ptr in self._peer_ptr.values():
+                self._peer_open.close_peer(ptr)
+            self._peer_ptr = {}
+
+    def _device_barrier(self):
+        """Order every rank's queued shard work before what follows, on the
+        device where possible: a one-element all_reduce on the shard stream
+        (NCCL) completes only after every rank's earlier kernels have run."""
+        if self.dist is None or len(self.owned) == self.world:
+            return
+        if self.dist.get_backend(self.group) == "nccl":
+            import torch
+            with torch.cuda.stream(self._stream):
+                flag = torch.zeros(1, device=f"cuda:{torch.cuda.current_device()}")
+                self.dist.all_reduce(flag, group=self.group)
+        else:
+            for s in self.shards.values():
+                s.sync()
+            self.dist.barrier(group=self.group)
 
     # -- helpers ------------------------------------------------------------
     def _logical_of(self):
@@ -364,7 +475,7 @@ class ShardedQuantumState:
         """Gather the full logical vector on every process (small n only)."""
         part = {r: s.get() for r, s in self.shards.items()}
         if self.dist is not None and len(self.owned) < self.world:
-            objs = [None] * self.world
+            objs = [None] * self.dist.get_world_size(self.group)
             self.dist.all_gather_object(objs, part, group=self.group)
             for o in objs:
                 part.update(o)
@@ -501,7 +612,11 @@ class ShardedQuantumState:
         def gbits(r):
             return sum(((r >> (g - L)) & 1) << j for j, g in enumerate(gs))
 
-        for s in range(1, 1 << k):
+        rounds = 1 << k
+        if self.exchange == "p2p":
+            self._remap_p2p(gs, ls, gbits)
+            rounds = 1  # done
+        for s in range(1, rounds):
             m = 0
             for j in range(k):
                 if (s >> j) & 1:
@@ -529,6 +644,34 @@ class ShardedQuantumState:
             self.phys[qg], self.phys[ql] = lp, g
         self.stats["swaps"] += 1
         self.stats["remapped_qubits"] = self.stats.get("remapped_qubits", 0) + k
+
+    def _remap_p2p(self, gs, ls, gbits):
+        """The exchange step over peer memory: every pair (r, r ^ m) of every
+        round trades slice gbits(partner) of shard r with slice gbits(r) of
+        the partner in place (qsv_slice_swap).  In-process pairs are swapped
+        whole by the lower rank; across processes each owner swaps half, so
+        both GPUs drive NVLink.  Different pairs and rounds touch disjoint
+        slices, so only the step as a whole is fenced by device barriers."""
+        L, k = self.L, len(gs)
+        count = 1 << (L - k)
+        self._device_barrier()
+        for s in range(1, 1 << k):
+            m = 0
+            for j in range(k):
+                if (s >> j) & 1:
+                    m |= 1 << (gs[j] - L)
+            for r in self.owned:
+                partner = r ^ m
+                dm, dp = gbits(partner), gbits(r)
+                if partner in self.shards:
+                    if r < partner:
+                        self.shards[r].slice_swap(self.shards[partner].ptr(), ls, dm, dp, 0, count)
+                else:
+                    half = count // 2
+                    j0, j1 = (0, half) if r < partner else (half, count)
+                    self.shards[r].slice_swap(self._peer_ptr[partner], ls, dm, dp, j0, j1)
+                self.stats["bytes_sent"] += 16 << (L - k)
+        self._device_barrier()
 
     def _swap(self, g, l):
         """Exchange physical global qubit g with local qubit l."""

@@ -2,6 +2,8 @@
 the CPU oracle (lets the host logic of paper_2011_13524_b200.dist run on CPU
 with gloo).  Test infrastructure, never used by the product."""
 
+from multiprocessing import resource_tracker, shared_memory
+
 import numpy as np
 import torch
 
@@ -45,6 +47,71 @@ class OracleShard:
 
     def sync(self):
         pass
+
+
+_BUFS = {}  # "pointer" -> numpy array (own shards and mapped peers)
+
+
+def _spread(j, ls):
+    for p in sorted(ls):
+        j = ((j >> p) << (p + 1)) | (j & ((1 << p) - 1))
+    return j
+
+
+class SharedOracleShard(OracleShard):
+    """OracleShard in POSIX shared memory with the peer-exchange interface
+    of CudaShard (ptr / ipc_handle / open_peer / slice_swap): lets the p2p
+    exchange protocol of dist.py (halves per owner, barriers, rounds) run
+    across gloo processes on CPU, with the shm name standing in for the CUDA
+    IPC handle."""
+
+    def __init__(self, L, rank):
+        self.L = L
+        self.shm = shared_memory.SharedMemory(create=True, size=16 << L)
+        self.a = np.ndarray(1 << L, dtype=np.complex128, buffer=self.shm.buf)
+        self.a[:] = 0
+        self.key = id(self.a)
+        _BUFS[self.key] = self.a
+        self._peers = {}
+
+    def ptr(self):
+        return self.key
+
+    def device_id(self):
+        return None
+
+    def can_reach(self, device):
+        return True
+
+    def ipc_handle(self):
+        return self.shm.name.encode()
+
+    def open_peer(self, handle):
+        shm = shared_memory.SharedMemory(name=handle.decode())
+        resource_tracker.unregister(shm._name, "shared_memory")  # the owner unlinks
+        arr = np.ndarray(1 << self.L, dtype=np.complex128, buffer=shm.buf)
+        _BUFS[id(arr)] = arr
+        self._peers[id(arr)] = shm
+        return id(arr)
+
+    def close_peer(self, key):
+        _BUFS.pop(key, None)
+        self._peers.pop(key).close()
+
+    def slice_swap(self, peer, ls, d_mine, d_peer, j0, j1):
+        j = _spread(np.arange(j0, j1, dtype=np.int64), ls)
+        va = sum(((d_mine >> i) & 1) << p for i, p in enumerate(ls))
+        vb = sum(((d_peer >> i) & 1) << p for i, p in enumerate(ls))
+        b = _BUFS[peer]
+        tmp = self.a[j | va].copy()
+        self.a[j | va] = b[j | vb]
+        b[j | vb] = tmp
+
+    def release(self):
+        _BUFS.pop(self.key, None)
+        del self.a
+        self.shm.close()
+        self.shm.unlink()
 
 
 def random_records(n, ngates, seed):

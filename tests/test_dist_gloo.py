@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 from paper_2011_13524_b200.dist import ShardedQuantumState, specialize
 
 from oracle import qsim_oracle as orc
-from dist_util import OracleShard, random_records
+from dist_util import OracleShard, SharedOracleShard, random_records
 
 
 def _reference(n, records, seed):
@@ -87,6 +87,80 @@ def _worker(rank, world, port, n, q):
         q.put((rank, vec, norm, e, dict(st.stats)))
     finally:
         dist.destroy_process_group()
+
+
+def _worker_p2p(rank, world, port, n, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        recs = random_records(n, 40, seed=77)
+        st = ShardedQuantumState(n, backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p")
+        st.load(orc.haar_state(n, 5))
+        st.apply_records(recs)
+        vec = st.get_vector()
+        e = st.expectation([(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])])
+        mode = st.exchange
+        st.close()
+        dist.barrier()
+        for s in st.shards.values():
+            s.release()
+        q.put((rank, mode, vec, e, dict(st.stats)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_processes_p2p_protocol(world):
+    """The peer-memory exchange protocol (dist.ShardedQuantumState
+    exchange="p2p": mapped peer shards, each owner swapping half of every
+    pair's slice, barriers around the step) across processes, with shared
+    memory standing in for CUDA IPC."""
+    n = 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_p2p, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = _reference(n, random_records(n, 40, seed=77), 5)
+    e_ref = orc.expectation(ref, ref, n, [(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])])
+    for rank, mode, vec, e, stats in res:
+        assert mode == "p2p"
+        assert np.max(np.abs(vec - ref)) <= 1e-12, rank
+        assert abs(e - e_ref) <= 1e-11
+        assert stats["swaps"] > 0
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_virtual_ranks_p2p_protocol(world):
+    n = 9
+    recs = random_records(n, 60, seed=5)
+    st = ShardedQuantumState(n, world=world, owned=list(range(world)),
+                             backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p")
+    assert st.exchange == "p2p"
+    st.load(orc.haar_state(n, 2))
+    st.apply_records(recs)
+    got = st.get_vector()
+    for s in st.shards.values():
+        s.release()
+    assert np.max(np.abs(got - _reference(n, recs, 2))) <= 1e-12
+
+
+def test_exchange_mode_selection():
+    with pytest.raises(ValueError):
+        ShardedQuantumState(5, world=2, owned=[0, 1], backend=lambda L, r: OracleShard(L, r),
+                            exchange="p2p")
+    with pytest.raises(ValueError):
+        ShardedQuantumState(5, world=2, owned=[0, 1], backend=lambda L, r: OracleShard(L, r),
+                            exchange="bogus")
+    st = ShardedQuantumState(5, world=2, owned=[0, 1], backend=lambda L, r: OracleShard(L, r))
+    assert st.exchange == "nccl"
 
 
 @pytest.mark.parametrize("world", [2, 4])
