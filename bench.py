@@ -344,7 +344,7 @@ def run_ours(args, rank, world, local_rank):
         pipe = None
         try:
             pipe = e2e_pipelined(qs, gates, n, dev, torch, bytes_step, world,
-                                 max(3, 2 * e2e_steps), barrier, dist)
+                                 max(8, 2 * e2e_steps), barrier, dist)
         except Exception as exc:  # noqa: BLE001  (reported, never fatal)
             serial["pipelined_error"] = f"{type(exc).__name__}: {exc}"
         e2e = pipe if pipe is not None else serial

@@ -398,14 +398,32 @@ class ShardedQuantumState:
         return "p2p"
 
     def close(self):
-        """Unmap the peers' shards (after a final barrier)."""
+        """Unmap the peers' shards after a final barrier (collective: every
+        rank calls it).  Also a context manager."""
         if self._peer_ptr:
             self._device_barrier()
             for s in self.shards.values():
                 s.sync()
-            for ptr in self._peer_ptr.values():
+            self._unmap()
+
+    def _unmap(self):
+        for ptr in self._peer_ptr.values():
+            try:
                 self._peer_open.close_peer(ptr)
-            self._peer_ptr = {}
+            except Exception:  # noqa: BLE001  (teardown: best effort)
+                pass
+        self._peer_ptr = {}
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        # no barrier here (not collective): just drop this process's mappings
+        if getattr(self, "_peer_ptr", None):
+            self._unmap()
 
     def _device_barrier(self):
         """Order every rank's queued shard work before what follows, on the

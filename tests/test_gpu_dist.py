@@ -148,3 +148,28 @@ def test_ipc_processes_p2p_exchange(world):
         assert abs(norm - 1.0) <= 1e-12
         assert abs(e - e_ref) <= 1e-11
         assert stats["swaps"] > 0
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_cfg5_shape_sharded_matches_single_state(world):
+    """cfg5's workload shape at n=24 (the sharded engine at
+    n<=24 on P=2/4/8): cz-ladder(24, depth 20, seed 1) over P virtual ranks
+    (p2p remaps, rank-specialised tiled segments) against the single-state
+    engine, itself pinned to the C oracle at n=30 (profiles/r1_parity_n30.json)."""
+    import torch
+    import paper_2011_13524_b200 as qs
+    from paper_2011_13524_b200 import workloads
+    from paper_2011_13524_b200._circuit import circuit_records
+    n = 24
+    circ = workloads.generate_cz_ladder(n, 20, seed=1)
+    one = qs.QuantumState(n)
+    circ.update_quantum_state(one)
+    ref = one.get_vector()
+    stream = torch.cuda.current_stream().cuda_stream
+    st = ShardedQuantumState(n, world=world, owned=list(range(world)),
+                             backend=lambda L, r: CudaShard(L, 0, stream))
+    st.set_zero_state()
+    st.apply_records(circuit_records(circ))
+    assert st.exchange == "p2p" and st.stats["swaps"] > 0
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+    assert abs(st.get_squared_norm() - 1.0) <= 1e-12
