@@ -566,9 +566,12 @@ def run_sharded_circuit(args, rank, world, dev, stream):
         ms = float(t.item())
     norm = st.get_squared_norm()
     mode = st.exchange
+    overlapped = {"enabled": st.overlap, "steps": st.stats.get("overlapped", 0) // 2,
+                  "gates": st.stats.get("overlapped_gates", 0) // 2}
     st.close()
     del st
     return {"metric": "random-circuit sec/layer (sharded)", "exchange": mode, "unit": "s/layer",
+            "exchange_compute_overlap": overlapped,
             "value": ms / 1e3 / (depth + 1), "higher_is_better": False,
             "workload": f"cz-ladder n={n} depth={depth} seed=1 over {vworld} "
                         f"{'virtual ranks on one GPU' if virtual else 'GPUs'} "

@@ -212,6 +212,10 @@ typedef struct qsv_plan_opts {
   int32_t use_graph;      /* 1: replay through a CUDA graph                */
   int32_t real_frames;    /* 1: run 1-qubit gates as real rotations with   */
                           /*    their phases merged into diagonal flushes */
+  int32_t reserved;       /* 0                                             */
+  uint64_t outer_mask;    /* qubits never chosen as tile qubits, so the    */
+                          /* program can run on the block of amplitudes   */
+                          /* with those bits fixed (qsv_program_run_fixed) */
 } qsv_plan_opts;
 
 typedef struct qsv_program_stats {
@@ -226,6 +230,14 @@ typedef struct qsv_program_stats {
 int qsv_program_create(int num_qubits, const qsv_op* ops, int nops,
                        const qsv_plan_opts* opts, qsv_program** out);
 int qsv_program_run(qsv_program* prog, qsv_state* st);
+/* Run on the amplitudes whose bits in `mask` equal `value` only (the other
+ * blocks are untouched): the program's tile passes enumerate just those
+ * tiles.  `mask` must avoid every tile qubit (plan with outer_mask ⊇ mask)
+ * and the program must consist of tile passes only (QSV_EUNSUPPORTED
+ * otherwise; qsv_program_stats.num_gate_kernels == 0).  The sharded engine
+ * runs a segment block by block this way while the next block is still
+ * being exchanged (dist.py _remap_overlapped). */
+int qsv_program_run_fixed(qsv_program* prog, qsv_state* st, uint64_t mask, uint64_t value);
 int qsv_program_stats_get(const qsv_program* prog, qsv_program_stats* out);
 int qsv_program_destroy(qsv_program* prog);
 /* Host-only: plan without touching a device (stats only). */
@@ -253,6 +265,19 @@ int qsv_ipc_open(const void* handle, int device, void** peer_amps);
 int qsv_ipc_close(int device, void* peer_amps);
 int qsv_slice_swap(qsv_state* st, void* peer_amps, const int* ls, int k, uint64_t d_mine,
                    uint64_t d_peer, uint64_t j0, uint64_t j1);
+
+/* Exchange / compute overlap (dist.py _remap_overlapped).  qsv_state_view
+ * makes a non-owning state over amplitudes [offset, offset + 2^num_qubits)
+ * of `parent` (offset a multiple of 2^num_qubits): the block of a shard
+ * whose top qubits are fixed, so a segment of local gates that leaves those
+ * qubits alone runs on it (own stream, own reduction scratch) while the
+ * rest of the shard is still being exchanged.  The view must be destroyed
+ * before its parent and cannot be IPC-exported.  qsv_set_sm_limit caps the
+ * SMs used by the tile passes and slice swaps launched for a state (0 = all),
+ * so an exchange kernel and a tile pass on two streams share the GPU instead
+ * of one waiting for the other's persistent CTAs. */
+int qsv_state_view(qsv_state* parent, uint64_t offset, int num_qubits, qsv_state** out);
+int qsv_set_sm_limit(qsv_state* st, int sms);
 
 #ifdef __cplusplus
 }

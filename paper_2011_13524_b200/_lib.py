@@ -54,6 +54,8 @@ class QsvPlanOpts(C.Structure):
         ("fuse", C.c_int32),
         ("use_graph", C.c_int32),
         ("real_frames", C.c_int32),
+        ("reserved", C.c_int32),
+        ("outer_mask", C.c_uint64),
     ]
 
 
@@ -92,6 +94,8 @@ _SIGS = {
     "qsv_ipc_open": ([_P, _I, C.POINTER(_P)], _I),
     "qsv_ipc_close": ([_I, _P], _I),
     "qsv_slice_swap": ([_P, _P, _IP, _I, _U64, _U64, _U64, _U64], _I),
+    "qsv_state_view": ([_P, _U64, _I, C.POINTER(_P)], _I),
+    "qsv_set_sm_limit": ([_P, _I], _I),
     "qsv_state_destroy": ([_P], _I),
     "qsv_state_num_qubits": ([_P, _IP], _I),
     "qsv_state_device_ptr": ([_P, C.POINTER(_P)], _I),
@@ -128,6 +132,7 @@ _SIGS = {
     "qsv_trace_pairs": ([_P, C.POINTER(C.c_double)], _I),
     "qsv_program_create": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts), C.POINTER(_P)], _I),
     "qsv_program_run": ([_P, _P], _I),
+    "qsv_program_run_fixed": ([_P, _P, _U64, _U64], _I),
     "qsv_program_stats_get": ([_P, C.POINTER(QsvProgramStats)], _I),
     "qsv_program_destroy": ([_P], _I),
     "qsv_plan_stats": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts),

@@ -27,7 +27,7 @@ def _check_count(n) -> int:
 class StateVector:
     """2^n amplitudes on a GPU plus the classical register list."""
 
-    __slots__ = ("_h", "_n", "_device", "_cregs", "__weakref__")
+    __slots__ = ("_h", "_n", "_device", "_cregs", "_parent", "__weakref__")
 
     def __init__(self, qubit_count: int, device: int = 0, shared: bool = False):
         n = _check_count(qubit_count)
@@ -35,6 +35,7 @@ class StateVector:
         self._n = n
         self._device = int(device)
         self._cregs: list[int] = []
+        self._parent = None
         h = C.c_void_p()
         create = lib.qsv_state_create_shared if shared else lib.qsv_state_create
         check(create(n, self._device, C.byref(h)))
@@ -48,6 +49,23 @@ class StateVector:
 
     def _handle(self):
         return self._h
+
+    def _view(self, offset: int, qubit_count: int) -> "StateVector":
+        """Non-owning state over amplitudes [offset, offset + 2^qubit_count)
+        (qsv_state_view); keeps this state alive while it exists."""
+        v = StateVector.__new__(StateVector)
+        v._h = None
+        v._n = int(qubit_count)
+        v._device = self._device
+        v._cregs = []
+        v._parent = self
+        h = C.c_void_p()
+        check(lib.qsv_state_view(self._h, int(offset), v._n, C.byref(h)))
+        v._h = h
+        return v
+
+    def _set_sm_limit(self, sms: int) -> None:
+        check(lib.qsv_set_sm_limit(self._h, int(sms)))
 
     # -- shape -------------------------------------------------------------
     def get_qubit_count(self) -> int:

@@ -66,6 +66,18 @@ static std::map<const qsv_state*, Scratch> g_payload;
 static std::map<const qsv_state*, Scratch> g_results;
 static std::map<const qsv_state*, Scratch> g_analysis;
 static constexpr size_t kPartialBytes = sizeof(double) * 2 * kRedBlocks * kMaxTerms;
+// the tile kernel's work counters follow the reduction scratch (zeroed once,
+// reset by the last CTA of every tile pass)
+static constexpr size_t kScratchBytes = kPartialBytes + 2 * sizeof(unsigned long long);
+
+static cudaError_t alloc_scratch(qsv_state* st) {
+  cudaError_t e = dev_alloc(reinterpret_cast<void**>(&st->partials), kScratchBytes, st->device,
+                            st->stream);
+  if (e != cudaSuccess) return e;
+  st->tile_ctr = reinterpret_cast<unsigned long long*>(
+      reinterpret_cast<char*>(st->partials) + kPartialBytes);
+  return cudaMemsetAsync(st->tile_ctr, 0, 2 * sizeof(unsigned long long), st->stream);
+}
 
 // ------------------------------------------------------------ allocator
 // State vectors up to kPoolMaxBytes come from the device's stream-ordered
@@ -278,6 +290,9 @@ static int state_create(int num_qubits, int device, bool plain, qsv_state** out)
   st->partials = nullptr;
   st->host_res = nullptr;
   st->plain = plain ? 1 : 0;
+  st->view = 0;
+  st->sm_limit = 0;
+  st->tile_ctr = nullptr;
   const size_t bytes = std::max<size_t>(st->dim * sizeof(double2), 32);
   cudaError_t e = plain ? cudaMalloc(reinterpret_cast<void**>(&st->amps), bytes)
                         : dev_alloc(reinterpret_cast<void**>(&st->amps), bytes, device, st->stream);
@@ -288,7 +303,7 @@ static int state_create(int num_qubits, int device, bool plain, qsv_state** out)
     cudaGetLastError();
     return QSV_ENOMEM;
   }
-  e = dev_alloc(reinterpret_cast<void**>(&st->partials), kPartialBytes, device, st->stream);
+  e = alloc_scratch(st);
   if (e != cudaSuccess) {
     if (plain) cudaFree(st->amps);
     else dev_free(st->amps, bytes, st->stream);
@@ -307,18 +322,68 @@ int qsv_state_create_shared(int num_qubits, int device, qsv_state** out) {
   return state_create(num_qubits, device, true, out);
 }
 
+int qsv_state_view(qsv_state* parent, uint64_t offset, int num_qubits, qsv_state** out) {
+  if (bad_state(parent) || !out) {
+    if (!out) set_error("null output pointer");
+    return QSV_EINVAL;
+  }
+  *out = nullptr;
+  if (num_qubits < 1 || num_qubits > parent->n) {
+    set_error("view qubit count %d outside [1, %d]", num_qubits, parent->n);
+    return QSV_EINVAL;
+  }
+  const uint64_t dim = 1ULL << num_qubits;
+  if (offset % dim != 0 || offset >= parent->dim) {
+    set_error("view offset %llu is not a multiple of 2^%d inside the state",
+              (unsigned long long)offset, num_qubits);
+    return QSV_EINVAL;
+  }
+  DeviceGuard dg(parent->device);
+  qsv_state* st = new qsv_state();
+  st->n = num_qubits;
+  st->device = parent->device;
+  st->dim = dim;
+  st->stream = parent->stream;
+  st->amps = parent->amps + offset;
+  st->partials = nullptr;
+  st->host_res = nullptr;
+  st->plain = 0;
+  st->view = 1;
+  st->sm_limit = 0;
+  st->tile_ctr = nullptr;
+  cudaError_t e = alloc_scratch(st);
+  if (e != cudaSuccess) {
+    delete st;
+    return cuda_fail(e, "cudaMalloc(partials)");
+  }
+  *out = st;
+  return QSV_OK;
+}
+
+int qsv_set_sm_limit(qsv_state* st, int sms) {
+  if (bad_state(st)) return QSV_EINVAL;
+  if (sms < 0) {
+    set_error("SM limit must be >= 0, got %d", sms);
+    return QSV_EINVAL;
+  }
+  st->sm_limit = sms;
+  return QSV_OK;
+}
+
 int qsv_state_destroy(qsv_state* st) {
   if (!st) return QSV_OK;
   DeviceGuard dg(st->device);
   // stream-ordered release: the pool reuses the blocks after the work queued
   // on this stream (no host synchronisation for pooled blocks)
-  if (st->plain) {
+  if (st->view) {
+    // the parent owns the amplitudes
+  } else if (st->plain) {
     cudaStreamSynchronize(st->stream);
     cudaFree(st->amps);
   } else {
     dev_free(st->amps, std::max<size_t>(st->dim * sizeof(double2), 32), st->stream);
   }
-  dev_free(st->partials, kPartialBytes, st->stream);
+  dev_free(st->partials, kScratchBytes, st->stream);
   for (auto* mp : {&g_payload, &g_results, &g_analysis}) {
     auto it = mp->find(st);
     if (it != mp->end()) {

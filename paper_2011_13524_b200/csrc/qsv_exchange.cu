@@ -29,6 +29,7 @@ struct SliceMap {
 };
 
 constexpr int kSwapThreads = 256;
+constexpr int kSwapFatThreads = 1024;  // SM-limited launches: one fat CTA per SM
 constexpr int kSwapPer = 4;  // elements per thread in flight (loads before stores)
 
 __device__ __forceinline__ uint64_t spread(uint64_t j, const SliceMap& m) {
@@ -40,10 +41,10 @@ __device__ __forceinline__ uint64_t spread(uint64_t j, const SliceMap& m) {
   return j;
 }
 
-__global__ void __launch_bounds__(kSwapThreads) k_slice_swap(double2* __restrict__ a,
-                                                             double2* __restrict__ b,
-                                                             SliceMap m, uint64_t j0,
-                                                             uint64_t j1) {
+template <int Threads>
+__global__ void __launch_bounds__(Threads) k_slice_swap(double2* __restrict__ a,
+                                                        double2* __restrict__ b, SliceMap m,
+                                                        uint64_t j0, uint64_t j1) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = j0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; base < j1;
        base += stride * kSwapPer) {
@@ -80,6 +81,10 @@ extern "C" {
 int qsv_ipc_export(const qsv_state* st, void* handle_out) {
   if (!st || !handle_out) {
     set_error("null state or handle buffer");
+    return QSV_EINVAL;
+  }
+  if (st->view) {
+    set_error("a state view cannot be exported (export the state that owns the buffer)");
     return QSV_EINVAL;
   }
   if (!st->plain && st->dim * sizeof(double2) <= (1ULL << 30)) {
@@ -148,11 +153,23 @@ int qsv_slice_swap(qsv_state* st, void* peer_amps, const int* ls, int k, uint64_
   DeviceGuard dg(st->device);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st->device);
-  const uint64_t per_block = (uint64_t)kSwapThreads * kSwapPer;
-  const uint64_t want = (j1 - j0 + per_block - 1) / per_block;
-  const int blocks = (int)std::min<uint64_t>(want, (uint64_t)sms * 8);
-  k_slice_swap<<<blocks, kSwapThreads, 0, st->stream>>>(
-      st->amps, static_cast<double2*>(peer_amps), m, j0, j1);
+  double2* peer = static_cast<double2*>(peer_amps);
+  if (st->sm_limit > 0) {
+    // overlapped with tile passes on another stream: at most sm_limit SMs,
+    // one 1024-thread CTA each (the tile kernel's CTAs fill a whole SM, so
+    // thin CTAs spread over many SMs would block its launch)
+    const uint64_t per_block = (uint64_t)kSwapFatThreads * kSwapPer;
+    const uint64_t want = (j1 - j0 + per_block - 1) / per_block;
+    const int blocks = (int)std::min<uint64_t>(want, (uint64_t)std::min(st->sm_limit, sms));
+    k_slice_swap<kSwapFatThreads><<<blocks, kSwapFatThreads, 0, st->stream>>>(
+        st->amps, peer, m, j0, j1);
+  } else {
+    const uint64_t per_block = (uint64_t)kSwapThreads * kSwapPer;
+    const uint64_t want = (j1 - j0 + per_block - 1) / per_block;
+    const int blocks = (int)std::min<uint64_t>(want, (uint64_t)sms * 8);
+    k_slice_swap<kSwapThreads><<<blocks, kSwapThreads, 0, st->stream>>>(
+        st->amps, peer, m, j0, j1);
+  }
   QSV_TRY(cudaGetLastError());
   return QSV_OK;
 }

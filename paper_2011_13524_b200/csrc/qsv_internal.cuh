@@ -155,6 +155,10 @@ struct qsv_state {
   double* partials;   // device reduction scratch
   double* host_res;   // pinned result slots
   int plain;          // amps from cudaMalloc (IPC-exportable shard), not the pool
+  int view;           // amps alias another state's buffer (qsv_state_view): not freed
+  int sm_limit;       // > 0: tile passes / slice swaps launched for this state use at
+                      // most this many SMs (qsv_set_sm_limit; exchange overlap)
+  unsigned long long* tile_ctr;  // tile-pass work counters (2, self-resetting; after partials)
 };
 
 // ----------------------------------------------------------------------

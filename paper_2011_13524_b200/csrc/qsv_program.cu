@@ -22,6 +22,7 @@ struct qsv_program {
   void* dev_payload = nullptr;
   size_t payload_bytes = 0;
   int payload_device = -1;       // device holding dev_payload
+  cudaEvent_t payload_ready = nullptr;  // the upload's completion (runs wait on it)
   std::vector<char> host_payload;  // re-uploaded when a state on another device runs it
   qsv_program_stats stats;
   qsv_plan_opts opts;
@@ -30,6 +31,7 @@ struct qsv_program {
   cudaGraph_t graph = nullptr;
   double2* graph_amps = nullptr;
   cudaStream_t graph_stream = nullptr;
+  int graph_sm_limit = 0;
   cudaStream_t last_stream = 0;  // the payload is released in this stream's order
   uint64_t runs = 0;
   int device = -1;
@@ -37,7 +39,8 @@ struct qsv_program {
 
 namespace {
 
-int launch_steps(qsv_program* p, double2* amps, cudaStream_t s) {
+int launch_steps(qsv_program* p, double2* amps, cudaStream_t s, int max_ctas,
+                 unsigned long long* ctr, uint64_t fmask = 0, uint64_t fval = 0) {
   for (const Step& st : p->steps) {
     int rc;
     if (st.type == 0) {
@@ -46,15 +49,29 @@ int launch_steps(qsv_program* p, double2* amps, cudaStream_t s) {
                          : nullptr;
       rc = launch_gate(amps, p->n, st.gate, dev, s);
     } else {
-      rc = launch_tile_pass(amps, p->n, p->tiles[st.tile], p->dev_payload, s);
+      rc = launch_tile_pass(amps, p->n, p->tiles[st.tile], p->dev_payload, s, max_ctas, ctr,
+                            fmask, fval);
     }
     if (rc) return rc;
   }
   return QSV_OK;
 }
 
+// A private non-blocking stream per device for payload uploads: the copy
+// neither waits for nor blocks the work queued on the legacy / state streams
+// (a synchronous cudaMemcpy would first drain the legacy stream, stalling the
+// host behind every kernel queued so far -- e.g. the sharded engine compiling
+// the next segment while the current exchange is still running).
+cudaStream_t upload_stream(int dev) {
+  static cudaStream_t streams[64] = {};
+  if (dev < 0 || dev >= 64) return 0;
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
 // payload on `dev` (programs are built on the current device; a state on
-// another device triggers a re-upload there)
+// another device triggers a re-upload there).  Asynchronous: runs wait on
+// payload_ready; host_payload stays alive as the copy's source.
 int upload_payload(qsv_program* p, int dev) {
   if (p->host_payload.empty() || p->payload_device == dev) return QSV_OK;
   if (p->dev_payload) {
@@ -62,14 +79,22 @@ int upload_payload(qsv_program* p, int dev) {
     dev_free(p->dev_payload, p->payload_bytes, p->last_stream);
     p->dev_payload = nullptr;
   }
+  if (p->payload_ready) {
+    cudaEventDestroy(p->payload_ready);
+    p->payload_ready = nullptr;
+  }
   DeviceGuard dg(dev);
-  cudaError_t e = dev_alloc(&p->dev_payload, p->payload_bytes, dev, 0);
+  cudaStream_t us = upload_stream(dev);
+  cudaError_t e = dev_alloc(&p->dev_payload, p->payload_bytes, dev, us);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(program payload)");
-  e = cudaMemcpy(p->dev_payload, p->host_payload.data(), p->payload_bytes,
-                 cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(program payload)");
+  e = cudaMemcpyAsync(p->dev_payload, p->host_payload.data(), p->payload_bytes,
+                      cudaMemcpyHostToDevice, us);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(program payload)");
+  e = cudaEventCreateWithFlags(&p->payload_ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(p->payload_ready, us);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(program payload)");
   p->payload_device = dev;
-  p->last_stream = 0;
+  p->last_stream = us;
   return QSV_OK;
 }
 
@@ -224,13 +249,14 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
     const int rc = upload_payload(p, st->device);
     if (rc) return rc;
   }
+  if (p->payload_ready) QSV_TRY(cudaStreamWaitEvent(st->stream, p->payload_ready, 0));
   p->last_stream = st->stream;
   // the first run launches directly: a program that runs once (a recompile
   // after set_parameter) never pays for graph capture + instantiation
   if (!p->opts.use_graph || p->steps.empty() || p->runs++ == 0)
-    return launch_steps(p, st->amps, st->stream);
+    return launch_steps(p, st->amps, st->stream, st->sm_limit, st->tile_ctr);
   if (!(p->gexec && p->graph_amps == st->amps && p->graph_stream == st->stream &&
-        p->device == st->device)) {
+        p->device == st->device && p->graph_sm_limit == st->sm_limit)) {
     drop_graph(p);
     // capture on a private stream (the legacy stream cannot be captured)
     cudaStream_t cap;
@@ -240,7 +266,7 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
       cudaStreamDestroy(cap);
       return cuda_fail(e, "cudaStreamBeginCapture");
     }
-    int rc = launch_steps(p, st->amps, cap);
+    int rc = launch_steps(p, st->amps, cap, st->sm_limit, st->tile_ctr);
     cudaGraph_t g = nullptr;
     e = cudaStreamEndCapture(cap, &g);
     cudaStreamDestroy(cap);
@@ -257,10 +283,46 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
     p->graph = g;
     p->graph_amps = st->amps;
     p->graph_stream = st->stream;
+    p->graph_sm_limit = st->sm_limit;
     p->device = st->device;
   }
   QSV_TRY(cudaGraphLaunch(p->gexec, st->stream));
   return QSV_OK;
+}
+
+int qsv_program_run_fixed(qsv_program* p, qsv_state* st, uint64_t mask, uint64_t value) {
+  if (!p || !st) {
+    set_error("null handle");
+    return QSV_EINVAL;
+  }
+  if (p->n != st->n) {
+    set_error("state and circuit qubit counts differ (%d vs %d)", st->n, p->n);
+    return QSV_EINVAL;
+  }
+  if ((st->n < 64 && (mask >> st->n) != 0) || (value & ~mask) != 0) {
+    set_error("fixed mask / value outside the state's qubits");
+    return QSV_EINVAL;
+  }
+  for (const Step& s : p->steps) {
+    if (s.type == 0) {
+      set_error("program has per-gate kernels; only tile passes can run on a block");
+      return QSV_EUNSUPPORTED;
+    }
+    for (int q : p->tiles[s.tile].qubits)
+      if ((mask >> q) & 1) {
+        set_error("fixed qubit %d is a tile qubit (plan with outer_mask)", q);
+        return QSV_EINVAL;
+      }
+  }
+  DeviceGuard dg(st->device);
+  if (p->payload_device != st->device && !p->host_payload.empty()) {
+    drop_graph(p);
+    const int rc = upload_payload(p, st->device);
+    if (rc) return rc;
+  }
+  if (p->payload_ready) QSV_TRY(cudaStreamWaitEvent(st->stream, p->payload_ready, 0));
+  p->last_stream = st->stream;
+  return launch_steps(p, st->amps, st->stream, st->sm_limit, st->tile_ctr, mask, value);
 }
 
 int qsv_program_stats_get(const qsv_program* p, qsv_program_stats* out) {
@@ -280,6 +342,7 @@ int qsv_program_destroy(qsv_program* p) {
     DeviceGuard dg(p->payload_device);
     dev_free(p->dev_payload, p->payload_bytes, p->last_stream);
   }
+  if (p->payload_ready) cudaEventDestroy(p->payload_ready);
   delete p;
   return QSV_OK;
 }

@@ -127,7 +127,8 @@ struct PlanMix {
   std::vector<GateDesc> preprocess(int n, const std::vector<GateDesc>& gates,              \
                                    const qsv_plan_opts& opts);                              \
   int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,   \
-                       cudaStream_t s);                                                     \
+                       cudaStream_t s, int max_ctas, unsigned long long* ctr,               \
+                       uint64_t fmask, uint64_t fval);                                      \
   }
 QSV_TILE_DECLARE(r4)
 QSV_TILE_DECLARE(r5)
@@ -139,6 +140,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
                  std::vector<char>& payload, qsv_program_stats* stats);
 
 int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,
-                     cudaStream_t s);
+                     cudaStream_t s, int max_ctas, unsigned long long* ctr, uint64_t fmask,
+                     uint64_t fval);
 
 }  // namespace qsv

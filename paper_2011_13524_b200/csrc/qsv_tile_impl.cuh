@@ -612,7 +612,12 @@ __device__ __forceinline__ void group_sync(int group) {
 }
 
 // Persistent tile kernel.  Each CTA = kGroups groups of kGroupThreads threads;
-// group g of CTA b walks tiles g + kGroups * (b + k * gridDim.x).  A group
+// a group takes its next tile from a global work counter (ctr[0], fetched one
+// tile ahead so the atomic's latency hides behind the current tile), so CTAs
+// that become resident late -- e.g. while an exchange kernel holds some SMs
+// (dist.py overlap) -- simply process fewer tiles.  The last CTA to finish
+// resets both counters (ctr[1] counts finished CTAs) for the next launch on
+// the stream.  A group
 // copies its tile HBM -> shared memory (cp.async, XOR-swizzled 16-byte
 // slots), runs the phases with its own named barrier, and writes it back;
 // the groups drift apart so copies/transposes of one overlap the math of the
@@ -621,8 +626,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     k_tile(double2* __restrict__ a, const TilePassDev* __restrict__ pd,
            const TilePhase* __restrict__ phases, const TileOp* __restrict__ g_ops,
            const double2* __restrict__ g_data, FixedBits tb, uint64_t ntiles, int nops,
-           int ndata) {
+           int ndata, unsigned long long* __restrict__ ctr) {
   extern __shared__ double2 smem_all[];
+  __shared__ unsigned long long s_next[kGroups];
   __shared__ uint64_t s_hi[kRegs + 1];   // HBM offset of copy-index bits >= kTidBits (+ flag)
   __shared__ uint64_t s_lo[kCtaThreads]; // HBM offset of copy-index bits < kTidBits
   const int L = pd->L;
@@ -674,8 +680,12 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     while (*s_go < group) __nanosleep(256);
   bool first = true;
 
-  for (uint64_t tile = (uint64_t)blockIdx.x * kGroups + group; tile < ntiles;
-       tile += (uint64_t)gridDim.x * kGroups) {
+  if (tid == 0) s_next[group] = atomicAdd(ctr, 1ULL);
+  group_sync(group);
+  uint64_t tile = s_next[group];
+  while (tile < ntiles) {
+    unsigned long long next = 0;
+    if (tid == 0) next = atomicAdd(ctr, 1ULL);  // the group's following tile
     const uint64_t base = widen(tile, tb);
     if (copy_thread) {
       const uint64_t gb = base | s_lo[threadIdx.x];
@@ -729,11 +739,23 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         }
       }
     }
+    if (tid == 0) s_next[group] = next;
     group_sync(group);  // the tile buffer is refilled next iteration
     if (group == 0 && first && tid == 0) *s_go = kGroups;
     first = false;
+    tile = s_next[group];
   }
   if (group == 0 && tid == 0) *s_go = kGroups;  // no tile / no phase: release the others
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // every atomic of this CTA is done; the last CTA resets the counters
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1ULL) == gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ======================================================================= host
@@ -888,7 +910,7 @@ struct PassSel {
 // a qubit with it and its active qubits fit in S (growing S up to L).
 PassSel select_pass(int n, int L, const std::vector<GateDesc>& gates,
                     const std::vector<uint64_t>& act, const std::vector<char>& ok,
-                    const std::vector<char>& done, size_t first) {
+                    const std::vector<char>& done, size_t first, uint64_t outer) {
   PassSel ps;
   const int c = std::min(kLowQubits, n);
   ps.S = (c >= 64) ? ~0ULL : ((1ULL << c) - 1);
@@ -924,8 +946,10 @@ PassSel select_pass(int n, int L, const std::vector<GateDesc>& gates,
       if ((blocked & all) == all) break;
     }
   }
-  // pad S to exactly L qubits with the lowest unused qubits
-  for (int q = 0; q < n && popc64(ps.S) < L; ++q) ps.S |= 1ULL << q;
+  // pad S to exactly L qubits with the lowest unused qubits (never an
+  // outer-mask qubit: those stay outside so blocks can run separately)
+  for (int q = 0; q < n && popc64(ps.S) < L; ++q)
+    if (!((outer >> q) & 1)) ps.S |= 1ULL << q;
   return ps;
 }
 
@@ -1829,7 +1853,8 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
   // a gate fits a tile only together with the always-present low qubits
   const uint64_t lowq = (n >= 64) ? ~0ULL : ((1ULL << std::min(kLowQubits, n)) - 1);
   for (size_t i = 0; i < G; ++i)
-    ok[i] = active_qubits(gates[i], &act[i]) && popc64(act[i] | lowq) <= L;
+    ok[i] = active_qubits(gates[i], &act[i]) && popc64(act[i] | lowq) <= L &&
+            !(act[i] & opts.outer_mask);
   size_t first = 0;
   while (true) {
     while (first < G && done[first]) ++first;
@@ -1839,10 +1864,15 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       done[first] = 1;
       continue;
     }
-    PassSel ps = select_pass(n, L, gates, act, ok, done, first);
-    if (ps.taken.size() <= 1) {
-      if (ps.taken.empty()) ps.taken.push_back((int)first);  // cannot happen (ok[] checks fit)
-      // a lone gate is cheaper as its own streaming kernel
+    PassSel ps = select_pass(n, L, gates, act, ok, done, first, opts.outer_mask);
+    if (popc64(ps.S) < L || (ps.S & opts.outer_mask)) {
+      set_error("outer mask leaves too few tile qubits (%d qubits, tile %d)", n, L);
+      return QSV_EINVAL;
+    }
+    if (ps.taken.empty()) ps.taken.push_back((int)first);  // cannot happen (ok[] checks fit)
+    if (ps.taken.size() == 1 && !opts.outer_mask) {
+      // a lone gate is cheaper as its own streaming kernel (not when the
+      // program must run block by block: there every step is a tile pass)
       add_gate_step(n, gates[ps.taken[0]], steps, payload, stats);
       done[ps.taken[0]] = 1;
       continue;
@@ -1914,7 +1944,8 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
 }
 
 int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,
-                     cudaStream_t s) {
+                     cudaStream_t s, int max_ctas, unsigned long long* ctr, uint64_t fmask,
+                     uint64_t fval) {
   const char* basep = (const char*)dev_payload + tp.dev_off;
   size_t off = align_up(sizeof(TilePassDev), 16);
   const TilePassDev* pd = reinterpret_cast<const TilePassDev*>(basep);
@@ -1923,9 +1954,20 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
   const TileOp* ops = reinterpret_cast<const TileOp*>(basep + off);
   off = align_up(off + tp.nops * sizeof(TileOp), 16);
   const double2* data = reinterpret_cast<const double2*>(basep + off);
-  int pos[kMaxTileQubits];
-  for (int j = 0; j < tp.L; ++j) pos[j] = tp.qubits[j];
-  FixedBits tb = make_fixed(pos, tp.L, 0);
+  // tiles enumerate the outer qubits; fixed ones (fmask, run_fixed) are
+  // inserted with their value, so only that block's tiles are visited
+  int pos[kMaxFixed];
+  int np = 0;
+  for (int j = 0; j < tp.L; ++j) pos[np++] = tp.qubits[j];
+  for (int q = 0; q < n; ++q)
+    if ((fmask >> q) & 1) {
+      if (np >= kMaxFixed) {
+        set_error("too many fixed qubits for a tile pass");
+        return QSV_EINVAL;
+      }
+      pos[np++] = q;
+    }
+  FixedBits tb = make_fixed(pos, np, fval & fmask);
   const size_t smem = kGroups * (sizeof(double2) << tp.L) + tp.nops * sizeof(TileOp) +
                       tp.ndata * sizeof(double2) + tp.nphases * sizeof(TilePhase);
   if (smem > kTileSmemLimit) {
@@ -1943,11 +1985,12 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     attr_dev = dev;
   }
-  const uint64_t ntiles = 1ULL << (n - tp.L);
+  const uint64_t ntiles = 1ULL << (n - np);
   const uint64_t ctas = (ntiles + kGroups - 1) / kGroups;
-  const unsigned grid = (unsigned)std::min<uint64_t>(ctas, (uint64_t)num_sms);
+  const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms) : num_sms;
+  const unsigned grid = (unsigned)std::min<uint64_t>(ctas, (uint64_t)sms);
   k_tile<<<grid, kCtaThreads, smem, s>>>(amps, pd, ph, ops, data, tb, ntiles, tp.nops,
-                                          tp.ndata);
+                                          tp.ndata, ctr);
   QSV_CHECK_LAUNCH("k_tile");
   return QSV_OK;
 }

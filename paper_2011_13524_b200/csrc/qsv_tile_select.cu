@@ -63,9 +63,11 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
 }
 
 int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,
-                     cudaStream_t s) {
-  return tp.variant == 5 ? r5::launch_tile_pass(amps, n, tp, dev_payload, s)
-                         : r4::launch_tile_pass(amps, n, tp, dev_payload, s);
+                     cudaStream_t s, int max_ctas, unsigned long long* ctr, uint64_t fmask,
+                     uint64_t fval) {
+  return tp.variant == 5
+             ? r5::launch_tile_pass(amps, n, tp, dev_payload, s, max_ctas, ctr, fmask, fval)
+             : r4::launch_tile_pass(amps, n, tp, dev_payload, s, max_ctas, ctr, fmask, fval);
 }
 
 }  // namespace qsv

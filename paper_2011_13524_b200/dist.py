@@ -45,6 +45,14 @@ from ._circuit import default_plan_opts
 from ._lib import check, lib
 
 
+# tile-engine constants the overlap planner respects (qsv_tile.cuh /
+# qsv_tile_impl.cuh: kLowQubits are in every tile, tiles hold kMaxTileQubits
+# qubits, dense blocks up to QSV_TILE_MAX_DENSE targets run inside tiles)
+_LOW_QUBITS = 4
+_TILE_QUBITS = 12
+_TILE_MAX_DENSE = 4
+
+
 # --------------------------------------------------------------------- records
 def _bit(x, q):
     return (x >> q) & 1
@@ -139,6 +147,31 @@ def specialize(rec, phys, L, rank):
     raise ValueError(kind)
 
 
+def _specialize_all(records, phys, L, rank):
+    out = []
+    for rec in records:
+        loc = specialize(rec, phys, L, rank)
+        if loc is None:
+            continue
+        if isinstance(loc, list):
+            out.extend(loc)
+        else:
+            out.append(loc)
+    return out
+
+
+def _tileable(rec):
+    """Does the record always run inside a tile pass (qsv_tile_impl.cuh
+    active_qubits: dense blocks up to 4 targets, diagonals up to 4,
+    uncontrolled Pauli products; controlled Paulis run as dense)?"""
+    kind = rec[0]
+    if kind in ("dense", "diag"):
+        return len(rec[1]) <= _TILE_MAX_DENSE
+    if rec[-1]:
+        return len(rec[1]) <= _TILE_MAX_DENSE
+    return True
+
+
 def active_qubits(rec):
     """Logical qubits that must be local for the record to run."""
     kind = rec[0]
@@ -221,19 +254,77 @@ class CudaShard:
         return self.state.get_vector()
 
     def apply_records(self, records):
+        self.run(self.prepare(records))
+
+    def prepare(self, records, outer_mask=0):
+        """Compile records into a runnable (a libqsv program; the payload is
+        uploaded here, so nothing synchronous is left for ``run``).  With
+        ``outer_mask`` the planner keeps those qubits out of every tile, so
+        the program can run block by block (``run_block``)."""
         if not records:
-            return
+            return None
         if not self._plan.use_tiles and not self._plan.fuse:
-            for rec in records:  # per-gate mode: one kernel per gate, no program
+            return ("direct", list(records))  # per-gate mode: one kernel per gate
+        ops, keep = records_to_ops(records)
+        opts = _lib.QsvPlanOpts.from_buffer_copy(self._plan)
+        opts.outer_mask = int(outer_mask)
+        h = C.c_void_p()
+        check(lib.qsv_program_create(self.L, ops, len(records), C.byref(opts), C.byref(h)))
+        return ("program", h)
+
+    def run(self, prepared):
+        """Enqueue a ``prepare`` result on the shard's stream (consumes it)."""
+        if prepared is None:
+            return
+        kind, obj = prepared
+        if kind == "direct":
+            for rec in obj:
                 self._apply_direct(rec)
             return
-        ops, keep = records_to_ops(records)
-        h = C.c_void_p()
-        check(lib.qsv_program_create(self.L, ops, len(records), C.byref(self._plan), C.byref(h)))
         try:
-            check(lib.qsv_program_run(h, self.state._handle()))
+            check(lib.qsv_program_run(obj, self.state._handle()))
         finally:
-            lib.qsv_program_destroy(h)
+            lib.qsv_program_destroy(obj)
+
+    @staticmethod
+    def blockwise(prepared):
+        """Can ``prepared`` run block by block (tile passes only)?"""
+        if prepared is None:
+            return True
+        if prepared[0] != "program":
+            return False
+        st = _lib.QsvProgramStats()
+        check(lib.qsv_program_stats_get(prepared[1], C.byref(st)))
+        return st.num_gate_kernels == 0
+
+    def run_block(self, prepared, mask, value, stream_ptr=None):
+        """Enqueue ``prepared`` on the amplitudes whose ``mask`` bits equal
+        ``value`` only (qsv_program_run_fixed), on ``stream_ptr`` through a
+        second handle on the same buffer (does not consume ``prepared``)."""
+        if prepared is None:
+            return
+        h = self.state._handle()
+        if stream_ptr is not None:
+            h = self._side_handle(stream_ptr)._handle()
+        check(lib.qsv_program_run_fixed(prepared[1], h, int(mask), int(value)))
+
+    def discard(self, prepared):
+        if prepared is not None and prepared[0] == "program":
+            lib.qsv_program_destroy(prepared[1])
+
+    def _side_handle(self, stream_ptr):
+        """A view of the whole shard whose work goes to another stream
+        (qsv_state_view), created once per stream."""
+        cache = self.__dict__.setdefault("_side", {})
+        v = cache.get(stream_ptr)
+        if v is None:
+            v = self.state._view(0, self.L)
+            v.set_stream(stream_ptr)
+            cache[stream_ptr] = v
+        return v
+
+    def set_sm_limit(self, sms):
+        self.state._set_sm_limit(sms)
 
     def _apply_direct(self, rec):
         from ._lib import int_array
@@ -324,7 +415,9 @@ class ShardedQuantumState:
     ``backend``: callable (L, rank) -> shard backend (default CudaShard)."""
 
     def __init__(self, num_qubits, world=None, rank=None, owned=None, backend=None,
-                 group=None, chunk_bytes=1 << 30, plan=None, exchange="auto"):
+                 group=None, chunk_bytes=1 << 30, plan=None, exchange="auto",
+                 overlap="auto", overlap_bits=2, overlap_sms=16, overlap_min_qubits=20,
+                 exchange_sms=0):
         import torch.distributed as dist
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
         if world is None:
@@ -343,10 +436,25 @@ class ShardedQuantumState:
         if exchange not in ("auto", "p2p", "nccl"):
             raise ValueError(f"unknown exchange mode {exchange!r}")
         self._stream = None
+        self._cstream = None  # compute stream of overlapped remaps (CUDA shards)
+        if overlap not in ("auto", True, False):
+            raise ValueError(f"overlap must be 'auto', True or False, got {overlap!r}")
+        # "auto": pipeline exchange steps with compute only when the exchange
+        # crosses GPUs (NVLink-bound).  Between virtual ranks on one GPU the
+        # swap runs at HBM speed on every SM and the extra tile pass a split
+        # segment costs outweighs what the overlap hides.
+        self.overlap = (len(self.owned) < world) if overlap == "auto" else overlap
+        self.overlap_bits = int(overlap_bits)
+        self.overlap_sms = int(overlap_sms)
+        self.overlap_min_qubits = int(overlap_min_qubits)
+        self.exchange_sms = int(exchange_sms)  # > 0: SM cap of non-overlapped swaps
+        self._num_sms = 0
         if backend is None:
             import torch
             dev = torch.cuda.current_device()
             self._stream = torch.cuda.current_stream()
+            self._cstream = torch.cuda.Stream()
+            self._num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
             stream = self._stream.cuda_stream
             plan = dict(plan or {})
             shared = exchange != "nccl" and len(self.owned) < world
@@ -558,22 +666,25 @@ class ShardedQuantumState:
         return steps
 
     def apply_records(self, records):
-        for step in self.plan(records):
+        steps = self.plan(records)
+        i = 0
+        while i < len(steps):
+            step = steps[i]
             if step[0] == "swap":
+                nxt = steps[i + 1] if i + 1 < len(steps) else None
+                ov = None
+                if nxt is not None and nxt[0] == "seg":
+                    ov = self._overlap_plan(step[1], step[2], nxt[1])
+                if ov is not None:
+                    self._remap_overlapped(step[1], step[2], nxt[1], *ov)
+                    i += 2
+                    continue
                 self._remap(step[1], step[2])
             else:
                 self.stats["segments"] += 1
                 for r, s in self.shards.items():
-                    local = []
-                    for rec in step[1]:
-                        out = specialize(rec, self.phys, self.L, r)
-                        if out is None:
-                            continue
-                        if isinstance(out, list):
-                            local.extend(out)
-                        else:
-                            local.append(out)
-                    s.apply_records(local)
+                    s.apply_records(_specialize_all(step[1], self.phys, self.L, r))
+            i += 1
 
     def update_quantum_state(self, circuit):
         from ._circuit import circuit_records
@@ -672,6 +783,9 @@ class ShardedQuantumState:
         slices, so only the step as a whole is fenced by device barriers."""
         L, k = self.L, len(gs)
         count = 1 << (L - k)
+        if self.exchange_sms:
+            for sh in self.shards.values():
+                sh.set_sm_limit(self.exchange_sms)
         self._device_barrier()
         for s in range(1, 1 << k):
             m = 0
@@ -690,6 +804,137 @@ class ShardedQuantumState:
                     self.shards[r].slice_swap(self._peer_ptr[partner], ls, dm, dp, j0, j1)
                 self.stats["bytes_sent"] += 16 << (L - k)
         self._device_barrier()
+        if self.exchange_sms:
+            for sh in self.shards.values():
+                sh.set_sm_limit(0)
+
+    # -- exchange / compute overlap ----------------------------------------
+    def _overlap_plan(self, gs, ls, seg):
+        """Can the exchange step (gs, ls) overlap the segment that follows?
+
+        A remap rewrites only bits gs and ls of an amplitude's address, so
+        fixing c other local qubits C splits every shard into 2^c blocks that
+        are exchanged independently.  The segment's prefix that acts
+        non-diagonally only off C runs block by block (C kept out of every
+        tile: diagonals and controls on C are tile constants), so block j
+        computes while block j+1 is still being exchanged.  C = the local
+        qubits (not 0..3, which every tile holds) whose first non-diagonal
+        use in the segment comes last.  Returns (C, phys after the remap,
+        prefix length) or None."""
+        if not self.overlap or self.exchange != "p2p":
+            return None
+        if not all(hasattr(s, "run_block") for s in self.shards.values()):
+            return None
+        L, c = self.L, self.overlap_bits
+        if c < 1 or L < self.overlap_min_qubits or L - c < _TILE_QUBITS + 1:
+            return None
+        inv = self._logical_of()
+        phys = list(self.phys)
+        for g, lp in zip(gs, ls):
+            qg, ql = inv[g], inv[lp]
+            phys[qg], phys[ql] = lp, g
+        first = {p: len(seg) for p in range(_LOW_QUBITS, L) if p not in ls}
+        for i, rec in enumerate(seg):
+            if not _tileable(rec):
+                # every block-wise step must be a tile pass; the cut is
+                # rank-independent (each rank runs the same exchange steps)
+                for p in first:
+                    first[p] = min(first[p], i)
+                break
+            for q in active_qubits(rec):
+                p = phys[q]
+                if p in first and first[p] > i:
+                    first[p] = i
+        if len(first) < c:
+            return None
+        order = sorted(first, key=lambda p: (first[p], p), reverse=True)
+        blk = sorted(order[:c])
+        prefix = min(first[p] for p in blk)
+        if prefix == 0:
+            return None
+        return blk, phys, prefix
+
+    def _mark(self, label, stream):
+        """Timeline probe (profiles/time_overlap.py --trace): a CUDA event on
+        ``stream`` when ``self.trace`` is a list."""
+        if getattr(self, "trace", None) is None or stream is None:
+            return
+        import torch
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        self.trace.append((label, ev))
+
+    def _remap_overlapped(self, gs, ls, seg, blk, phys, prefix):
+        """Exchange step + the following segment, pipelined over the 2^c
+        blocks of ``_overlap_plan``: the exchange of block j runs on the shard
+        stream (``overlap_sms`` one-CTA-per-SM swap kernels) while the
+        segment prefix runs on block j-1 on the compute stream; tile passes
+        take tiles from a work counter, so they use every SM the swap does
+        not hold and the rest as soon as it finishes.  A device barrier
+        after each block's exchange (all ranks' halves done) releases its
+        compute.  Everything is compiled before anything is enqueued; a
+        prefix that is not all tile passes falls back to the plain step."""
+        L, k, c = self.L, len(gs), len(blk)
+        pre, post = seg[:prefix], seg[prefix:]
+        bmask = sum(1 << p for p in blk)
+        progs = {r: s.prepare(_specialize_all(pre, phys, L, r), outer_mask=bmask)
+                 for r, s in self.shards.items()}
+        if not all(s.blockwise(progs[r]) for r, s in self.shards.items()):
+            raise RuntimeError("overlapped segment prefix compiled to per-gate kernels")
+        rest = {r: s.prepare(_specialize_all(post, phys, L, r)) for r, s in self.shards.items()}
+
+        def gbits(r):
+            return sum(((r >> (g - L)) & 1) << j for j, g in enumerate(gs))
+
+        ls_c = list(ls) + list(blk)
+        count = 1 << (L - k - c)
+        cptr = self._cstream.cuda_stream if self._cstream is not None else None
+        if self._cstream is not None:
+            self._cstream.wait_stream(self._stream)  # after everything queued so far
+        for s in self.shards.values():
+            s.set_sm_limit(self.overlap_sms if self._num_sms else 0)
+        self._device_barrier()
+        self._mark("start", self._stream)
+        for j in range(1 << c):
+            value = sum(((j >> b) & 1) << p for b, p in enumerate(blk))
+            for s_ in range(1, 1 << k):
+                m = 0
+                for b in range(k):
+                    if (s_ >> b) & 1:
+                        m |= 1 << (gs[b] - L)
+                for r in self.owned:
+                    partner = r ^ m
+                    dm, dp = gbits(partner) | (j << k), gbits(r) | (j << k)
+                    if partner in self.shards:
+                        if r < partner:
+                            self.shards[r].slice_swap(self.shards[partner].ptr(), ls_c, dm, dp,
+                                                      0, count)
+                    else:
+                        half = count // 2
+                        j0, j1 = (0, half) if r < partner else (half, count)
+                        self.shards[r].slice_swap(self._peer_ptr[partner], ls_c, dm, dp, j0, j1)
+                    self.stats["bytes_sent"] += 16 << (L - k - c)
+            self._device_barrier()
+            self._mark(f"swapped{j}", self._stream)
+            if self._cstream is not None:
+                self._cstream.wait_stream(self._stream)
+            for r, s in self.shards.items():
+                s.run_block(progs[r], bmask, value, cptr)
+            self._mark(f"computed{j}", self._cstream)
+        if self._cstream is not None:
+            self._stream.wait_stream(self._cstream)
+        for r, s in self.shards.items():
+            s.set_sm_limit(0)
+            s.discard(progs[r])
+        self.phys = phys
+        self.stats["swaps"] += 1
+        self.stats["remapped_qubits"] = self.stats.get("remapped_qubits", 0) + k
+        self.stats["overlapped"] = self.stats.get("overlapped", 0) + 1
+        self.stats["overlapped_gates"] = self.stats.get("overlapped_gates", 0) + prefix
+        self.stats["segments"] += 1
+        for r, s in self.shards.items():
+            s.run(rest[r])
+        self._mark("end", self._stream)
 
     def _swap(self, g, l):
         """Exchange physical global qubit g with local qubit l."""

@@ -33,6 +33,13 @@ class OracleShard:
     def apply_records(self, records):
         orc.run_records(self.a, self.L, records)
 
+    def prepare(self, records, outer_mask=0):
+        return list(records)
+
+    def run(self, records):
+        if records:
+            orc.run_records(self.a, self.L, records)
+
     def norm2(self):
         return orc.squared_norm(self.a)
 
@@ -106,6 +113,26 @@ class SharedOracleShard(OracleShard):
         tmp = self.a[j | va].copy()
         self.a[j | va] = b[j | vb]
         b[j | vb] = tmp
+
+    @staticmethod
+    def blockwise(prepared):
+        return True
+
+    def run_block(self, records, mask, value, stream_ptr=None):
+        """The records on the block {x : x & mask == value} only (they do not
+        mix blocks): applied to a copy, the block copied back."""
+        if not records:
+            return
+        idx = np.nonzero((np.arange(1 << self.L) & mask) == value)[0]
+        tmp = self.a.copy()
+        orc.run_records(tmp, self.L, records)
+        self.a[idx] = tmp[idx]
+
+    def discard(self, prepared):
+        pass
+
+    def set_sm_limit(self, sms):
+        pass
 
     def release(self):
         _BUFS.pop(self.key, None)

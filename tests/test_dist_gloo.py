@@ -89,14 +89,15 @@ def _worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-def _worker_p2p(rank, world, port, n, q):
+def _worker_p2p(rank, world, port, n, q, overlap_min=20):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         recs = random_records(n, 40, seed=77)
-        st = ShardedQuantumState(n, backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p")
+        st = ShardedQuantumState(n, backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p",
+                                 overlap_min_qubits=overlap_min)
         st.load(orc.haar_state(n, 5))
         st.apply_records(recs)
         vec = st.get_vector()
@@ -111,17 +112,20 @@ def _worker_p2p(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_gloo_processes_p2p_protocol(world):
+@pytest.mark.parametrize("world,overlap_min", [(2, 20), (4, 20), (2, 2), (4, 2)])
+def test_gloo_processes_p2p_protocol(world, overlap_min):
     """The peer-memory exchange protocol (dist.ShardedQuantumState
     exchange="p2p": mapped peer shards, each owner swapping half of every
     pair's slice, barriers around the step) across processes, with shared
-    memory standing in for CUDA IPC."""
-    n = 7
+    memory standing in for CUDA IPC.  overlap_min=2: exchange steps are
+    pipelined block by block with the following segment (barrier per
+    block; 17 qubits, so that a shard leaves block qubits besides a tile)."""
+    n = 7 if overlap_min >= 20 else 17
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_p2p, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker_p2p, args=(r, world, port, n, q, overlap_min))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
@@ -135,6 +139,7 @@ def test_gloo_processes_p2p_protocol(world):
         assert np.max(np.abs(vec - ref)) <= 1e-12, rank
         assert abs(e - e_ref) <= 1e-11
         assert stats["swaps"] > 0
+        assert (stats.get("overlapped", 0) > 0) == (overlap_min < 20)
 
 
 @pytest.mark.parametrize("world", [2, 8])
@@ -150,6 +155,67 @@ def test_virtual_ranks_p2p_protocol(world):
     for s in st.shards.values():
         s.release()
     assert np.max(np.abs(got - _reference(n, recs, 2))) <= 1e-12
+
+
+@pytest.mark.parametrize("world,bits", [(2, 1), (2, 2), (4, 2), (8, 1)])
+def test_virtual_ranks_overlapped_remaps(world, bits):
+    """Exchange steps pipelined with the segment that follows (block by
+    block over 2^bits blocks) give the oracle's state, for random mixed
+    records and for the cz-ladder (long overlappable prefixes).  Shards keep
+    a 12-qubit tile besides the block qubits."""
+    n = 14 + bits + world.bit_length() - 1
+    for recs, seed in ((random_records(n, 80, seed=world + bits), 4),
+                       (orc.cz_ladder_records(n, 6, seed=2), None)):
+        st = ShardedQuantumState(n, world=world, owned=list(range(world)),
+                                 backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p",
+                                 overlap=True, overlap_bits=bits, overlap_min_qubits=2)
+        if seed is None:
+            st.set_zero_state()
+            ref = orc.run_records(orc.zero_state(n), n, recs)
+        else:
+            st.load(orc.haar_state(n, seed))
+            ref = _reference(n, recs, seed)
+        st.apply_records(recs)
+        got = st.get_vector()
+        for s in st.shards.values():
+            s.release()
+        assert st.stats.get("overlapped", 0) > 0
+        assert np.max(np.abs(got - ref)) <= 1e-12
+
+
+def test_overlap_plan_blocks_and_prefix():
+    """The block qubits are the local qubits (not 0..3, not exchanged) whose
+    first non-diagonal use comes last; the prefix stops at the first gate
+    acting non-diagonally on one of them."""
+    n, world = 16, 2  # L = 15
+    st = ShardedQuantumState(n, world=world, owned=[0, 1],
+                             backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p",
+                             overlap=True, overlap_bits=2, overlap_min_qubits=2)
+    h = np.array([[1, 1], [1, -1]]) / np.sqrt(2)
+    seg = [("dense", (15,), h, ())] + [("dense", (q,), h, ()) for q in range(14, -1, -1)]
+    seg.insert(3, ("diag", (6,), np.array([1, 1j]), ()))
+    # logical 15 (global) swaps with physical 3: H on 15, 14, 13, diag, 12, ...
+    blk, phys, prefix = st._overlap_plan([15], [3], seg)
+    assert phys[15] == 3 and phys[3] == 15
+    # positions 4 and 5 are used last (the H on qubit 3 acts on the global slot)
+    assert blk == [4, 5] and prefix == seg.index(("dense", (5,), h, ()))
+    assert st._overlap_plan([15], [3], seg[:1]) == ([13, 14], phys, 1)
+    st.overlap = False
+    assert st._overlap_plan([15], [3], seg) is None
+    for s in st.shards.values():
+        s.release()
+
+
+def test_overlap_auto_only_across_processes():
+    """overlap="auto" pipelines exchange steps only when peers are remote."""
+    st = ShardedQuantumState(8, world=2, owned=[0, 1],
+                             backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p")
+    assert st.overlap is False
+    for s in st.shards.values():
+        s.release()
+    with pytest.raises(ValueError):
+        ShardedQuantumState(8, world=2, owned=[0, 1], backend=lambda L, r: OracleShard(L, r),
+                            overlap="yes")
 
 
 def test_exchange_mode_selection():
