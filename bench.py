@@ -550,6 +550,7 @@ def run_sharded_circuit(args, rank, world, dev, stream):
         s.set_random(97 + r)          # each shard normalised to 1 ...
         s.scale(1.0 / math.sqrt(vworld))  # ... so the whole state has norm 1
     model = plan_exchange_bytes(n, vworld, recs)
+    model_in_order = plan_exchange_bytes(n, vworld, recs, reorder=False)
     st.apply_records(recs)  # warm-up: programs compiled per segment
     torch.cuda.synchronize(dev)
     if dist.is_initialized():
@@ -577,6 +578,7 @@ def run_sharded_circuit(args, rank, world, dev, stream):
                         f"{'virtual ranks on one GPU' if virtual else 'GPUs'} "
                         f"(2^{L} amplitudes per rank)",
             "circuit_s": ms / 1e3, "norm_after": norm, "exchange_model": model,
+            "exchange_model_circuit_order": model_in_order,
             "nvlink_roofline_s": model["bytes_sent_per_rank"] / 900e9}
 
 

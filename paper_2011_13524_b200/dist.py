@@ -172,6 +172,11 @@ def _tileable(rec):
     return True
 
 
+def _touched_qubits(rec):
+    """Logical qubits a record reads or writes (targets and controls)."""
+    return set(rec[1]) | {q for q, _ in rec[-1]}
+
+
 def active_qubits(rec):
     """Logical qubits that must be local for the record to run."""
     kind = rec[0]
@@ -417,7 +422,7 @@ class ShardedQuantumState:
     def __init__(self, num_qubits, world=None, rank=None, owned=None, backend=None,
                  group=None, chunk_bytes=1 << 30, plan=None, exchange="auto",
                  overlap="auto", overlap_bits=2, overlap_sms=16, overlap_min_qubits=20,
-                 exchange_sms=0):
+                 exchange_sms=0, reorder=True):
         import torch.distributed as dist
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
         if world is None:
@@ -448,6 +453,7 @@ class ShardedQuantumState:
         self.overlap_sms = int(overlap_sms)
         self.overlap_min_qubits = int(overlap_min_qubits)
         self.exchange_sms = int(exchange_sms)  # > 0: SM cap of non-overlapped swaps
+        self.reorder = bool(reorder)  # segments run ahead past deferred gates (plan)
         self._num_sms = 0
         if backend is None:
             import torch
@@ -620,49 +626,67 @@ class ShardedQuantumState:
         """Split records into segments of local gates and qubit remaps.
 
         Returns a list of ("swap", [g_phys...], [l_phys...]) / ("seg",
-        [records]); pure function of the current map.  When a gate needs
-        global qubits, every other global qubit needed within the next
-        ``lookahead`` gates (default 2n) is brought local in the same remap
-        (one exchange step moving (1 - 2^-k) of the shard instead of k steps
-        moving half of it each); the local qubits that become global are the
-        ones whose next use is furthest away (Belady), high positions first."""
+        [records]); pure function of the current map.  A segment takes, in
+        order, every gate that needs no global qubit and shares no qubit with
+        a gate deferred before it (gates on disjoint qubits commute), so it
+        runs ahead on the qubits far from the global ones -- several layers
+        deep for a nearest-neighbour circuit, which lets the tile planner
+        pack as many gates per HBM pass as on a single GPU.  The deferred
+        gates form the next segment after a remap.  A remap brings local the
+        global qubits of the first deferred gate plus every global qubit the
+        deferred gates need within ``lookahead`` gates (default 2n), in one
+        exchange step (moving (1 - 2^-k) of the shard instead of k steps of
+        half of it); the local qubits that become global are the ones whose
+        next use is furthest away (Belady), high positions first.  With
+        ``reorder=False`` a segment ends at the first gate that needs a
+        global qubit (circuit order)."""
         phys = list(self.phys)
         L = self.L
         steps = []
-        seg = []
-        act = [active_qubits(r) for r in records]
         window = 2 * self.n if lookahead is None else int(lookahead)
+        reorder = getattr(self, "reorder", True)
+        remaining = list(records)
+        while remaining:
+            act = [active_qubits(r) for r in remaining]
+            seg, deferred, dact = [], [], []
+            blocked = set()
+            for rec, a in zip(remaining, act):
+                touched = _touched_qubits(rec)
+                if (deferred and not reorder) or touched & blocked or \
+                        any(phys[q] >= L for q in a):
+                    deferred.append(rec)
+                    dact.append(a)
+                    blocked |= touched
+                else:
+                    seg.append(rec)
+            if seg:
+                steps.append(("seg", seg))
+            if not deferred:
+                break
+            need = [q for q in dact[0] if phys[q] >= L]
 
-        def next_use(q, start):
-            for k in range(start, len(records)):
-                if q in act[k]:
-                    return k
-            return len(records) + (self.n - phys[q])  # never: prefer high phys
+            def next_use(q, start):
+                for k in range(start, len(deferred)):
+                    if q in dact[k]:
+                        return k
+                return len(deferred) + (self.n - phys[q])  # never: prefer high phys
 
-        for i, rec in enumerate(records):
-            need = [q for q in act[i] if phys[q] >= L]
-            if need:
-                if seg:
-                    steps.append(("seg", seg))
-                    seg = []
-                soon = sorted((next_use(q, i), q) for q in range(self.n)
-                              if phys[q] >= L and q not in need)
-                want = list(need) + [q for k, q in soon if k < i + window]
-                busy = set(act[i]) | set(want)
-                cands = [lq for lq in range(self.n) if phys[lq] < L and lq not in busy]
-                cands.sort(key=lambda lq: (next_use(lq, i + 1), phys[lq]), reverse=True)
-                if len(cands) < len(need):
-                    raise ValueError("gate needs more local qubits than the shard has")
-                want = want[:len(cands)]
-                victims = cands[:len(want)]
-                gs = [phys[q] for q in want]
-                ls = [phys[v] for v in victims]
-                steps.append(("swap", gs, ls))
-                for q, v, g, lp in zip(want, victims, gs, ls):
-                    phys[q], phys[v] = lp, g
-            seg.append(rec)
-        if seg:
-            steps.append(("seg", seg))
+            soon = sorted((next_use(q, 0), q) for q in range(self.n)
+                          if phys[q] >= L and q not in need)
+            want = list(need) + [q for k, q in soon if k < window]
+            busy = set(dact[0]) | set(want)
+            cands = [lq for lq in range(self.n) if phys[lq] < L and lq not in busy]
+            cands.sort(key=lambda lq: (next_use(lq, 1), phys[lq]), reverse=True)
+            if len(cands) < len(need):
+                raise ValueError("gate needs more local qubits than the shard has")
+            want = want[:len(cands)]
+            victims = cands[:len(want)]
+            gs = [phys[q] for q in want]
+            ls = [phys[v] for v in victims]
+            steps.append(("swap", gs, ls))
+            for q, v, g, lp in zip(want, victims, gs, ls):
+                phys[q], phys[v] = lp, g
+            remaining = deferred
         return steps
 
     def apply_records(self, records):
@@ -995,7 +1019,7 @@ class ShardedQuantumState:
             part.copy_(recv)
 
 
-def plan_exchange_bytes(num_qubits, world, records, lookahead=None):
+def plan_exchange_bytes(num_qubits, world, records, lookahead=None, reorder=True):
     """Host-only model of a sharded run (no shards allocated): number of
     remap steps, qubits remapped and NVLink bytes sent per rank, for the
     combined HBM + NVLink roofline."""
@@ -1003,6 +1027,7 @@ def plan_exchange_bytes(num_qubits, world, records, lookahead=None):
     p = int(round(math.log2(world)))
     eng.n, eng.p, eng.L = num_qubits, p, num_qubits - p
     eng.phys = list(range(num_qubits))
+    eng.reorder = reorder
     steps = eng.plan(records, lookahead)
     remaps = [s for s in steps if s[0] == "swap"]
     sent = sum((16 << eng.L) - (16 << (eng.L - len(s[1]))) for s in remaps)
