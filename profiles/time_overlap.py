@@ -27,7 +27,9 @@ from paper_2011_13524_b200.dist import ShardedQuantumState  # noqa: E402
 
 
 def run(n, recs, reps, **kw):
-    st = ShardedQuantumState(n, world=4, owned=[0, 1, 2, 3], **kw)
+    # circuit-order segments (reorder=False): an exchange step per layer, the
+    # regime the overlap is for (the run-ahead planner needs one remap here)
+    st = ShardedQuantumState(n, world=4, owned=[0, 1, 2, 3], reorder=False, **kw)
     for r, s in st.shards.items():
         s.set_random(97 + r)
         s.scale(0.5)
@@ -69,7 +71,7 @@ def main():
 
 def trace(n, recs, sms, bits):
     st = ShardedQuantumState(n, world=4, owned=[0, 1, 2, 3], overlap=True, overlap_bits=bits,
-                             overlap_sms=sms)
+                             overlap_sms=sms, reorder=False)
     for r, s in st.shards.items():
         s.set_random(97 + r)
         s.scale(0.5)
