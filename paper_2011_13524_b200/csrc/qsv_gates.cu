@@ -39,9 +39,21 @@ constexpr int kUnroll = 2;  // units per thread, loads issued before compute
 //   MODE 1 (TGT0):  target is bit 0, controls >= 1 -> unit = one pair held in
 //                   one 256-bit word.
 //   MODE 2 (SCALAR): a control sits on bit 0 -> 16-byte accesses.
+//   MODE 3 (PAIR):   a control sits on bit 0 -> the aligned 32-byte pairs are
+//                    read and written whole (default; see k_diag MODE 2).
 struct Mat2 {
   double2 m00, m01, m10, m11;
 };
+
+// QSV_DIAG_PAIR=0 selects the 16-byte paths for controls on bit 0 (A/B measurements)
+static bool diag_pair_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QSV_DIAG_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads)
@@ -93,6 +105,38 @@ __global__ void __launch_bounds__(kThreads)
         st2(a + idx[j], o);
       }
     }
+  } else if (MODE == 3) {
+    // control on bit 0: each side's aligned 32-byte pair is read and written
+    // whole (full-sector stores; the neighbour fails the control, so no other
+    // thread touches it)
+    Amp2 lo[kUnroll], hi[kUnroll];
+    uint64_t idx[kUnroll];
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) {
+      const uint64_t u = first + (uint64_t)j * kThreads;
+      if (u < units) {
+        idx[j] = widen(u, fb);
+        lo[j] = ld2(a + (idx[j] & ~1ULL));
+        hi[j] = ld2(a + (idx[j] & ~1ULL) + tbit);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) {
+      const uint64_t u = first + (uint64_t)j * kThreads;
+      if (u < units) {
+        if (idx[j] & 1) {
+          const double2 x = lo[j].b, y = hi[j].b;
+          lo[j].b = cfma(M.m01, y, cmul(M.m00, x));
+          hi[j].b = cfma(M.m11, y, cmul(M.m10, x));
+        } else {
+          const double2 x = lo[j].a, y = hi[j].a;
+          lo[j].a = cfma(M.m01, y, cmul(M.m00, x));
+          hi[j].a = cfma(M.m11, y, cmul(M.m10, x));
+        }
+        st2(a + (idx[j] & ~1ULL), lo[j]);
+        st2(a + (idx[j] & ~1ULL) + tbit, hi[j]);
+      }
+    }
   } else {
     double2 x[kUnroll], y[kUnroll];
     uint64_t idx[kUnroll];
@@ -120,7 +164,12 @@ __global__ void __launch_bounds__(kThreads)
 // Diagonal: psi_x *= d[sub(x)] over the amplitudes whose control bits match
 // (kernels.py:155-173).  The table lives in shared memory (m <= 8) or is read
 // through the read-only path (m > 8).  MODE 0: lowest fixed bit >= 1 (or no
-// controls) -> 256-bit accesses; MODE 1: control on bit 0 -> 16-byte.
+// controls) -> 256-bit accesses; MODE 1: control on bit 0, 16-byte accesses;
+// MODE 2: control on bit 0, the touched amplitude's aligned 32-byte pair is
+// read and written whole (the neighbour unchanged, and untouched by any other
+// thread since it fails the bit-0 control): a full-sector store instead of a
+// 16-byte partial write, which HBM serves as read-modify-write (CZ on qubits
+// 0 and 1).
 struct DiagSmall {
   double2 d[32];
 };
@@ -168,6 +217,27 @@ __global__ void __launch_bounds__(kThreads)
         o.a = cmul(v[j].a, lookup(sub_of(idx[j])));
         o.b = cmul(v[j].b, lookup(sub_of(idx[j] + 1)));
         st2(a + idx[j], o);
+      }
+    }
+  } else if (MODE == 2) {
+    Amp2 v[kUnroll];
+    uint64_t idx[kUnroll];
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) {
+      const uint64_t u = first + (uint64_t)j * kThreads;
+      if (u < units) {
+        idx[j] = widen(u, fb);
+        v[j] = ld2(a + (idx[j] & ~1ULL));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) {
+      const uint64_t u = first + (uint64_t)j * kThreads;
+      if (u < units) {
+        const double2 f = lookup(sub_of(idx[j]));
+        if (idx[j] & 1) v[j].b = cmul(v[j].b, f);
+        else v[j].a = cmul(v[j].a, f);
+        st2(a + (idx[j] & ~1ULL), v[j]);
       }
     }
   } else {
@@ -761,6 +831,8 @@ int launch_gate(double2* a, int n, const GateDesc& g0, const Cplx* dev_data, cud
     if (lowest_ctl >= 1 && cnt >= 2) {
       const uint64_t units = cnt / 2;
       k_diag<0><<<grid_for(units, kUnroll), kThreads, 0, s>>>(a, fb, g.m, small, big, tp, units);
+    } else if (lowest_ctl == 0 && dim >= 2 && diag_pair_mode()) {
+      k_diag<2><<<grid_for(cnt, kUnroll), kThreads, 0, s>>>(a, fb, g.m, small, big, tp, cnt);
     } else {
       k_diag<1><<<grid_for(cnt, kUnroll), kThreads, 0, s>>>(a, fb, g.m, small, big, tp, cnt);
     }
@@ -818,6 +890,8 @@ int launch_gate(double2* a, int n, const GateDesc& g0, const Cplx* dev_data, cud
       k_pair2x2<0><<<grid_for(units, kUnroll), kThreads, 0, s>>>(a, fb, tbit, M, units);
     } else if (t == 0) {
       k_pair2x2<1><<<grid_for(ncos, kUnroll), kThreads, 0, s>>>(a, fb, tbit, M, ncos);
+    } else if (diag_pair_mode()) {
+      k_pair2x2<3><<<grid_for(ncos, kUnroll), kThreads, 0, s>>>(a, fb, tbit, M, ncos);
     } else {
       k_pair2x2<2><<<grid_for(ncos, kUnroll), kThreads, 0, s>>>(a, fb, tbit, M, ncos);
     }

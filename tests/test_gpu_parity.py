@@ -208,6 +208,23 @@ def test_low_qubit_layouts():
             g.update_quantum_state(st)
             c_oracle.apply_record(ref, n, g._core.record())
             assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (c, t)
+    # controls on bit 0 with value 0 / 1 (the whole-32-byte-pair paths of
+    # k_pair2x2 MODE 3 and k_diag MODE 2), extra controls above
+    rng = np.random.default_rng(9)
+    for v in (0, 1):
+        for t in (1, 2, 7):
+            for mk in (lambda: qg.RandomUnitary([t], seed=t + v),
+                       lambda: qg.DiagonalMatrix([t], np.exp(1j * rng.uniform(0, 6, 2))),
+                       lambda: qg.DiagonalMatrix([t, 8], np.exp(1j * rng.uniform(0, 6, 4)))):
+                g = mk()
+                g.add_control_qubit(0, v)
+                if t == 7:
+                    g.add_control_qubit(3, 1 - v)
+                st = haar(n, 31 * t + v)
+                ref = orc.haar_state(n, 31 * t + v)
+                g.update_quantum_state(st)
+                c_oracle.apply_record(ref, n, g._core.record())
+                assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL, (v, t)
 
 
 def test_big_diagonal_and_pauli_products():
