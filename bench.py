@@ -354,6 +354,7 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     if rank == 0 and not args.skip_circuit:
         extra["random_circuit"] = run_random_circuit(args, dev, stream, qs, workloads, torch)
+        extra["per_gate_n30"] = run_per_gate_at(qs, torch, dev, stream, 30)
         extra["cfg1_cnot_ring"] = run_cfg1(qs, workloads, torch, dev, stream)
         extra["cfg3_vqe"] = run_cfg3(qs, workloads, torch, dev, stream)
         del st
@@ -728,6 +729,45 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
         "fp64_tflops_per_s": st5.get("fp64_flops", 0.0) / t5 / 1e12}
     del s5
     return out
+
+
+def run_per_gate_at(qs, torch, dev, stream, n=30, reps=2):
+    """The north star's per-gate target is quoted at 30 qubits: the same
+    H/RX/RZ/CNOT/CZ x every-target sweep at n (one warm-up pass, then reps
+    passes with CUDA events around every gate), GB/s per gate kind."""
+    gates = build_gates(n)
+    st = qs.QuantumState(n, device=dev)
+    st.set_stream(stream.cuda_stream)
+    st.set_random_state_device(77)
+    for _, _, g in gates:
+        g.update_quantum_state(st)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(reps * len(gates))]
+    torch.cuda.synchronize(dev)
+    i = 0
+    for _ in range(reps):
+        for _, _, g in gates:
+            ev[i][0].record(stream)
+            g.update_quantum_state(st)
+            ev[i][1].record(stream)
+            i += 1
+    torch.cuda.synchronize(dev)
+    per_kind = {k: [0.0, 0.0] for k in GATE_KINDS}
+    i = 0
+    for _ in range(reps):
+        for kind, _, _ in gates:
+            per_kind[kind][0] += ev[i][0].elapsed_time(ev[i][1])
+            per_kind[kind][1] += gate_bytes(kind, n)
+            i += 1
+    del st
+    peak, _ = measured_peaks()
+    out = {k: {"gbs": b / (ms / 1e3) / 1e9, "frac_of_peak": b / (ms / 1e3) / 1e9 / peak}
+           for k, (ms, b) in per_kind.items() if ms > 0}
+    tot_ms = sum(v[0] for v in per_kind.values())
+    tot_b = sum(v[1] for v in per_kind.values())
+    return {"qubits": n, "per_gate": out, "sweep_gbs": tot_b / (tot_ms / 1e3) / 1e9,
+            "sweep_frac_of_peak": tot_b / (tot_ms / 1e3) / 1e9 / peak,
+            "note": "touched-byte model (SURVEY 8(d)); device time per gate"}
 
 
 def run_cfg1(qs, workloads, torch, dev, stream, n=16, reps=20):

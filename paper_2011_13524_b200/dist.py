@@ -669,7 +669,7 @@ class ShardedQuantumState:
                 for k in range(start, len(deferred)):
                     if q in dact[k]:
                         return k
-                return len(deferred) + (self.n - phys[q])  # never: prefer high phys
+                return len(deferred) + 1 + phys[q]  # never used again: prefer high phys
 
             soon = sorted((next_use(q, 0), q) for q in range(self.n)
                           if phys[q] >= L and q not in need)
