@@ -27,22 +27,23 @@ namespace qsv {
 constexpr int kXTileQubits = 12;
 constexpr int kXThreads = 256;
 constexpr int kXPer = (1 << kXTileQubits) / kXThreads;  // amplitudes per thread (16)
-constexpr int kXMaxTerms = 64;                          // terms per pass
+constexpr int kXMaxTerms = 44;                          // terms per pass
 constexpr int kXWarps = kXThreads / 32;
+constexpr int kXTileAmps = 1 << kXTileQubits;
 
 struct XGroup {
   uint32_t xl;     // flip mask over the tile's local bits
   int32_t first;   // first term of the group
   int32_t count;
-  int32_t pad;
+  int32_t hb;      // pairing bit (highest bit of xl; -1 for xl == 0)
 };
 
 struct XTerm {
   uint32_t zl;     // sign mask over local bits
-  uint32_t kmask;  // bit k: parity of ((k * 256) ^ xl) & zl over the k-indexed local bits
-                   // (bits 8..11) and of the flip mask's low bits: the per-amplitude
-                   // sign is bit k of kmask ^ parity(tid & zl_lo & ~...) (see kernel)
+  uint32_t zk;     // its k part: bits 8..11 of zl (sign (-1)^popc(k & zk) over slot k)
   uint64_t zg;     // sign mask over the other (tile-constant) bits
+  uint32_t imag;   // parity(xl & zl): the pair sums are imaginary (and carry a - sign)
+  uint32_t pad;
 };
 
 struct XPass {
@@ -52,13 +53,84 @@ struct XPass {
   XTerm terms[kXMaxTerms];
 };
 
-__global__ void __launch_bounds__(kXThreads, 2)
+// dynamic shared memory: two tile buffers (the next tile streams in with
+// cp.async while this one is evaluated) + one accumulator per (term, thread);
+// a term's sum is purely real or purely imaginary (XTerm::imag), one double
+constexpr size_t kXSmemBytes =
+    2 * sizeof(double2) * kXTileAmps + sizeof(double) * kXMaxTerms * kXThreads;
+static_assert(kXSmemBytes + sizeof(XPass) + 1024 <= 232448, "expectation tile smem");
+
+// sum_k (-1)^popc(k & z) x[k] over 16 slots: four uniform-branch folds,
+// 15 additions of depth 4
+__device__ __forceinline__ double fold16(const double (&x)[16], uint32_t z) {
+  double a[8], b[4], c[2];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = (z & 8) ? x[k] - x[k + 8] : x[k] + x[k + 8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) b[k] = (z & 4) ? a[k] - a[k + 4] : a[k] + a[k + 4];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) c[k] = (z & 2) ? b[k] - b[k + 2] : b[k] + b[k + 2];
+  return (z & 1) ? c[0] - c[1] : c[0] + c[1];
+}
+
+// in-place 16-point Walsh-Hadamard transform: x[z] = sum_k (-1)^popc(k & z) x[k]
+__device__ __forceinline__ void wht16(double (&x)[16]) {
+#pragma unroll
+  for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (!(k & h)) {
+        const double u = x[k], w = x[k + h];
+        x[k] = u + w;
+        x[k + h] = u - w;
+      }
+}
+
+__device__ __forceinline__ double pick16(const double (&x)[16], uint32_t z) {
+  switch (z & 15u) {
+    case 0: return x[0];
+    case 1: return x[1];
+    case 2: return x[2];
+    case 3: return x[3];
+    case 4: return x[4];
+    case 5: return x[5];
+    case 6: return x[6];
+    case 7: return x[7];
+    case 8: return x[8];
+    case 9: return x[9];
+    case 10: return x[10];
+    case 11: return x[11];
+    case 12: return x[12];
+    case 13: return x[13];
+    case 14: return x[14];
+    default: return x[15];
+  }
+}
+
+__device__ __forceinline__ void x_cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void x_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void x_cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// S_t = sum_x conj(psi_x) psi_{x ^ xl} (-1)^popc((x ^ xl) & zl) over the tile,
+// accumulated per thread across all of the CTA's tiles (one shared-memory
+// read-modify-write per term and tile instead of a warp reduction), reduced
+// once at the end.  For xl != 0 the pairs x, x ^ xl contribute
+// sigma(x ^ xl) (p + c conj p) with p = conj(psi_x) psi_{x ^ xl} and
+// c = (-1)^popc(xl & zl): 2 Re p or 2i Im p, so only the half of the tile with
+// bit hb = 0 is visited and only the needed part of p is formed.
+__global__ void __launch_bounds__(kXThreads, 1)
     k_expect_tile(const double2* __restrict__ a, const XPass* __restrict__ gp, FixedBits tb,
                   uint64_t ntiles, double* __restrict__ partials) {
-  extern __shared__ double2 sm[];  // 2^12 amplitudes (64 KiB, dynamic)
+  extern __shared__ double2 xdyn[];
+  double* acc = reinterpret_cast<double*>(xdyn + 2 * kXTileAmps);  // [term][thread]
   __shared__ XPass P;
   __shared__ uint64_t s_hi[kXPer];
-  __shared__ double2 s_acc[kXWarps][kXMaxTerms];
+  __shared__ double s_red[kXWarps];
   {
     const int* src = reinterpret_cast<const int*>(gp);
     int* dst = reinterpret_cast<int*>(&P);
@@ -72,64 +144,109 @@ __global__ void __launch_bounds__(kXThreads, 2)
       if ((tid >> b) & 1) h |= 1ULL << P.spos[8 + b];
     s_hi[tid] = h;
   }
-  for (int i = tid; i < kXWarps * kXMaxTerms; i += kXThreads)
-    s_acc[i / kXMaxTerms][i % kXMaxTerms] = make_double2(0.0, 0.0);
+  for (int t = 0; t < P.nterms; ++t) acc[t * kXThreads + tid] = 0.0;
   uint64_t lo = 0;
   for (int b = 0; b < 8; ++b)
     if ((tid >> b) & 1) lo |= 1ULL << P.spos[b];
+  // thread part of every term's sign, tile-invariant
+  uint64_t tsg = 0;
+  for (int t = 0; t < P.nterms; ++t)
+    tsg |= (uint64_t)(__popc((uint32_t)tid & P.terms[t].zl & 0xffu) & 1) << t;
   __syncthreads();
 
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  auto issue = [&](uint64_t tile, int buf) {
     const uint64_t base = widen(tile, tb);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(xdyn + buf * kXTileAmps);
 #pragma unroll
-    for (int k = 0; k < kXPer; ++k) sm[k * kXThreads + tid] = ld1(a + (base | lo | s_hi[k]));
+    for (int k = 0; k < kXPer; ++k)
+      x_cp_async16(sb + (uint32_t)(k * kXThreads + tid) * 16u, a + (base | lo | s_hi[k]));
+    x_cp_commit();
+  };
+  uint64_t tile = blockIdx.x;
+  int buf = 0;
+  if (tile < ntiles) issue(tile, 0);
+  for (; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+    const uint64_t next = tile + gridDim.x;
+    if (next < ntiles) {
+      issue(next, buf ^ 1);
+      x_cp_wait<1>();
+    } else {
+      x_cp_wait<0>();
+    }
     __syncthreads();
-    double2 v[kXPer];  // this thread's amplitudes, shared by every group
+    const double2* sm = xdyn + buf * kXTileAmps;
+    const uint64_t base = widen(tile, tb);
+    double2 v[kXPer];
 #pragma unroll
     for (int k = 0; k < kXPer; ++k) v[k] = sm[k * kXThreads + tid];
     for (int g = 0; g < P.ngroups; ++g) {
-      const uint32_t xl = P.groups[g].xl;
-      double2 p[kXPer];
-#pragma unroll
-      for (int k = 0; k < kXPer; ++k) {
-        const double2 w = xl ? sm[(uint32_t)(k * kXThreads + tid) ^ xl] : v[k];
-        p[k] = make_double2(fma(v[k].x, w.x, v[k].y * w.y), fma(v[k].x, w.y, -v[k].y * w.x));
-      }
-      const int t1 = P.groups[g].first + P.groups[g].count;
-      for (int t = P.groups[g].first; t < t1; ++t) {
-        const XTerm T = P.terms[t];
-        // sign of x ^ xl for x = k * 256 + tid: tile part, thread part, k part
-        const uint32_t tpar =
-            (uint32_t)((__popcll(base & T.zg) ^ __popc((uint32_t)tid & T.zl & 0xffu)) & 1);
-        const uint32_t M = T.kmask ^ (0u - tpar);
-        double2 acc = make_double2(0.0, 0.0);
+      const XGroup G = P.groups[g];
+      const int t1 = G.first + G.count;
+      double re[kXPer], im[kXPer];
+      uint32_t own = 0xffffu;  // k slots this thread visits
+      double f = 1.0;
+      if (G.xl == 0) {
 #pragma unroll
         for (int k = 0; k < kXPer; ++k) {
-          const bool neg = (M >> k) & 1u;
-          acc.x += neg ? -p[k].x : p[k].x;
-          acc.y += neg ? -p[k].y : p[k].y;
+          re[k] = fma(v[k].x, v[k].x, v[k].y * v[k].y);
+          im[k] = 0.0;
+        }
+      } else {
+        f = 2.0;
+        if (G.hb >= 8) {
+          const int kb = G.hb - 8;
+          own = 0;
+#pragma unroll
+          for (int k = 0; k < kXPer; ++k)
+            if (!((k >> kb) & 1)) own |= 1u << k;
+        } else if ((tid >> G.hb) & 1) {
+          continue;  // the partner thread covers these pairs
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-        }
-        if (lane == 0) {
-          s_acc[warp][t].x += acc.x;
-          s_acc[warp][t].y += acc.y;
+        for (int k = 0; k < kXPer; ++k) {
+          if (!((own >> k) & 1)) {
+            re[k] = im[k] = 0.0;
+            continue;
+          }
+          const double2 w = sm[(uint32_t)(k * kXThreads + tid) ^ G.xl];
+          re[k] = fma(v[k].x, w.x, v[k].y * w.y);
+          im[k] = fma(v[k].x, w.y, -v[k].y * w.x);
         }
       }
+      // a slot sign pattern (-1)^popc(k & zk) is one Walsh-Hadamard
+      // coefficient: groups with many terms transform once and pick, small
+      // groups fold per term
+      const bool many = G.count >= 4;
+      if (many) {
+        wht16(re);
+        if (G.xl) wht16(im);
+      }
+      for (int t = G.first; t < t1; ++t) {
+        const XTerm T = P.terms[t];
+        const uint32_t neg = (uint32_t)((__popcll(base & T.zg) ^ (tsg >> t) ^ T.imag) & 1);
+        double val;
+        if (many) val = T.imag ? pick16(im, T.zk) : pick16(re, T.zk);
+        else val = T.imag ? fold16(im, T.zk) : fold16(re, T.zk);
+        acc[t * kXThreads + tid] = fma(neg ? -f : f, val, acc[t * kXThreads + tid]);
+      }
     }
-    __syncthreads();  // the tile buffer is refilled next iteration
+    __syncthreads();  // this buffer is refilled by the prefetch two tiles on
   }
-  if (tid < P.nterms) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int w = 0; w < kXWarps; ++w) {
-      s.x += s_acc[w][tid].x;
-      s.y += s_acc[w][tid].y;
+  // per term: fixed-order block sum of the per-thread accumulators
+  for (int t = 0; t < P.nterms; ++t) {
+    double s = acc[t * kXThreads + tid];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) s_red[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double r = 0.0;
+      for (int w = 0; w < kXWarps; ++w) r += s_red[w];
+      const bool imag = P.terms[t].imag;
+      partials[((size_t)blockIdx.x * kXMaxTerms + t) * 2 + 0] = imag ? 0.0 : r;
+      partials[((size_t)blockIdx.x * kXMaxTerms + t) * 2 + 1] = imag ? r : 0.0;
     }
-    partials[((size_t)blockIdx.x * kXMaxTerms + tid) * 2 + 0] = s.x;
-    partials[((size_t)blockIdx.x * kXMaxTerms + tid) * 2 + 1] = s.y;
+    __syncthreads();
   }
 }
 
@@ -166,37 +283,47 @@ struct XTermIn {
 };
 
 // Pack terms into passes: each pass is a tile set of 12 qubits (0..3 plus
-// flip qubits) and at most kXMaxTerms terms.  Returns false if some flip mask
-// does not fit a tile (the caller then uses the sweep kernels).
+// flip qubits) and at most kXMaxTerms terms; a flip mask with more terms is
+// split into chunks.  Returns false if some flip mask does not fit a tile
+// (the caller then uses the sweep kernels).
 static bool pack_passes(int n, const std::vector<XTermIn>& terms,
                         std::vector<std::pair<uint64_t, std::vector<int>>>& passes) {
   if (n < kXTileQubits) return false;
   const uint64_t low = 0xFULL;
-  // distinct flip masks in first-appearance order
+  // units: (flip mask, up to kXMaxTerms of its terms), masks in first-appearance order
   std::vector<uint64_t> masks;
   for (const XTermIn& t : terms)
     if (std::find(masks.begin(), masks.end(), t.xm) == masks.end()) masks.push_back(t.xm);
-  for (uint64_t m : masks)
+  std::vector<std::pair<uint64_t, std::vector<int>>> units;
+  for (uint64_t m : masks) {
     if (__builtin_popcountll(m | low) > kXTileQubits) return false;
-  std::vector<char> done(masks.size(), 0);
-  size_t left = masks.size();
+    std::vector<int> chunk;
+    for (size_t k = 0; k < terms.size(); ++k) {
+      if (terms[k].xm != m) continue;
+      chunk.push_back((int)k);
+      if ((int)chunk.size() == kXMaxTerms) {
+        units.push_back({m, chunk});
+        chunk.clear();
+      }
+    }
+    if (!chunk.empty()) units.push_back({m, chunk});
+  }
+  std::vector<char> done(units.size(), 0);
+  size_t left = units.size();
   while (left) {
     uint64_t S = low;
     std::vector<int> members;
     int nterms = 0;
-    for (size_t i = 0; i < masks.size(); ++i) {
+    for (size_t i = 0; i < units.size(); ++i) {
       if (done[i]) continue;
-      if (__builtin_popcountll(S | masks[i]) > kXTileQubits) continue;
-      int cnt = 0;
-      for (const XTermIn& t : terms) cnt += t.xm == masks[i];
-      if (nterms + cnt > kXMaxTerms && nterms > 0) continue;
-      if (cnt > kXMaxTerms) return false;
-      S |= masks[i];
+      if (__builtin_popcountll(S | units[i].first) > kXTileQubits) continue;
+      const int cnt = (int)units[i].second.size();
+      if (nterms + cnt > kXMaxTerms) continue;
+      S |= units[i].first;
       nterms += cnt;
       done[i] = 1;
       --left;
-      for (size_t k = 0; k < terms.size(); ++k)
-        if (terms[k].xm == masks[i]) members.push_back((int)k);
+      members.insert(members.end(), units[i].second.begin(), units[i].second.end());
     }
     // pad S with the lowest unused qubits
     for (int q = 0; q < n && __builtin_popcountll(S) < kXTileQubits; ++q) S |= 1ULL << q;
@@ -231,7 +358,7 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
     if (num_sms <= 0) num_sms = 148;
   }
   const uint64_t ntiles = 1ULL << (n - kXTileQubits);
-  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)std::min(num_sms * 2, 296));
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)std::min(num_sms, 296));
   char* base = reinterpret_cast<char*>(scratch);
   XPass* dpass0 = reinterpret_cast<XPass*>(base);
   double* partials = reinterpret_cast<double*>(base + ((sizeof(XPass) * kXBatch + 255) / 256) * 256);
@@ -282,27 +409,23 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
       XGroup G;
       G.first = (int32_t)order.size();
       G.count = 0;
-      G.pad = 0;
       G.xl = 0;
       for (int q = 0; q < n; ++q)
         if ((m >> q) & 1ULL) G.xl |= 1u << local_of[q];
+      G.hb = G.xl ? 31 - __builtin_clz(G.xl) : -1;
       for (int k : ps.second)
         if (terms[k].xm == m) {
           XTerm T;
-          T.zl = 0;
-          T.kmask = 0;
-          T.zg = 0;
+          memset(&T, 0, sizeof(T));
           for (int q = 0; q < n; ++q)
             if ((terms[k].zm >> q) & 1ULL) {
               if (local_of[q] >= 0) T.zl |= 1u << local_of[q];
               else T.zg |= 1ULL << q;
             }
-          // parity((x ^ xl) & zl) = parity(tid & zl & 0xff) ^ parity((k << 8) & zl)
+          // parity((x ^ xl) & zl) = parity(tid & zl & 0xff) ^ parity(k & zk)
           //                          ^ parity(xl & zl)
-          for (int kk = 0; kk < kXPer; ++kk)
-            if ((__builtin_popcount(((uint32_t)kk << 8) & T.zl) ^
-                 __builtin_popcount(G.xl & T.zl)) & 1)
-              T.kmask |= 1u << kk;
+          T.zk = (T.zl >> 8) & 0xFu;
+          T.imag = (uint32_t)(__builtin_popcount(G.xl & T.zl) & 1);
           P.terms[order.size()] = T;
           order.push_back(k);
           ++G.count;
@@ -314,7 +437,7 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
     int pos[kXTileQubits];
     for (int b = 0; b < kXTileQubits; ++b) pos[b] = P.spos[b];
     FixedBits tb = make_fixed(pos, kXTileQubits, 0);
-    const size_t smem = sizeof(double2) << kXTileQubits;
+    const size_t smem = kXSmemBytes;
     static uint64_t attr_done = 0;
     QSV_TRY(ensure_smem_attr(k_expect_tile, (int)smem, attr_done));
     k_expect_tile<<<grid, kXThreads, smem, s>>>(a, dpass, tb, ntiles, partials);
