@@ -1,0 +1,139 @@
+"""Edge cases of the GPU path against the numpy oracle: the smallest states
+(n = 1..7, below and across the tile-pass threshold), empty circuits and
+observables, identity terms, and the reference's argument errors
+(gates.py:26-32,74-77; observable.py:75-77,106-107; state.py:40-44,78-81)."""
+
+import numpy as np
+import pytest
+
+import paper_2011_13524_b200 as qs
+from paper_2011_13524_b200 import gate as qg
+from paper_2011_13524_b200._circuit import circuit_records
+
+from oracle import qsim_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def small_circuit(n, ngates, seed):
+    """Random gates of every kind that fits n qubits (k-qubit gates only
+    when k <= n, controls only when a spare qubit exists)."""
+    rng = np.random.default_rng(seed)
+    c = qs.QuantumCircuit(n)
+    for _ in range(ngates):
+        perm = [int(v) for v in rng.permutation(n)]
+        kind = int(rng.integers(0, 10))
+        if kind == 0:
+            g = qg.H(perm[0])
+        elif kind == 1:
+            g = qg.RX(perm[0], float(rng.uniform(-7, 7)))
+        elif kind == 2:
+            g = qg.RZ(perm[0], float(rng.uniform(-7, 7)))
+        elif kind == 3 and n >= 2:
+            g = qg.CNOT(perm[0], perm[1])
+        elif kind == 4 and n >= 2:
+            g = qg.CZ(perm[0], perm[1])
+        elif kind == 5:
+            k = int(rng.integers(1, min(n, 5) + 1))
+            g = qg.RandomUnitary(perm[:k], seed=int(rng.integers(1 << 30)))
+        elif kind == 6:
+            k = int(rng.integers(1, min(n, 3) + 1))
+            g = qg.DiagonalMatrix(perm[:k], np.exp(1j * rng.uniform(0, 6, 1 << k)))
+        elif kind == 7:
+            k = int(rng.integers(1, min(n, 4) + 1))
+            g = qg.PauliRotation(perm[:k], [int(v) for v in rng.integers(1, 4, k)],
+                                 float(rng.uniform(-7, 7)))
+        elif kind == 8:
+            k = int(rng.integers(1, min(n, 3) + 1))
+            g = qg.Pauli(perm[:k], [int(v) for v in rng.integers(1, 4, k)])
+        elif n >= 2:
+            g = qg.RandomUnitary([perm[0]], seed=int(rng.integers(1 << 30)))
+            g.add_control_qubit(perm[1], int(rng.integers(2)))
+        else:
+            g = qg.X(perm[0])
+        c.add_gate(g)
+    return c
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("use_tiles", [0, 1])
+def test_small_states_match_oracle(n, use_tiles):
+    circ = small_circuit(n, 60, seed=100 + n)
+    circ.set_plan_options(use_tiles=use_tiles)
+    st = qs.QuantumState(n)
+    st.set_Haar_random_state(n)
+    circ.update_quantum_state(st)
+    ref = orc.run_records(orc.haar_state(n, n), n, circuit_records(circ))
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+    assert abs(st.get_squared_norm() - 1.0) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [1, 9])
+def test_empty_circuit_is_identity(n):
+    st = qs.QuantumState(n)
+    st.set_Haar_random_state(3)
+    before = st.get_vector()
+    qs.QuantumCircuit(n).update_quantum_state(st)
+    assert np.array_equal(st.get_vector(), before)  # bit-exact: nothing ran
+
+
+def test_single_gate_circuit_equals_gate():
+    n = 10
+    a, b = qs.QuantumState(n), qs.QuantumState(n)
+    a.set_Haar_random_state(4)
+    b.set_Haar_random_state(4)
+    c = qs.QuantumCircuit(n)
+    c.add_gate(qg.RX(3, 0.7))
+    c.update_quantum_state(a)
+    qg.RX(3, 0.7).update_quantum_state(b)
+    assert np.max(np.abs(a.get_vector() - b.get_vector())) <= 1e-15
+
+
+def test_empty_and_identity_observables():
+    n = 5
+    st = qs.QuantumState(n)
+    st.set_Haar_random_state(7)
+    empty = qs.Observable(n)
+    assert empty.get_term_count() == 0
+    assert empty.get_expectation_value(st) == 0.0  # sum over no terms
+    ident = qs.Observable(n)
+    ident.add_operator(2.5, "")  # identity term: coef * <psi|psi>
+    assert abs(ident.get_expectation_value(st) - 2.5) <= 1e-12
+    op = qs.GeneralQuantumOperator(n)
+    op.add_operator(0.5 - 0.25j, "")
+    op.add_operator(1.5, "X 0 Y 4")
+    ref = orc.expectation(st.get_vector(), st.get_vector(), n,
+                          [(0.5 - 0.25j, ()), (1.5, ((0, 1), (4, 2)))])
+    assert abs(op.get_expectation_value(st) - ref) <= 1e-12
+
+
+def test_one_qubit_observable():
+    st = qs.QuantumState(1)
+    qg.H(0).update_quantum_state(st)
+    obs = qs.Observable(1)
+    obs.add_operator(1.0, "X 0")
+    obs.add_operator(-2.0, "Z 0")
+    assert abs(obs.get_expectation_value(st) - 1.0) <= 1e-12
+
+
+def test_argument_errors():
+    st = qs.QuantumState(3)
+    with pytest.raises(ValueError):
+        qg.X(3).update_quantum_state(st)  # target outside the state
+    with pytest.raises(ValueError):
+        qg.CNOT(1, 1)  # control == target
+    with pytest.raises(ValueError):
+        st.set_computational_basis(8)
+    with pytest.raises(ValueError):
+        st.load([1.0, 0.0])  # length mismatch
+    obs = qs.Observable(3)
+    with pytest.raises(ValueError):
+        obs.add_operator(1.0, "Z 3")  # term outside the operator
+    with pytest.raises(ValueError):
+        obs.add_operator(1.0j, "Z 0")  # observables need real coefficients
+    with pytest.raises(ValueError):
+        obs.get_expectation_value(qs.QuantumState(4))  # qubit counts differ
+    c = qs.QuantumCircuit(2)
+    c.add_gate(qg.H(1))
+    with pytest.raises(ValueError):
+        c.update_quantum_state(st)  # circuit and state sizes differ
