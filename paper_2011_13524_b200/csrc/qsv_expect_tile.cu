@@ -116,6 +116,28 @@ __device__ __forceinline__ void x_cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// products p = conj(psi_x) psi_{x ^ xl} of the 8 slots k whose bit J equals b
+// (b is per thread; selects instead of branches), zero in the other 8
+template <int J>
+__device__ __forceinline__ void pair_products(const double2 (&v)[kXPer], const double2* sm,
+                                              int tid, uint32_t xl, uint32_t b,
+                                              double (&re)[kXPer], double (&im)[kXPer]) {
+#pragma unroll
+  for (int i = 0; i < kXPer / 2; ++i) {
+    const int k0 = ((i >> J) << (J + 1)) | (i & ((1 << J) - 1));
+    const int k1 = k0 | (1 << J);
+    const double2 x = b ? v[k1] : v[k0];
+    const uint32_t k = b ? (uint32_t)k1 : (uint32_t)k0;
+    const double2 w = sm[(k * kXThreads + (uint32_t)tid) ^ xl];
+    const double r = fma(x.x, w.x, x.y * w.y);
+    const double m = fma(x.x, w.y, -x.y * w.x);
+    re[k0] = b ? 0.0 : r;
+    re[k1] = b ? r : 0.0;
+    im[k0] = b ? 0.0 : m;
+    im[k1] = b ? m : 0.0;
+  }
+}
+
 // S_t = sum_x conj(psi_x) psi_{x ^ xl} (-1)^popc((x ^ xl) & zl) over the tile,
 // accumulated per thread across all of the CTA's tiles (one shared-memory
 // read-modify-write per term and tile instead of a warp reduction), reduced
@@ -183,7 +205,6 @@ __global__ void __launch_bounds__(kXThreads, 1)
       const XGroup G = P.groups[g];
       const int t1 = G.first + G.count;
       double re[kXPer], im[kXPer];
-      uint32_t own = 0xffffu;  // k slots this thread visits
       double f = 1.0;
       if (G.xl == 0) {
 #pragma unroll
@@ -192,25 +213,19 @@ __global__ void __launch_bounds__(kXThreads, 1)
           im[k] = 0.0;
         }
       } else {
+        // every thread visits 8 of its 16 slots, so no lane or warp idles:
+        // a pairing bit on the slots (hb >= 8) is visited from its 0 side; a
+        // pairing bit on the thread bits (then the slot part of xl is 0) is
+        // visited by the bit-0 thread on slots 0..7 and by the bit-1 thread
+        // on slots 8..15 (each pair once; the summand is symmetric in which
+        // end visits it)
         f = 2.0;
-        if (G.hb >= 8) {
-          const int kb = G.hb - 8;
-          own = 0;
-#pragma unroll
-          for (int k = 0; k < kXPer; ++k)
-            if (!((k >> kb) & 1)) own |= 1u << k;
-        } else if ((tid >> G.hb) & 1) {
-          continue;  // the partner thread covers these pairs
-        }
-#pragma unroll
-        for (int k = 0; k < kXPer; ++k) {
-          if (!((own >> k) & 1)) {
-            re[k] = im[k] = 0.0;
-            continue;
-          }
-          const double2 w = sm[(uint32_t)(k * kXThreads + tid) ^ G.xl];
-          re[k] = fma(v[k].x, w.x, v[k].y * w.y);
-          im[k] = fma(v[k].x, w.y, -v[k].y * w.x);
+        const uint32_t b = G.hb >= 8 ? 0u : ((uint32_t)tid >> G.hb) & 1u;
+        switch (G.hb >= 8 ? G.hb - 8 : 3) {
+          case 0: pair_products<0>(v, sm, tid, G.xl, b, re, im); break;
+          case 1: pair_products<1>(v, sm, tid, G.xl, b, re, im); break;
+          case 2: pair_products<2>(v, sm, tid, G.xl, b, re, im); break;
+          default: pair_products<3>(v, sm, tid, G.xl, b, re, im); break;
         }
       }
       // a slot sign pattern (-1)^popc(k & zk) is one Walsh-Hadamard
