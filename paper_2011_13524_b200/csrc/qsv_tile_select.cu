@@ -3,6 +3,7 @@
 // batches, otherwise the 16-amplitude kernel (r4); one plan per program.  Measured (profiles/variant_ab.py, time_fused.py):
 // cz-ladder r5, cnot-ring / QV / QFT / heavy(2..4) r4, heavy(5) r5 (2x).
 // QSV_TILE_VARIANT=4|5 forces one (A/B experiments).
+#include <cmath>
 #include <cstdlib>
 
 #include "qsv_tile.cuh"
@@ -58,8 +59,59 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
   }
   if (force == 4 && on4 != on5)
     return r4::plan_program(n, gates, opts, steps, tiles, payload, stats, nullptr, false);
-  return use5 ? r5::plan_program(n, pre, opts, steps, tiles, payload, stats, nullptr, true)
-              : r4::plan_program(n, pre, opts, steps, tiles, payload, stats, nullptr, true);
+  auto plan_with = [&](const qsv_plan_opts& o, std::vector<Step>& st, std::vector<TilePlan>& tp,
+                       std::vector<char>& pl, qsv_program_stats* ps) {
+    return use5 ? r5::plan_program(n, pre, o, st, tp, pl, ps, nullptr, true)
+                : r4::plan_program(n, pre, o, st, tp, pl, ps, nullptr, true);
+  };
+  // Small states (n <= 20, default tile size, unsharded): a pass has at most
+  // a few waves of tiles, so its time is a per-pass latency plus, per phase,
+  // work proportional to the tile size times the waves; smaller tiles put
+  // more SMs to work at the price of more passes.  Plan L = 10, 11, 12 and
+  // keep the cheapest under that model (fitted on cnot-ring / cz-ladder at
+  // n = 14..20, profiles/time_small_n.py: it picks the measured best or
+  // within 4% of it in all eight cases; cnot-ring(16) 0.63 -> 0.52 ms).
+  if (opts.tile_qubits == 0 && opts.outer_mask == 0 && n <= 20 && n >= 11 && on4 && on5 &&
+      !getenv("QSV_FIXED_TILE")) {
+    constexpr double kPass = 20.3e-3, kAmpPhase = 9.05e-7;  // ms
+    constexpr double kGroupsPerGpu = 296.0;                 // 2 tile groups x 148 SMs
+    double best_cost = 0;
+    int best_rc = QSV_OK;
+    bool have = false;
+    const qsv_program_stats init = *stats;
+    for (int L = 10; L <= 12; ++L) {
+      qsv_plan_opts o = opts;
+      o.tile_qubits = L;
+      std::vector<Step> st;
+      std::vector<TilePlan> tp;
+      std::vector<char> pl;
+      qsv_program_stats ps = init;
+      const int rc = plan_with(o, st, tp, pl, &ps);
+      if (rc) {
+        if (!have) best_rc = rc;
+        continue;
+      }
+      double cost = 0;
+      for (const Step& s : st) {
+        cost += kPass;
+        if (s.type == 1) {
+          const TilePlan& t = tp[s.tile];
+          const double waves = std::ceil(std::ldexp(1.0, n - t.L) / kGroupsPerGpu);
+          cost += t.nphases * kAmpPhase * std::ldexp(1.0, t.L) * waves;
+        }
+      }
+      if (!have || cost < best_cost) {
+        have = true;
+        best_cost = cost;
+        steps.swap(st);
+        tiles.swap(tp);
+        payload.swap(pl);
+        *stats = ps;
+      }
+    }
+    return have ? QSV_OK : best_rc;
+  }
+  return plan_with(opts, steps, tiles, payload, stats);
 }
 
 int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,
