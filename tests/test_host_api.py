@@ -185,3 +185,19 @@ def test_core_module_exports_reference_core_names():
              "tensor_product"]
     missing = [n for n in names if not hasattr(core, n)]
     assert not missing, missing
+
+
+def _core(circ):
+    return circ._core if hasattr(circ, "_core") else circ
+
+
+def test_small_state_tile_size_choice():
+    """n <= 20: the planner keeps the cheapest of the L = 10/11/12 plans
+    (qsv_tile_select.cu); larger states and explicit tile sizes are unchanged."""
+    for n, expect_l in ((16, 10), (20, 12)):
+        c = _core(workloads.generate_cnot_ring(n, seed=1))
+        auto = c.plan_stats(use_tiles=1)
+        per_l = {L: c.plan_stats(use_tiles=1, tile_qubits=L) for L in (10, 11, 12)}
+        assert auto == per_l[expect_l], (n, auto, per_l)
+    c = _core(workloads.generate_cz_ladder(24, 4, seed=1))
+    assert c.plan_stats(use_tiles=1) == c.plan_stats(use_tiles=1, tile_qubits=12)
