@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     k_tile(double2* __restrict__ a, const TilePassDev* __restrict__ pd,
            const TilePhase* __restrict__ phases, const TileOp* __restrict__ g_ops,
            const double2* __restrict__ g_data, FixedBits tb, uint64_t ntiles, int nops,
-           int ndata, unsigned long long* __restrict__ ctr) {
+           int ndata, unsigned long long* __restrict__ ctr, int nostagger) {
   extern __shared__ double2 smem_all[];
   __shared__ unsigned long long s_next[kGroups];
   __shared__ uint64_t s_hi[kRegs + 1];   // HBM offset of copy-index bits >= kTidBits (+ flag)
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   // through its first tile, so one group's HBM traffic overlaps the other's
   // math from then on.
   volatile int* s_go = reinterpret_cast<volatile int*>(&s_hi[kRegs]);
-  if (threadIdx.x == 0) *s_go = (kGroups < 2 || (pd->debug & 16)) ? kGroups : 0;
+  if (threadIdx.x == 0) *s_go = (kGroups < 2 || nostagger || (pd->debug & 16)) ? kGroups : 0;
   __syncthreads();
   if (group > 0)
     while (*s_go < group) __nanosleep(256);
@@ -1986,11 +1986,22 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     attr_dev = dev;
   }
   const uint64_t ntiles = 1ULL << (n - np);
-  const uint64_t ctas = (ntiles + kGroups - 1) / kGroups;
   const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms) : num_sms;
-  const unsigned grid = (unsigned)std::min<uint64_t>(ctas, (uint64_t)sms);
+  // Few tiles (small states): one tile per SM while they last -- group 0 of
+  // every CTA takes one, group 1 is held back by the stagger and finds none
+  // left; up to two tiles per SM: both groups start at once (the stagger
+  // would delay the second tile by half a tile); otherwise persistent CTAs.
+  unsigned grid;
+  int nostagger = 0;
+  if (ntiles <= (uint64_t)sms) {
+    grid = (unsigned)ntiles;
+  } else {
+    const uint64_t ctas = (ntiles + kGroups - 1) / kGroups;
+    grid = (unsigned)std::min<uint64_t>(ctas, (uint64_t)sms);
+    nostagger = ntiles <= (uint64_t)kGroups * grid;
+  }
   k_tile<<<grid, kCtaThreads, smem, s>>>(amps, pd, ph, ops, data, tb, ntiles, tp.nops,
-                                          tp.ndata, ctr);
+                                          tp.ndata, ctr, nostagger);
   QSV_CHECK_LAUNCH("k_tile");
   return QSV_OK;
 }

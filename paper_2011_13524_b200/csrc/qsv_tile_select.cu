@@ -69,11 +69,12 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
   // work proportional to the tile size times the waves; smaller tiles put
   // more SMs to work at the price of more passes.  Plan L = 10, 11, 12 and
   // keep the cheapest under that model (fitted on cnot-ring / cz-ladder at
-  // n = 14..20, profiles/time_small_n.py: it picks the measured best or
-  // within 4% of it in all eight cases; cnot-ring(16) 0.63 -> 0.52 ms).
+  // n = 14..20 with the few-tile grid policy of launch_tile_pass,
+  // profiles/time_small_n.py: it picks the measured best or within 1% of it
+  // in all eight cases).
   if (opts.tile_qubits == 0 && opts.outer_mask == 0 && n <= 20 && n >= 11 && on4 && on5 &&
       !getenv("QSV_FIXED_TILE")) {
-    constexpr double kPass = 20.3e-3, kAmpPhase = 9.05e-7;  // ms
+    constexpr double kPass = 15.2e-3, kAmpPhase = 2.95e-7;  // ms
     constexpr double kGroupsPerGpu = 296.0;                 // 2 tile groups x 148 SMs
     double best_cost = 0;
     int best_rc = QSV_OK;

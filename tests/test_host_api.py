@@ -194,7 +194,7 @@ def _core(circ):
 def test_small_state_tile_size_choice():
     """n <= 20: the planner keeps the cheapest of the L = 10/11/12 plans
     (qsv_tile_select.cu); larger states and explicit tile sizes are unchanged."""
-    for n, expect_l in ((16, 10), (20, 12)):
+    for n, expect_l in ((16, 11), (20, 12)):
         c = _core(workloads.generate_cnot_ring(n, seed=1))
         auto = c.plan_stats(use_tiles=1)
         per_l = {L: c.plan_stats(use_tiles=1, tile_qubits=L) for L in (10, 11, 12)}
