@@ -669,7 +669,7 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
     del st
     # the headline curve: sec/layer vs qubits (same generator, same depth)
     curve = {}
-    for m in range(20, n + 1, 2):
+    for m in list(range(14, 20, 2)) + list(range(20, n + 1, 2)):
         c = workloads.generate_cz_ladder(m, depth, seed=1)
         s2 = qs.QuantumState(m, device=dev)
         s2.set_stream(stream.cuda_stream)
