@@ -236,6 +236,13 @@ class Circuit:
             raise ValueError("state and circuit qubit counts differ")
         if not self.gates:
             return
+        if getattr(state, "is_sharded", False):
+            # dist.ShardedQuantumState: the sharded engine plans remaps and
+            # compiles its own per-rank programs from the gate records
+            if not all(isinstance(g, BasicGate) for g in self.gates):
+                raise ValueError("quantum maps cannot run on a sharded state")
+            state.apply_records([g.record() for g in self.gates])
+            return
         prog = self.compile()
         if isinstance(prog, _Program):
             prog.run(state)

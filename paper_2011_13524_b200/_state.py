@@ -24,6 +24,16 @@ def _check_count(n) -> int:
     return int(n)
 
 
+def haar_vector(num_qubits: int, seed=None) -> np.ndarray:
+    """Host draw of the reference's Haar state: real block, then imaginary
+    block of PCG64 normals, divided by the norm (state.py:46-54)."""
+    dim = 1 << int(num_qubits)
+    gen = np.random.default_rng(seed)
+    raw = gen.standard_normal(dim) + 1j * gen.standard_normal(dim)
+    raw /= np.linalg.norm(raw)
+    return raw
+
+
 class StateVector:
     """2^n amplitudes on a GPU plus the classical register list."""
 
@@ -96,10 +106,7 @@ class StateVector:
         """Complex Gaussian (real block, then imaginary block, PCG64) divided
         by its norm -- drawn on the host with numpy so that a seed gives the
         bit-identical state of the reference (state.py:46-54)."""
-        gen = np.random.default_rng(seed)
-        raw = gen.standard_normal(self.dim) + 1j * gen.standard_normal(self.dim)
-        raw /= np.linalg.norm(raw)
-        self._upload(raw)
+        self._upload(haar_vector(self._n, seed))
 
     set_haar_random = set_Haar_random_state
 

@@ -120,6 +120,31 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
   else cudaFreeAsync(p, s);
 }
 
+
+// Cross-state ordering.  An op queued on `s` (device `dev`) that reads another
+// state `src` must (1) start after the work already queued on src's stream and
+// (2) finish before anything queued on src's stream later (a gate overwriting
+// the amplitudes being read, or the stream-ordered free of src).  Both sides
+// are expressed as event waits on the device, no host synchronisation.
+static int stream_wait(cudaStream_t waiter, cudaStream_t signaler, int signaler_dev) {
+  if (waiter == signaler) return QSV_OK;
+  DeviceGuard dg(signaler_dev);
+  cudaEvent_t ev;
+  QSV_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  cudaError_t e = cudaEventRecord(ev, signaler);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(waiter, ev, 0);
+  cudaEventDestroy(ev);  // released once the recorded work completes
+  if (e != cudaSuccess) return cuda_fail(e, "cross-state stream ordering");
+  return QSV_OK;
+}
+static int read_begin(const qsv_state* src, cudaStream_t s, int dev) {
+  (void)dev;
+  return stream_wait(s, src->stream, src->device);
+}
+static int read_end(const qsv_state* src, cudaStream_t s, int dev) {
+  return stream_wait(src->stream, s, dev);
+}
+
 static int ensure(Scratch& s, size_t bytes, cudaStream_t stream) {
   if (s.cap >= bytes) return QSV_OK;
   if (s.ptr) {
@@ -524,7 +549,8 @@ int qsv_copy(const qsv_state* src, qsv_state* dst) {
     return QSV_EINVAL;
   }
   DeviceGuard dg(dst->device);
-  if (src->stream != dst->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
+  int rc = read_begin(src, dst->stream, dst->device);
+  if (rc) return rc;
   if (src->device == dst->device) {
     QSV_TRY(cudaMemcpyAsync(dst->amps, src->amps, src->dim * sizeof(double2),
                             cudaMemcpyDeviceToDevice, dst->stream));
@@ -532,7 +558,7 @@ int qsv_copy(const qsv_state* src, qsv_state* dst) {
     QSV_TRY(cudaMemcpyPeerAsync(dst->amps, dst->device, src->amps, src->device,
                                 src->dim * sizeof(double2), dst->stream));
   }
-  return QSV_OK;
+  return read_end(src, dst->stream, dst->device);
 }
 
 int qsv_set_random_device(qsv_state* st, uint64_t seed) {
@@ -623,7 +649,9 @@ static int run_sweeps(const qsv_state* bra, const qsv_state* ket,
                       const std::vector<Sweep>& sweeps, std::vector<double>& res) {
   DeviceGuard dg(ket->device);
   cudaStream_t s = ket->stream;
-  if (bra->stream != ket->stream) QSV_TRY(cudaStreamSynchronize(bra->stream));
+  // the host waits for s below, so the bra's later work is ordered already
+  int rc0 = read_begin(bra, s, ket->device);
+  if (rc0) return rc0;
   const size_t need = sizeof(double) * 2 * kMaxTerms * std::max<size_t>(1, sweeps.size());
   Scratch& sc = g_results[ket];
   int rc = ensure(sc, need, s);
@@ -786,8 +814,10 @@ int qsv_add(qsv_state* dst, const qsv_state* src) {
     return QSV_EINVAL;
   }
   DeviceGuard dg(dst->device);
-  if (src->stream != dst->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
-  return launch_add(dst->amps, src->amps, dst->dim, dst->stream);
+  int rc = read_begin(src, dst->stream, dst->device);
+  if (!rc) rc = launch_add(dst->amps, src->amps, dst->dim, dst->stream);
+  if (!rc) rc = read_end(src, dst->stream, dst->device);
+  return rc;
 }
 
 // ------------------------------------------------- analysis / reshaping
@@ -871,9 +901,12 @@ int qsv_tensor_product(const qsv_state* first, const qsv_state* second, qsv_stat
   }
   if (same_device3(first, second, out)) return QSV_EINVAL;
   DeviceGuard dg(out->device);
-  if (first->stream != out->stream) QSV_TRY(cudaStreamSynchronize(first->stream));
-  if (second->stream != out->stream) QSV_TRY(cudaStreamSynchronize(second->stream));
-  return launch_kron(first->amps, first->n, second->amps, second->n, out->amps, out->stream);
+  int rc = read_begin(first, out->stream, out->device);
+  if (!rc) rc = read_begin(second, out->stream, out->device);
+  if (!rc) rc = launch_kron(first->amps, first->n, second->amps, second->n, out->amps, out->stream);
+  if (!rc) rc = read_end(first, out->stream, out->device);
+  if (!rc) rc = read_end(second, out->stream, out->device);
+  return rc;
 }
 
 int qsv_permutate_qubit(const qsv_state* src, const int* order, int n, qsv_state* out) {
@@ -896,8 +929,10 @@ int qsv_permutate_qubit(const qsv_state* src, const int* order, int n, qsv_state
   }
   if (same_device3(src, out, out)) return QSV_EINVAL;
   DeviceGuard dg(out->device);
-  if (src->stream != out->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
-  return launch_permute(src->amps, out->amps, n, order, out->stream);
+  int rc = read_begin(src, out->stream, out->device);
+  if (!rc) rc = launch_permute(src->amps, out->amps, n, order, out->stream);
+  if (!rc) rc = read_end(src, out->stream, out->device);
+  return rc;
 }
 
 int qsv_drop_qubit(const qsv_state* src, const int* targets, const int* values, int k,
@@ -921,8 +956,10 @@ int qsv_drop_qubit(const qsv_state* src, const int* targets, const int* values, 
   }
   if (same_device3(src, out, out)) return QSV_EINVAL;
   DeviceGuard dg(out->device);
-  if (src->stream != out->stream) QSV_TRY(cudaStreamSynchronize(src->stream));
-  return launch_drop(src->amps, src->n, targets, values, k, out->amps, out->stream);
+  int rc = read_begin(src, out->stream, out->device);
+  if (!rc) rc = launch_drop(src->amps, src->n, targets, values, k, out->amps, out->stream);
+  if (!rc) rc = read_end(src, out->stream, out->device);
+  return rc;
 }
 
 int qsv_branch_norm2(const qsv_state* st, const int* targets, int k, const double* matrix,

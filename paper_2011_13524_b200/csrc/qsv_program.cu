@@ -30,6 +30,7 @@ struct qsv_program {
   cudaGraphExec_t gexec = nullptr;
   cudaGraph_t graph = nullptr;
   double2* graph_amps = nullptr;
+  unsigned long long* graph_ctr = nullptr;  // the captured tile passes' work counter
   cudaStream_t graph_stream = nullptr;
   int graph_sm_limit = 0;
   cudaStream_t last_stream = 0;  // the payload is released in this stream's order
@@ -104,6 +105,7 @@ void drop_graph(qsv_program* p) {
   p->gexec = nullptr;
   p->graph = nullptr;
   p->graph_amps = nullptr;
+  p->graph_ctr = nullptr;
 }
 
 }  // namespace
@@ -255,7 +257,11 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
   // after set_parameter) never pays for graph capture + instantiation
   if (!p->opts.use_graph || p->steps.empty() || p->runs++ == 0)
     return launch_steps(p, st->amps, st->stream, st->sm_limit, st->tile_ctr);
-  if (!(p->gexec && p->graph_amps == st->amps && p->graph_stream == st->stream &&
+  // the graph bakes in the amplitude buffer AND the state's work counter: a
+  // new state may reuse a freed amplitude block while its counter lives
+  // elsewhere, so both pointers are part of the key
+  if (!(p->gexec && p->graph_amps == st->amps && p->graph_ctr == st->tile_ctr &&
+        p->graph_stream == st->stream &&
         p->device == st->device && p->graph_sm_limit == st->sm_limit)) {
     drop_graph(p);
     // capture on a private stream (the legacy stream cannot be captured)
@@ -282,6 +288,7 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
     }
     p->graph = g;
     p->graph_amps = st->amps;
+    p->graph_ctr = st->tile_ctr;
     p->graph_stream = st->stream;
     p->graph_sm_limit = st->sm_limit;
     p->device = st->device;

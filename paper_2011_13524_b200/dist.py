@@ -416,8 +416,18 @@ class CudaShard:
 class ShardedQuantumState:
     """2^n amplitudes over P = 2^p shards (see module docstring).
 
+    Drop-in for the reference's state in the calls that act on it:
+    ``QuantumCircuit.update_quantum_state(state)``, a gate's
+    ``update_quantum_state(state)`` and ``Observable.get_expectation_value
+    (state)`` (bindings __init__.py:77-78, 118-119) dispatch here through
+    ``is_sharded``; ``get_qubit_count``, ``set_zero_state``,
+    ``set_computational_basis``, ``set_Haar_random_state``, ``load``,
+    ``get_vector`` and ``get_squared_norm`` keep the reference names.
+
     ``owned``: list of ranks this process simulates (default: its own rank);
     ``backend``: callable (L, rank) -> shard backend (default CudaShard)."""
+
+    is_sharded = True
 
     def __init__(self, num_qubits, world=None, rank=None, owned=None, backend=None,
                  group=None, chunk_bytes=1 << 30, plan=None, exchange="auto",
@@ -618,6 +628,17 @@ class ShardedQuantumState:
             ph |= ((idx >> q) & 1) << self.phys[q]
         return full[ph]
 
+    def get_qubit_count(self) -> int:
+        return self.n
+
+    def set_Haar_random_state(self, seed=None):
+        """Same vector as QuantumState.set_Haar_random_state (host PCG64,
+        state.py:46-54), scattered to the shards (small n: every process
+        draws the full vector)."""
+        from ._state import haar_vector
+        self.phys = list(range(self.n))
+        self.load(haar_vector(self.n, seed))
+
     def get_squared_norm(self) -> float:
         return self._allreduce(complex(sum(s.norm2() for s in self.shards.values()))).real
 
@@ -711,23 +732,49 @@ class ShardedQuantumState:
             i += 1
 
     def update_quantum_state(self, circuit):
-        from ._circuit import circuit_records
-        self.apply_records(circuit_records(circuit))
+        """Deprecated spelling kept for existing callers: the reference call
+        is ``circuit.update_quantum_state(state)``."""
+        from ._handles import unwrap
+        unwrap(circuit).update_state(self)
 
     def expectation(self, terms) -> complex:
-        """terms: (coef, [(logical qubit, axis)...]); X/Y factors on global
-        qubits are brought local by swaps first."""
-        need = set()
-        for _, ops in terms:
-            need |= {q for q, a in ops if a in (1, 2)}
-        if any(self.phys[q] >= self.L for q in need):
-            if len(need) > self.L:
-                raise ValueError("X/Y factors on more qubits than a shard holds")
-            # one placeholder touching every X/Y qubit: all become local together
-            recs = [("dense", tuple(sorted(need)), None, ())]
-            for step in self.plan(recs):
-                if step[0] == "swap":
-                    self._remap(step[1], step[2])
+        """terms: (coef, [(logical qubit, axis)...]).  A term's X/Y factors
+        must sit on local qubits while it is evaluated.  Terms whose X/Y
+        qubits are local already are evaluated first; the rest are grouped
+        greedily so that each group's X/Y support fits in a shard (L qubits),
+        and each group is brought local by one remap and evaluated in turn.
+        So observables with X/Y on every qubit (TFIM, sum_i X_i) work on any
+        number of shards; only a single term with X/Y on more than L qubits
+        is rejected."""
+        terms = list(terms)
+        supp = [frozenset(q for q, a in ops if a in (1, 2)) for _, ops in terms]
+        for s_ in supp:
+            if len(s_) > self.L:
+                raise ValueError("a term has X/Y factors on more qubits than a shard holds")
+        pending = list(range(len(terms)))
+        total = 0j
+        while pending:
+            ready = [i for i in pending if all(self.phys[q] < self.L for q in supp[i])]
+            if not ready:
+                # next group: greedy union of X/Y supports within L qubits
+                need = set()
+                for i in pending:
+                    if len(need | supp[i]) <= self.L:
+                        need |= supp[i]
+                recs = [("dense", tuple(sorted(need)), None, ())]
+                for step in self.plan(recs):
+                    if step[0] == "swap":
+                        self._remap(step[1], step[2])
+                continue
+            total += self._expect_local([terms[i] for i in ready])
+            done = set(ready)
+            pending = [i for i in pending if i not in done]
+        return self._allreduce(total)
+
+    def _expect_local(self, terms) -> complex:
+        """Partial sum over this process's shards of terms whose X/Y factors
+        are all on local physical qubits (Z factors on global qubits become
+        per-rank signs)."""
         total = 0j
         for r, s in self.shards.items():
             loc = []
@@ -745,7 +792,7 @@ class ShardedQuantumState:
                         lops.append((p, a))
                 loc.append((coef * sign, lops))
             total += s.expect_terms(loc)
-        return self._allreduce(total)
+        return total
 
     # -- the exchange ---------------------------------------------------------
     def _remap(self, gs, ls):

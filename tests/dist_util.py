@@ -175,3 +175,44 @@ def random_records(n, ngates, seed):
             q, r = np.linalg.qr(z)
             out.append(("dense", t, q, ((perm[1], int(rng.integers(2))), (perm[2], 1))))
     return out
+
+
+def circuit_of(n, records):
+    """QuantumCircuit holding the gates of neutral records, so that tests
+    drive the sharded engine through the reference call
+    ``circuit.update_quantum_state(state)`` (bindings __init__.py:118-119)."""
+    from paper_2011_13524_b200 import QuantumCircuit
+    from paper_2011_13524_b200 import _gates as G
+    qc = QuantumCircuit(n)
+    for rec in records:
+        kind = rec[0]
+        if kind == "dense":
+            g = G.DenseGate(rec[1], rec[2], rec[3])
+        elif kind == "diag":
+            g = G.DiagonalGate(rec[1], rec[2], rec[3])
+        elif kind == "pauli":
+            g = G.PauliGate(rec[1], rec[2], rec[3])
+        elif kind == "pauli_rot":
+            g = G.PauliRotationGate(rec[1], rec[2], rec[3], rec[4])
+        else:
+            raise ValueError(f"no gate for record kind {kind!r}")
+        qc.add_gate(g)
+    return qc
+
+
+def observable_of(n, terms):
+    """Observable of (coef, [(qubit, axis)...]) terms, evaluated through the
+    reference call ``Observable.get_expectation_value(state)``."""
+    from paper_2011_13524_b200 import Observable
+    obs = Observable(n)
+    for coef, ops in terms:
+        obs.add_operator(float(np.real(coef)),
+                         " ".join(f"{'IXYZ'[a]} {q}" for q, a in ops))
+    return obs
+
+
+def tfim_terms(n, j=-1.0, h=-0.5):
+    """Transverse-field Ising terms (SURVEY 8(d) cfg3 shape): X on every
+    qubit, so no shard ever holds the union of the X supports."""
+    return ([(j, [(i, 3), (i + 1, 3)]) for i in range(n - 1)]
+            + [(h, [(i, 1)]) for i in range(n)])

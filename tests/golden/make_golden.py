@@ -19,6 +19,8 @@ fixtures next to this script:
 * ``haar.npz`` -- set_haar_random outputs (bit-exact pin of the PCG64 path).
 * ``analysis.json`` + ``analysis.npz`` -- marginal probabilities, sampling
   results, tensor_product / permutate_qubit / drop_qubit outputs.
+* ``cfg1.json`` + ``cfg1.npz`` -- cnot-ring(16) seeds 0..4 from |0> and from
+  Haar starts (digests: sampled amplitudes, random projections, <Z_q>).
 
 Nothing on the GPU box reads /root/reference; only these files travel.
 """
@@ -431,6 +433,35 @@ def make_serialize():
         json.dump({"cregs": list(st.classical_registers), "optimizer_counts": counts}, fh)
 
 
+def make_cfg1():
+    """cfg1: cnot-ring(16) seeds 0..4 from |0> and from a Haar
+    start (seed 10 + s), run by the reference.  A 16-qubit state is 1 MiB,
+    so each case keeps a digest instead of the full vector: the amplitudes at
+    CFG1_SAMPLES fixed indices, CFG1_PROJ projections <w_k|psi> onto fixed
+    PCG64 Gaussian vectors (every amplitude moves them), the squared norm
+    and <Z_q> of every qubit (golden_util.cfg1_digest recomputes the same
+    digest from any candidate state)."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from golden_util import cfg1_digest
+    entries, outs = [], {}
+    for s in range(5):
+        for start in (None, 10 + s):
+            circ = rbench.generate_cnot_ring(16, seed=s)
+            st = core.StateVector(16)
+            if start is not None:
+                st.set_haar_random(start)
+            circ.update_state(st)
+            key = f"cfg1_s{s}_" + ("zero" if start is None else f"haar{start}")
+            entries.append({"id": key, "seed": s, "start_seed": start,
+                            "gate_count": circ.get_gate_count()})
+            for k, v in cfg1_digest(st.get_vector()).items():
+                outs[f"{key}/{k}"] = v
+    with open(os.path.join(HERE, "cfg1.json"), "w") as fh:
+        json.dump({"cases": entries}, fh)
+    np.savez_compressed(os.path.join(HERE, "cfg1.npz"), **outs)
+    print(f"cfg1: {len(entries)} cases")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-cfg3", action="store_true",
@@ -451,6 +482,9 @@ def main():
     if args.only == "serialize":
         make_serialize()
         return
+    if args.only == "cfg1":
+        make_cfg1()
+        return
     make_haar()
     make_analysis()
     make_maps()
@@ -459,6 +493,7 @@ def main():
     make_gates()
     make_circuits()
     make_observables(args.with_cfg3)
+    make_cfg1()
 
 
 if __name__ == "__main__":

@@ -143,3 +143,29 @@ def load_density():
     with open(os.path.join(GOLDEN, "density.json")) as fh:
         meta = json.load(fh)
     return meta, np.load(os.path.join(GOLDEN, "density.npz"))
+
+
+CFG1_SAMPLES = 4096
+CFG1_PROJ = 16
+
+
+def cfg1_digest(psi):
+    """Size-independent digest of a 16-qubit state (see make_golden.make_cfg1):
+    amplitudes at fixed indices, projections onto fixed Gaussian vectors,
+    squared norm, <Z_q> for every qubit."""
+    psi = np.asarray(psi, dtype=np.complex128)
+    n = psi.size.bit_length() - 1
+    rng = np.random.default_rng(1601)
+    idx = np.sort(rng.choice(psi.size, CFG1_SAMPLES, replace=False))
+    w = rng.standard_normal((CFG1_PROJ, psi.size)) + 1j * rng.standard_normal((CFG1_PROJ, psi.size))
+    p = np.abs(psi) ** 2
+    x = np.arange(psi.size)
+    z = np.array([np.sum(p * (1 - 2 * ((x >> q) & 1))) for q in range(n)])
+    return {"idx": idx, "amps": psi[idx], "proj": w.conj() @ psi,
+            "norm2": np.array([np.sum(p)]), "z": z}
+
+
+def load_cfg1():
+    with open(os.path.join(GOLDEN, "cfg1.json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(GOLDEN, "cfg1.npz"))

@@ -13,7 +13,8 @@ import torch.multiprocessing as mp
 from paper_2011_13524_b200.dist import ShardedQuantumState, specialize
 
 from oracle import qsim_oracle as orc
-from dist_util import OracleShard, SharedOracleShard, random_records
+from dist_util import (OracleShard, SharedOracleShard, circuit_of, observable_of,
+                       random_records, tfim_terms)
 
 
 def _reference(n, records, seed):
@@ -27,7 +28,7 @@ def test_virtual_ranks_match_oracle(n, world):
     st = ShardedQuantumState(n, world=world, owned=list(range(world)),
                              backend=lambda L, r: OracleShard(L, r))
     st.load(orc.haar_state(n, 3))
-    st.apply_records(recs)
+    circuit_of(n, recs).update_quantum_state(st)
     got = st.get_vector()
     ref = _reference(n, recs, 3)
     assert np.max(np.abs(got - ref)) <= 1e-12
@@ -35,7 +36,7 @@ def test_virtual_ranks_match_oracle(n, world):
     assert abs(st.get_squared_norm() - orc.squared_norm(ref)) <= 1e-12
     terms = [(0.7, [(0, 1), (n - 1, 3)]), (-0.2, [(n - 1, 1)]), (0.4, [(1, 2), (n - 2, 2)]),
              (1.1, [])]
-    e = st.expectation(terms)
+    e = observable_of(n, terms).get_expectation_value(st)
     assert abs(e - orc.expectation(ref, ref, n, terms)) <= 1e-11
 
 
@@ -45,7 +46,7 @@ def test_cz_ladder_sharded_matches_oracle():
     st = ShardedQuantumState(n, world=4, owned=[0, 1, 2, 3],
                              backend=lambda L, r: OracleShard(L, r))
     st.set_zero_state()
-    st.apply_records(recs)
+    circuit_of(n, recs).update_quantum_state(st)
     ref = orc.run_records(orc.zero_state(n), n, recs)
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
 
@@ -80,11 +81,12 @@ def _worker(rank, world, port, n, q):
         recs = random_records(n, 40, seed=77)
         st = ShardedQuantumState(n, backend=lambda L, r: OracleShard(L, r), chunk_bytes=256)
         st.load(orc.haar_state(n, 5))
-        st.apply_records(recs)
+        circuit_of(n, recs).update_quantum_state(st)
         vec = st.get_vector()
         norm = st.get_squared_norm()
-        e = st.expectation([(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])])
-        q.put((rank, vec, norm, e, dict(st.stats)))
+        e = observable_of(n, [(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])]).get_expectation_value(st)
+        e_tf = observable_of(n, tfim_terms(n)).get_expectation_value(st)
+        q.put((rank, vec, norm, (e, e_tf), dict(st.stats)))
     finally:
         dist.destroy_process_group()
 
@@ -99,9 +101,9 @@ def _worker_p2p(rank, world, port, n, q, overlap_min=20):
         st = ShardedQuantumState(n, backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p",
                                  overlap_min_qubits=overlap_min)
         st.load(orc.haar_state(n, 5))
-        st.apply_records(recs)
+        circuit_of(n, recs).update_quantum_state(st)
         vec = st.get_vector()
-        e = st.expectation([(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])])
+        e = observable_of(n, [(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])]).get_expectation_value(st)
         mode = st.exchange
         st.close()
         dist.barrier()
@@ -150,7 +152,7 @@ def test_virtual_ranks_p2p_protocol(world):
                              backend=lambda L, r: SharedOracleShard(L, r), exchange="p2p")
     assert st.exchange == "p2p"
     st.load(orc.haar_state(n, 2))
-    st.apply_records(recs)
+    circuit_of(n, recs).update_quantum_state(st)
     got = st.get_vector()
     for s in st.shards.values():
         s.release()
@@ -175,7 +177,7 @@ def test_virtual_ranks_overlapped_remaps(world, bits):
         else:
             st.load(orc.haar_state(n, seed))
             ref = _reference(n, recs, seed)
-        st.apply_records(recs)
+        circuit_of(n, recs).update_quantum_state(st)
         got = st.get_vector()
         for s in st.shards.values():
             s.release()
@@ -216,7 +218,7 @@ def test_reordered_segments_match_oracle(reorder):
         st = ShardedQuantumState(n, world=world, owned=list(range(world)),
                                  backend=lambda L, r: OracleShard(L, r), reorder=reorder)
         st.load(orc.haar_state(n, 2))
-        st.apply_records(recs)
+        circuit_of(n, recs).update_quantum_state(st)
         ref = _reference(n, recs, 2)
         assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
 
@@ -260,10 +262,12 @@ def test_gloo_processes_match_oracle(world):
     ref = _reference(n, random_records(n, 40, seed=77), 5)
     terms = [(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])]
     e_ref = orc.expectation(ref, ref, n, terms)
-    for rank, vec, norm, e, stats in res:
+    tf_ref = orc.expectation(ref, ref, n, tfim_terms(n)).real
+    for rank, vec, norm, (e, e_tf), stats in res:
         assert np.max(np.abs(vec - ref)) <= 1e-12, rank
         assert abs(norm - orc.squared_norm(ref)) <= 1e-12
         assert abs(e - e_ref) <= 1e-11
+        assert abs(e_tf - tf_ref) <= 1e-11
         assert stats["swaps"] > 0
 
 
@@ -292,7 +296,7 @@ def test_multi_qubit_remaps_batch_global_qubits():
     st = ShardedQuantumState(n, world=8, owned=list(range(8)),
                              backend=lambda L, r: OracleShard(L, r), chunk_bytes=64)
     st.load(orc.haar_state(n, 4))
-    st.apply_records(recs)
+    circuit_of(n, recs).update_quantum_state(st)
     ref = orc.run_records(orc.haar_state(n, 4), n, recs)
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
     assert st.stats["remapped_qubits"] > st.stats["swaps"]
@@ -307,7 +311,7 @@ def _worker_k(rank, world, port, n, q):
         recs = orc.cz_ladder_records(n, 3, seed=3)
         st = ShardedQuantumState(n, backend=lambda L, r: OracleShard(L, r), chunk_bytes=96)
         st.load(orc.haar_state(n, 6))
-        st.apply_records(recs)
+        circuit_of(n, recs).update_quantum_state(st)
         q.put((rank, st.get_vector(), dict(st.stats)))
     finally:
         dist.destroy_process_group()
@@ -329,3 +333,56 @@ def test_gloo_multi_qubit_remap_processes():
     for rank, vec, stats in res:
         assert np.max(np.abs(vec - ref)) <= 1e-12, rank
         assert stats["remapped_qubits"] > stats["swaps"]
+
+
+@pytest.mark.parametrize("n,world", [(6, 2), (8, 4), (9, 8)])
+def test_sharded_tfim_expectation(n, world):
+    """Observables with X on every qubit (TFIM, sum_i X_i): the union of the
+    X/Y supports exceeds a shard, so terms are grouped and each group is
+    brought local by its own remap; the state itself is unchanged (only the
+    qubit map moves)."""
+    recs = random_records(n, 50, seed=n + 3 * world)
+    st = ShardedQuantumState(n, world=world, owned=list(range(world)),
+                             backend=lambda L, r: OracleShard(L, r))
+    st.set_Haar_random_state(9)
+    circuit_of(n, recs).update_quantum_state(st)
+    ref = _reference(n, recs, 9)
+    for terms in (tfim_terms(n), [(1.0, [(i, 1)]) for i in range(n)],
+                  [(0.5, [(i, 2), ((i + 1) % n, 2)]) for i in range(n)]):
+        e = observable_of(n, terms).get_expectation_value(st)
+        assert isinstance(e, float)
+        assert abs(e - orc.expectation(ref, ref, n, terms).real) <= 1e-11
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+    with pytest.raises(ValueError):  # one term wider than a shard
+        observable_of(n, [(1.0, [(i, 1) for i in range(n)])]).get_expectation_value(st)
+
+
+def test_sharded_state_reference_api():
+    """The reference calls reach the sharded engine: gate / circuit
+    update_quantum_state, Observable.get_expectation_value, get_qubit_count;
+    maps and transition amplitudes between sharded states are refused."""
+    from paper_2011_13524_b200 import GeneralQuantumOperator, QuantumCircuit, gate
+    n, world = 6, 4
+    st = ShardedQuantumState(n, world=world, owned=list(range(world)),
+                             backend=lambda L, r: OracleShard(L, r))
+    assert st.get_qubit_count() == n
+    st.set_computational_basis(5)
+    gate.H(n - 1).update_quantum_state(st)  # global qubit: a remap
+    gate.CNOT(n - 1, 0).update_quantum_state(st)
+    ref = np.zeros(1 << n, dtype=np.complex128)
+    ref[5] = 1
+    ref = orc.run_records(ref, n, [gate.H(n - 1)._core.record(),
+                                   gate.CNOT(n - 1, 0)._core.record()])
+    assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
+    qc = QuantumCircuit(n)
+    qc.add_gate(gate.DepolarizingNoise(0, 0.1))
+    with pytest.raises(ValueError):
+        qc.update_quantum_state(st)
+    op = GeneralQuantumOperator(n)
+    op.add_operator(1.0, "X 0")
+    st2 = ShardedQuantumState(n, world=world, owned=list(range(world)),
+                              backend=lambda L, r: OracleShard(L, r))
+    with pytest.raises(ValueError):
+        op.get_transition_amplitude(st, st2)
+    with pytest.raises(ValueError):
+        QuantumCircuit(n + 1).update_quantum_state(st)

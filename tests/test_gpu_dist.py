@@ -16,7 +16,7 @@ import torch.multiprocessing as mp
 from paper_2011_13524_b200.dist import CudaShard, ShardedQuantumState
 
 from oracle import c_oracle, qsim_oracle as orc
-from dist_util import random_records
+from dist_util import circuit_of, observable_of, random_records, tfim_terms
 
 pytestmark = pytest.mark.gpu
 
@@ -31,14 +31,18 @@ def test_cuda_virtual_ranks(n, world, exchange):
                              backend=lambda L, r: CudaShard(L, 0, stream), exchange=exchange)
     assert st.exchange == exchange
     st.load(orc.haar_state(n, 1))
-    st.apply_records(recs)
+    circuit_of(n, recs).update_quantum_state(st)
     got = st.get_vector()
     ref = c_oracle.run_records(orc.haar_state(n, 1), n, recs)
     assert np.max(np.abs(got - ref)) <= 1e-12
     assert st.stats["swaps"] > 0
     assert abs(st.get_squared_norm() - 1.0) <= 1e-12
     terms = [(0.5, [(n - 1, 1), (0, 3)]), (-1.0, [(n - 2, 2), (1, 1)]), (0.25, [])]
-    assert abs(st.expectation(terms) - orc.expectation(ref, ref, n, terms)) <= 1e-11
+    e = observable_of(n, terms).get_expectation_value(st)
+    assert abs(e - orc.expectation(ref, ref, n, terms)) <= 1e-11
+    tf = tfim_terms(n)  # X on every qubit: groups of terms remapped in turn
+    e = observable_of(n, tf).get_expectation_value(st)
+    assert abs(e - orc.expectation(ref, ref, n, tf).real) <= 1e-11
 
 
 def test_cuda_sharded_cz_ladder():
@@ -49,7 +53,7 @@ def test_cuda_sharded_cz_ladder():
     st = ShardedQuantumState(n, world=world, owned=list(range(world)),
                              backend=lambda L, r: CudaShard(L, 0, stream))
     st.set_zero_state()
-    st.apply_records(recs)
+    circuit_of(n, recs).update_quantum_state(st)
     ref = c_oracle.run_records(orc.zero_state(n), n, recs)
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
 
@@ -63,8 +67,9 @@ def test_cuda_sharded_per_gate_mode():
     st = ShardedQuantumState(n, world=world, owned=list(range(world)),
                              backend=lambda L, r: CudaShard(L, 0, stream, use_tiles=0, fuse=0))
     st.load(orc.haar_state(n, 2))
-    for r in recs:
-        st.apply_records([r])
+    from paper_2011_13524_b200 import QuantumGateBase
+    for g in circuit_of(n, recs)._core.gates:  # gate.update_quantum_state(state)
+        QuantumGateBase(g).update_quantum_state(st)
     ref = c_oracle.run_records(orc.haar_state(n, 2), n, recs)
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
 
@@ -111,10 +116,10 @@ def _ipc_worker(rank, world, port, n, q, overlap_min=20):
         st = ShardedQuantumState(n, exchange="p2p", overlap_min_qubits=overlap_min)
         recs = random_records(n, 60, seed=31)
         st.load(orc.haar_state(n, 6))
-        st.apply_records(recs)
+        circuit_of(n, recs).update_quantum_state(st)
         vec = st.get_vector()
         norm = st.get_squared_norm()
-        e = st.expectation([(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])])
+        e = observable_of(n, [(0.3, [(n - 1, 1), (0, 3)]), (0.9, [(1, 2)])]).get_expectation_value(st)
         stats = dict(st.stats)
         mode = st.exchange
         st.close()
@@ -155,29 +160,45 @@ def test_ipc_processes_p2p_exchange(world, overlap_min):
         assert (stats.get("overlapped", 0) > 0) == (overlap_min < 20)
 
 
+_CFG5_REF = {}
+
+
+def _cfg5_reference(n):
+    """cz-ladder(n, depth 20, seed 1) from |0> by the plain-C oracle
+    (computed once per session, shared by the P = 2/4/8 cases)."""
+    if n not in _CFG5_REF:
+        from paper_2011_13524_b200 import workloads
+        from paper_2011_13524_b200._circuit import circuit_records
+        recs = circuit_records(workloads.generate_cz_ladder(n, 20, seed=1))
+        _CFG5_REF[n] = c_oracle.run_records(orc.zero_state(n), n, recs)
+    return _CFG5_REF[n]
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_cfg5_shape_sharded_matches_single_state(world):
+def test_cfg5_shape_sharded_matches_oracle(world):
     """cfg5's workload shape at n=24 (the sharded engine at
-    n<=24 on P=2/4/8): cz-ladder(24, depth 20, seed 1) over P virtual ranks
-    (p2p remaps, rank-specialised tiled segments) against the single-state
-    engine, itself pinned to the C oracle at n=30 (profiles/r1_parity_n30.json)."""
+    n<=24 on P=2/4/8 vs the oracle): cz-ladder(24, depth 20, seed 1) over P
+    virtual ranks (p2p remaps, rank-specialised tiled segments), driven
+    through circuit.update_quantum_state / Observable.get_expectation_value,
+    against the plain-C oracle at 1e-12 (amplitudes) and 1e-10 relative
+    (TFIM energy)."""
     import torch
-    import paper_2011_13524_b200 as qs
     from paper_2011_13524_b200 import workloads
-    from paper_2011_13524_b200._circuit import circuit_records
     n = 24
+    ref = _cfg5_reference(n)
     circ = workloads.generate_cz_ladder(n, 20, seed=1)
-    one = qs.QuantumState(n)
-    circ.update_quantum_state(one)
-    ref = one.get_vector()
     stream = torch.cuda.current_stream().cuda_stream
     st = ShardedQuantumState(n, world=world, owned=list(range(world)),
                              backend=lambda L, r: CudaShard(L, 0, stream))
     st.set_zero_state()
-    st.apply_records(circuit_records(circ))
+    circ.update_quantum_state(st)
     assert st.exchange == "p2p" and st.stats["swaps"] > 0
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
     assert abs(st.get_squared_norm() - 1.0) <= 1e-12
+    tf = tfim_terms(n)
+    e = observable_of(n, tf).get_expectation_value(st)
+    e_ref = orc.expectation(ref, ref, n, tf).real
+    assert abs(e - e_ref) <= 1e-10 * max(abs(e_ref), 1e-6 * sum(abs(c) for c, _ in tf))
 
 
 @pytest.mark.parametrize("n,world,bits", [(16, 2, 1), (18, 4, 2), (20, 8, 3)])
@@ -197,27 +218,23 @@ def test_cuda_overlapped_remaps(n, world, bits):
         else:
             st.load(orc.haar_state(n, seed))
             ref = c_oracle.run_records(orc.haar_state(n, seed), n, recs)
-        st.apply_records(recs)
+        circuit_of(n, recs).update_quantum_state(st)
         assert st.stats.get("overlapped", 0) > 0
         assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
         assert abs(st.get_squared_norm() - 1.0) <= 1e-12
 
 
-def test_cfg5_shape_overlapped_matches_single_state():
+def test_cfg5_shape_overlapped_matches_oracle():
     """cz-ladder(24, 20) over 4 virtual ranks with every eligible exchange
-    step overlapped (L = 22, blocks of 2^20) against the single-state engine."""
-    import paper_2011_13524_b200 as qs
+    step overlapped (L = 22, blocks of 2^20) against the plain-C oracle."""
     from paper_2011_13524_b200 import workloads
-    from paper_2011_13524_b200._circuit import circuit_records
     n = 24
+    ref = _cfg5_reference(n)
     circ = workloads.generate_cz_ladder(n, 20, seed=1)
-    one = qs.QuantumState(n)
-    circ.update_quantum_state(one)
-    ref = one.get_vector()
     st = ShardedQuantumState(n, world=4, owned=[0, 1, 2, 3], overlap=True,
                              overlap_min_qubits=16)
     st.set_zero_state()
-    st.apply_records(circuit_records(circ))
+    circ.update_quantum_state(st)
     assert st.stats.get("overlapped", 0) > 0
     assert np.max(np.abs(st.get_vector() - ref)) <= 1e-12
 

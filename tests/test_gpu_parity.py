@@ -21,7 +21,8 @@ from paper_2011_13524_b200.quantum_operator import create_quantum_operator_from_
 from paper_2011_13524_b200.state import inner_product
 
 from oracle import c_oracle, qsim_oracle as orc
-from golden_util import build_gate, load_circuits, load_gate_cases, load_haar, load_observables
+from golden_util import (build_gate, cfg1_digest, load_cfg1, load_circuits, load_gate_cases,
+                         load_haar, load_observables)
 
 pytestmark = pytest.mark.gpu
 
@@ -36,7 +37,11 @@ def haar(n, seed):
 
 
 def close_expect(got, ref, scale):
-    return abs(got - ref) <= 1e-10 * max(abs(ref), scale)
+    """North-star bar: 1e-10 relative.  Only when the reference value is
+    itself tiny (|ref| < 1e-6 * sum|c|, e.g. an exactly cancelling sum) is
+    the relative bar taken against that floor instead (reference
+    test_observable.py:69-85)."""
+    return abs(got - ref) <= 1e-10 * max(abs(ref), 1e-6 * scale)
 
 
 # ----------------------------------------------------------------- golden
@@ -108,7 +113,7 @@ def test_golden_observables():
         n = case["n"]
         v = workloads.tfim_observable(n).get_expectation_value(haar(n, case["seed"]))
         assert isinstance(v, float)
-        assert close_expect(v, case["value"], 1.5 * n)
+        assert close_expect(v, case["value"], 1.5 * n - 1)
     op = create_quantum_operator_from_openfermion_text(data["hamiltonian_text"])
     assert abs(op.get_expectation_value(qs.QuantumState(4))) <= 1e-9
     assert close_expect(op.get_expectation_value(haar(4, 5)),
@@ -125,7 +130,7 @@ def test_golden_vqe(n):
     st = qs.QuantumState(n)
     circ.update_quantum_state(st)
     v = workloads.tfim_observable(n).get_expectation_value(st)
-    assert close_expect(v, ref[n]["value"], 1.5 * n), (v, ref[n]["value"])
+    assert close_expect(v, ref[n]["value"], 1.5 * n - 1), (v, ref[n]["value"])
     # parameter update invalidates the compiled program
     circ.set_parameter(0, circ.get_parameter(0) + 0.1)
     st2 = qs.QuantumState(n)
@@ -263,6 +268,87 @@ def test_cz_ladder_fused_n20_vs_oracle():
     assert np.max(np.abs(st.get_vector() - ref)) <= AMP_TOL
 
 
+_CFG1 = load_cfg1()
+
+
+@pytest.mark.parametrize("case", [c["id"] for c in _CFG1[0]["cases"]])
+def test_cfg1_cnot_ring_golden(case):
+    """cfg1 (BASELINE configs[0]): cnot-ring(16) seeds 0..4, from |0> and from
+    a Haar start, through the public API and the default planner, against
+    the reference's own outputs (tests/golden/cfg1.*): sampled amplitudes and
+    <Z_q> at 1e-12, random projections <w|psi> (every amplitude moves them) at
+    1e-11, and the whole state against the plain-C oracle at 1e-12."""
+    meta, outs = _CFG1
+    e = next(c for c in meta["cases"] if c["id"] == case)
+    n = 16
+    circ = workloads.generate_cnot_ring(n, seed=e["seed"])
+    assert circ.get_gate_count() == e["gate_count"]
+    st = qs.QuantumState(n)
+    if e["start_seed"] is not None:
+        st.set_Haar_random_state(e["start_seed"])
+    circ.update_quantum_state(st)
+    got = st.get_vector()
+    dg = cfg1_digest(got)
+    assert np.array_equal(dg["idx"], outs[f"{case}/idx"])
+    assert np.max(np.abs(dg["amps"] - outs[f"{case}/amps"])) <= AMP_TOL
+    assert np.max(np.abs(dg["proj"] - outs[f"{case}/proj"])) <= 1e-11
+    assert np.max(np.abs(dg["z"] - outs[f"{case}/z"])) <= AMP_TOL
+    assert abs(dg["norm2"][0] - outs[f"{case}/norm2"][0]) <= AMP_TOL
+    start = (orc.zero_state(n) if e["start_seed"] is None
+             else orc.haar_state(n, e["start_seed"]))
+    ref = c_oracle.run_records(start, n, circuit_records(circ))
+    assert np.max(np.abs(got - ref)) <= AMP_TOL
+
+
+def test_cz_ladder_n26_depth20_vs_c_oracle():
+    """cfg4's circuit family at full depth: cz-ladder(26, depth 20, seed 1)
+    from |0> through the default planner (fusion, real frames, tile passes)
+    against the plain-C oracle gate by gate, every amplitude at 1e-12."""
+    n = 26
+    circ = workloads.generate_cz_ladder(n, 20, seed=1)
+    st = qs.QuantumState(n)
+    circ.update_quantum_state(st)
+    got = st.get_vector()
+    ref = c_oracle.run_records(orc.zero_state(n), n, circuit_records(circ))
+    err = float(np.max(np.abs(got - ref)))
+    assert err <= AMP_TOL, err
+
+
+def _max_abs_diff(a, b, chunk_qubits=24):
+    """max |a - b| over two device states, read back block by block."""
+    n = a.get_qubit_count()
+    k = min(n, chunk_qubits)
+    worst = 0.0
+    for off in range(0, 1 << n, 1 << k):
+        va = a._view(off, k).get_vector()
+        vb = b._view(off, k).get_vector()
+        worst = max(worst, float(np.max(np.abs(va - vb))))
+    return worst
+
+
+def test_cfg4_full_size_planner_vs_per_gate_n30():
+    """BASELINE cfg4 at full size, cz-ladder(30, depth 20, seed 1): the
+    default planner (fusion, real frames, tile passes) against the per-gate
+    kernels (no fusion, no tiles) -- each gate kind of which is pinned to the
+    reference by test_golden_gate_cases -- on every amplitude at 1e-12.  Not
+    a mirror test, so a sign-convention error in either path shows."""
+    n = 30
+    circ = workloads.generate_cz_ladder(n, 20, seed=1)
+    a = qs.QuantumState(n)
+    a.set_random_state_device(11)
+    b = a.copy()
+    circ.update_quantum_state(a)
+    per_gate = qs.QuantumCircuit(n)
+    for g in circ._core.gates:
+        per_gate.add_gate(g)
+    per_gate.set_plan_options(use_tiles=0, fuse=0, real_frames=0)
+    assert per_gate.program_stats()["num_tile_passes"] == 0
+    per_gate.update_quantum_state(b)
+    err = _max_abs_diff(a, b)
+    assert err <= AMP_TOL, err
+    assert abs(a.get_squared_norm() - 1.0) <= 1e-12
+
+
 def test_unfused_cz_ladder_n22_vs_oracle():
     n = 22
     circ = workloads.generate_cz_ladder(n, 4, seed=2)
@@ -354,6 +440,60 @@ def test_program_stats_and_reuse():
     circ.update_quantum_state(a)
     circ.update_quantum_state(b)
     assert np.array_equal(a.get_vector(), b.get_vector())
+
+
+def test_graph_replay_on_reused_buffers():
+    """A program's CUDA graph bakes in the state's amplitude buffer and its
+    tile work counter.  Run one circuit twice on state A (the second run
+    captures the graph), destroy A, then run it on fresh states that may
+    reuse A's pooled blocks: every result equals the oracle."""
+    import gc
+    n = 14
+    circ = workloads.generate_cz_ladder(n, 6, seed=2)
+    ref = c_oracle.run_records(orc.haar_state(n, 3), n, circuit_records(circ))
+    a = haar(n, 3)
+    circ.update_quantum_state(a)
+    a.set_Haar_random_state(3)
+    circ.update_quantum_state(a)  # graph captured here
+    assert np.max(np.abs(a.get_vector() - ref)) <= AMP_TOL
+    del a
+    gc.collect()
+    for _ in range(4):
+        junk = [qs.QuantumState(n) for _ in range(3)]  # shuffle the pool
+        b = haar(n, 3)
+        circ.update_quantum_state(b)
+        assert np.max(np.abs(b.get_vector() - ref)) <= AMP_TOL
+        del junk, b
+        gc.collect()
+
+
+def test_copy_and_add_ordered_on_nonblocking_streams():
+    """copy() / add_state read another state on the destination's stream;
+    work queued afterwards on the source's (non-blocking) stream must not
+    overtake the read, and destroying the source right away is safe."""
+    import torch
+    n = 22
+    for _ in range(3):
+        src = haar(n, 7)
+        s = torch.cuda.Stream()
+        src.set_stream(s.cuda_stream)
+        expect = src.get_vector()
+        dup = src.copy()
+        for q in range(n):  # overwrite the source right after the copy
+            qg.H(q).update_quantum_state(src)
+        del src
+        assert np.array_equal(dup.get_vector(), expect)
+        acc = qs.QuantumState(n)
+        acc.set_zero_state()
+        other = haar(n, 8)
+        other.set_stream(torch.cuda.Stream().cuda_stream)
+        before = other.get_vector()
+        acc.add_state(other)
+        for q in range(n):
+            qg.X(q).update_quantum_state(other)
+        want = before.copy()
+        want[0] += 1.0
+        assert np.max(np.abs(acc.get_vector() - want)) <= 1e-15
 
 
 @pytest.mark.parametrize("m,nc", [(1, 0), (2, 1), (5, 0), (7, 2), (10, 0)])

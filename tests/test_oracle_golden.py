@@ -109,3 +109,22 @@ def test_cfg3_reference_value_recorded():
     if 24 in vqe:
         assert vqe[24]["value"] == pytest.approx(-0.201996915076406, abs=1e-14)
     assert vqe[8]["gates"] == 92 and vqe[12]["params"] == 96
+
+
+def test_cfg1_oracle_matches_reference():
+    """The numpy oracle reproduces the reference's cfg1 digests (cnot-ring(16)
+    seeds 0..4, from |0> and Haar starts; tests/golden/cfg1.*)."""
+    from paper_2011_13524_b200 import workloads
+    from paper_2011_13524_b200._circuit import circuit_records
+    from golden_util import cfg1_digest, load_cfg1
+    meta, outs = load_cfg1()
+    assert len(meta["cases"]) == 10
+    for e in meta["cases"]:
+        n = 16
+        recs = circuit_records(workloads.generate_cnot_ring(n, seed=e["seed"]))
+        start = orc.zero_state(n) if e["start_seed"] is None else orc.haar_state(n, e["start_seed"])
+        dg = cfg1_digest(orc.run_records(start, n, recs))
+        key = e["id"]
+        assert np.max(np.abs(dg["amps"] - outs[f"{key}/amps"])) <= 1e-15, key
+        assert np.max(np.abs(dg["proj"] - outs[f"{key}/proj"])) <= 1e-13, key
+        assert np.max(np.abs(dg["z"] - outs[f"{key}/z"])) <= 1e-15, key
