@@ -22,6 +22,7 @@ same metric on a bounded sample of the same sweep.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import math
 import os
@@ -68,14 +69,45 @@ def measured_peaks():
 
 
 def fp64_peak():
-    """Sustained FP64 FMA peak measured by profiles/micro/fp64_peak.cu."""
+    """Sustained FP64 DFMA peak measured by profiles/fp64_peak.py (the tile
+    passes of a circuit run back to back for seconds, so the sustained
+    figure is the denominator); the clocks it ran at are in the same file."""
     path = os.path.join(ROOT, "profiles", "fp64_peak.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return float(d["fp64_tflops_sustained"]), "measured sustained (profiles/fp64_peak.json)"
+        clk = d.get("clocks", {})
+        return (float(d["fp64_tflops_sustained"]),
+                f"measured sustained DFMA (profiles/fp64_peak.json, SM clock median "
+                f"{clk.get('sm_mhz')} MHz, reasons {clk.get('reasons')})")
     except Exception:
-        return 32.3, "measured burst (DESIGN.md)"
+        return 32.3, "measured burst (DESIGN.md; profiles/fp64_peak.json absent)"
+
+
+def cpu_circuit_baselines():
+    """Random-circuit CPU baselines: a live run of cfg1 (cnot-ring(16) seed 1,
+    full circuit, reference time_circuit semantics, QSIM_NUM_THREADS = 1 and
+    nproc) with the reference itself, plus the cfg1/cfg3/cfg4 record that
+    profiles/cpu_baselines.py wrote on a GPU box this round."""
+    out = {"cores": os.cpu_count() or 1, "cpu_model": cpu_model()}
+    core = reference_core()
+    if core is not None:
+        import qsimcore.bench as rb
+        live = {}
+        for th in (1, os.cpu_count() or 1):
+            core.config.set_num_threads(th)
+            circ = rb.generate_cnot_ring(16, seed=1)
+            best = min(rb.time_circuit(circ, 3))
+            live[f"threads={th}"] = {"circuit_s": best, "sec_per_layer": best / 11}
+        out["live_cfg1"] = {"kind": "reference", "workload": "cnot-ring n=16 seed=1, full",
+                            "semantics": "qsimcore.bench.time_circuit, min of 3", **live}
+    else:
+        out["live_cfg1"] = None
+    rec = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_cpu_baselines.json")))
+    if rec:
+        with open(rec[-1]) as fh:
+            out["recorded"] = {"file": os.path.relpath(rec[-1], ROOT), **json.load(fh)}
+    return out
 
 
 class ClockSampler:
@@ -138,27 +170,106 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def sweep_config(n, world):
+    """``config`` of the headline line; the reference arm prints the same
+    object (same workload), its per-step sample is described outside it."""
+    return {"workload": f"cfg2 per-gate sweep: 5 gates x {n} targets, n={n} qubits per GPU",
+            "qubits": n, "gates_per_step": 5 * n, "bytes_per_step": sweep_bytes(n),
+            "l2": "state 16*2^n B >> 126 MB L2, no flush needed",
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
+
+
+def sweep_bytes(n):
+    return sum(gate_bytes(k, n) for k, _, _ in sweep_spec(n))
+
+
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference algorithm (numpy port in oracle/) on host cores
-def cpu_sweep_sample(n, num_gates, threads, start=0, amps=None):
-    """Time ``num_gates`` gates of the cfg2 sweep at width n with the oracle
-    port; returns (bytes, seconds, description)."""
-    from oracle import qsim_oracle as orc
-    orc.set_threads(threads)
-    if amps is None:
-        amps = np.full(1 << n, (1.0 + 0.0j) / math.sqrt(1 << n), dtype=np.complex128)
+# CPU baseline: the reference implementation (qsimcore, installed unmodified
+# into baseline/_ref) on the host cores; the numpy port in oracle/ only when
+# that install is absent.
+def reference_core():
+    """qsimcore from baseline/_ref, or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "qsimcore")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import qsimcore
+        import qsimcore.bench  # noqa: F401
+    except Exception:  # noqa: BLE001
+        return None
+    return qsimcore
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _sweep_picks(n, num_gates, start, stride=37):
+    """Gate s of the sample = spec[(start + s) * 37 % 5n]: 37 is coprime with
+    5n for n = 28, so consecutive steps walk the whole 140-gate mix (every
+    kind on every target) rather than the low targets only."""
     spec = sweep_spec(n)
-    # spread the sample over kinds and targets
-    picks = [spec[(start + i * 37) % len(spec)] for i in range(num_gates)]
+    return [spec[((start + i) * stride) % len(spec)] for i in range(num_gates)]
+
+
+class _CpuSweep:
+    """Applies cfg2 sweep gates to one host state with the reference
+    (kind "reference") or the oracle port (kind "port")."""
+
+    def __init__(self, n, threads):
+        self.n = n
+        self.core = reference_core()
+        self.kind = "reference" if self.core is not None else "port"
+        if self.core is not None:
+            self.core.config.set_num_threads(threads)
+            self.state = self.core.StateVector(n)
+            self.state.load(np.full(1 << n, (1.0 + 0.0j) / math.sqrt(1 << n)))
+        else:
+            from oracle import qsim_oracle as orc
+            orc.set_threads(threads)
+            self.orc = orc
+            self.amps = np.full(1 << n, (1.0 + 0.0j) / math.sqrt(1 << n), dtype=np.complex128)
+
+    def apply(self, kind, t, theta):
+        n = self.n
+        if self.core is None:
+            self.orc.apply_record(self.amps, n, _oracle_record(kind, t, theta, n))
+            return
+        c = self.core
+        g = {"H": lambda: c.H(t), "RX": lambda: c.RX(t, theta), "RZ": lambda: c.RZ(t, theta),
+             "CNOT": lambda: c.CNOT((t + 1) % n, t), "CZ": lambda: c.CZ(t, (t + 1) % n)}[kind]()
+        g.apply(self.state)
+
+    def describe(self):
+        if self.core is not None:
+            return (f"reference qsimcore ({os.path.relpath(self.core.__file__, ROOT)}), "
+                    "QSIM_NUM_THREADS=nproc")
+        return ("numpy port of the qsimcore kernels (oracle/qsim_oracle.py), reference "
+                "thread chunking with nproc threads (baseline/_ref absent)")
+
+
+def cpu_sweep_sample(n, num_gates, threads, start=0, runner=None):
+    """Time ``num_gates`` gates of the cfg2 sweep at width n on the host;
+    returns (bytes, seconds, description, runner)."""
+    runner = runner or _CpuSweep(n, threads)
     tot_b = tot_s = 0.0
+    picks = _sweep_picks(n, num_gates, start)
     for kind, t, theta in picks:
-        rec = _oracle_record(kind, t, theta, n)
         t0 = time.perf_counter()
-        orc.apply_record(amps, n, rec)
+        runner.apply(kind, t, theta)
         tot_s += time.perf_counter() - t0
         tot_b += gate_bytes(kind, n)
     desc = ", ".join(f"{k}@{t}" for k, t, _ in picks)
-    return tot_b, tot_s, desc
+    return tot_b, tot_s, desc, runner
 
 
 def _oracle_record(kind, t, theta, n):
@@ -175,37 +286,40 @@ def _oracle_record(kind, t, theta, n):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference CPU algorithm, rank 0 only."""
+    """--impl reference: the reference CPU implementation (qsimcore from
+    baseline/_ref) on the host cores, rank 0 only.  Each step applies
+    ``--ref-gates-per-step`` gates of the same 140-gate sweep, walking the
+    whole mix across steps (_sweep_picks), at the same n."""
     if rank != 0:
         return
     n = args.qubits
     threads = os.cpu_count() or 1
     steps, warm = args.steps, args.warmup
-    # each step = a bounded sample of the sweep (1 gate at 28 qubits)
     per_step = max(1, args.ref_gates_per_step)
-    amps = np.full(1 << n, (1.0 + 0.0j) / math.sqrt(1 << n), dtype=np.complex128)
-    for w in range(warm):
-        cpu_sweep_sample(min(n, 20), per_step, threads, start=w)
+    small = None
+    for w in range(warm):  # warm-up at n=20 (imports, thread pools, page cache)
+        _, _, _, small = cpu_sweep_sample(min(n, 20), per_step, threads, start=w, runner=small)
+    runner = _CpuSweep(n, threads)
     tb = ts = 0.0
     descs = []
     for s in range(steps):
-        b, t, d = cpu_sweep_sample(n, per_step, threads, start=s * per_step, amps=amps)
+        b, t, d, _ = cpu_sweep_sample(n, per_step, threads, start=s * per_step, runner=runner)
         tb += b
         ts += t
         descs.append(d)
     value = tb / ts / 1e9
+    sample = (f"{steps} steps x {per_step} gate(s) of the n={n} sweep, gate s = sweep "
+              f"spec[37*s mod {5 * n}] (all kinds and targets): " + "; ".join(descs))
     line = {
         "impl": "reference",
         "metric": "per-gate HBM GB/s vs 8 TB/s peak (cfg2 28-qubit H/RX/RZ/CNOT/CZ sweep)",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": ts / steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (uniform superposition)",
-        "config": {"workload": f"cfg2 per-gate sweep, n={n}", "qubits": n,
-                   "sample": f"{per_step} gate(s)/step: " + "; ".join(descs)},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{steps} steps x {per_step} gate(s) at n={n}, "
-                                   "numpy port of qsimcore kernels (oracle/qsim_oracle.py), "
-                                   "reference thread chunking with QSIM_NUM_THREADS=nproc"},
+        "config": sweep_config(n, world),
+        "sample": sample,
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": runner.kind,
+                         "cpu_model": cpu_model(), "sample": sample + "; " + runner.describe()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -362,12 +476,14 @@ def run_ours(args, rank, world, local_rank):
         del st
         torch.cuda.empty_cache()
     if rank == 0 and not args.skip_cpu:
-        b, s, desc = cpu_sweep_sample(n, args.cpu_gates, os.cpu_count() or 1)
+        b, s, desc, runner = cpu_sweep_sample(n, args.cpu_gates, os.cpu_count() or 1)
         cpu = {"value": b / s / 1e9, "unit": "GB/s", "cores": os.cpu_count() or 1,
-               "kind": "port",
-               "sample": f"{args.cpu_gates} gates of the n={n} sweep ({desc}); numpy port "
-                         "of the qsimcore kernels (oracle/qsim_oracle.py), reference "
-                         "thread chunking with nproc threads"}
+               "kind": runner.kind, "cpu_model": cpu_model(),
+               "sample": f"{args.cpu_gates} gates of the n={n} sweep spread over kinds and "
+                         f"targets ({desc}); {runner.describe()}"}
+        del runner
+        if "random_circuit" in extra:
+            extra["random_circuit"]["cpu_baseline"] = cpu_circuit_baselines()
     else:
         cpu = None
 
@@ -380,11 +496,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (device-generated random state)",
-        "config": {"workload": f"cfg2 per-gate sweep: 5 gates x {n} targets, n={n} qubits "
-                               "per GPU", "qubits": n, "gates_per_step": len(gates),
-                   "bytes_per_step": bytes_step,
-                   "l2": "state 16*2^n B >> 126 MB L2, no flush needed",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+        "config": sweep_config(n, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_pair2x2 (1-qubit dense: H, RX)", "launches": dom_n,
