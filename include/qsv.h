@@ -212,7 +212,11 @@ typedef struct qsv_plan_opts {
   int32_t use_graph;      /* 1: replay through a CUDA graph                */
   int32_t real_frames;    /* 1: run 1-qubit gates as real rotations with   */
                           /*    their phases merged into diagonal flushes */
-  int32_t reserved;       /* 0                                             */
+  int32_t jit;            /* tile passes as runtime-compiled straight-line */
+                          /* kernels (NVRTC, cached by structure):        */
+                          /* 0 off (interpreter), 1 auto: from the second */
+                          /* run (or the first when every pass is cached),*/
+                          /* 2 eager: compiled at qsv_program_create      */
   uint64_t outer_mask;    /* qubits never chosen as tile qubits, so the    */
                           /* program can run on the block of amplitudes   */
                           /* with those bits fixed (qsv_program_run_fixed) */
@@ -225,6 +229,8 @@ typedef struct qsv_program_stats {
   int32_t num_gate_kernels;
   double hbm_bytes;       /* algorithmic HBM bytes per run                 */
   double fp64_flops;      /* FP64 flops per run (2 per FMA), planner count */
+  int32_t num_jit_passes; /* tile passes running as generated kernels      */
+  int32_t reserved;
 } qsv_program_stats;
 
 int qsv_program_create(int num_qubits, const qsv_op* ops, int nops,
@@ -243,6 +249,11 @@ int qsv_program_destroy(qsv_program* prog);
 /* Host-only: plan without touching a device (stats only). */
 int qsv_plan_stats(int num_qubits, const qsv_op* ops, int nops, const qsv_plan_opts* opts,
                    qsv_program_stats* out);
+
+/* Generated tile-pass kernels compiled by NVRTC in this process (misses of
+ * both caches), loaded from the on-disk cubin cache, and reused from the
+ * in-process cache (qsv_plan_opts.jit).  No GPU needed. */
+int qsv_jit_stats(long* compiles, long* disk_hits, long* mem_hits);
 
 /* --------------------------------------------------------------- sharding
  * Exchange primitives of the sharded engine (dist.py; no reference

@@ -77,16 +77,19 @@ def _fill_ops_uncached(gates):
 class _Program:
     """Owner of one native program handle."""
 
-    __slots__ = ("h", "stats")
+    __slots__ = ("h",)
 
     def __init__(self, n, gates, opts, cache_owner=None):
         ops = fill_ops(gates, cache_owner)
         h = C.c_void_p()
         check(lib.qsv_program_create(n, ops, len(gates), C.byref(opts), C.byref(h)))
         self.h = h
+
+    @property
+    def stats(self) -> dict:
         st = _lib.QsvProgramStats()
-        check(lib.qsv_program_stats_get(h, C.byref(st)))
-        self.stats = {f: getattr(st, f) for f, _ in _lib.QsvProgramStats._fields_}
+        check(lib.qsv_program_stats_get(self.h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in _lib.QsvProgramStats._fields_ if f != "reserved"}
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -105,6 +108,7 @@ def default_plan_opts(**kw) -> _lib.QsvPlanOpts:
     o.fuse = int(kw.get("fuse", 1))
     o.use_graph = int(kw.get("use_graph", 1))
     o.real_frames = int(kw.get("real_frames", 1))
+    o.jit = int(kw.get("jit", 1))
     return o
 
 
@@ -173,7 +177,9 @@ class Circuit:
 
     # -- execution -------------------------------------------------------------
     def set_plan_options(self, **kw) -> None:
-        """Engine knobs: use_tiles, tile_qubits, fuse, use_graph, real_frames."""
+        """Engine knobs: use_tiles, tile_qubits, fuse, use_graph, real_frames,
+        jit (0 interpreter only, 1 generated pass kernels from the second
+        run, 2 compiled at program creation)."""
         self._plan = default_plan_opts(**kw)
         self._prog = None
 
@@ -211,7 +217,7 @@ class Circuit:
         prog = self.compile()
         if isinstance(prog, _Program):
             return dict(prog.stats)
-        total = {f: 0 for f, _ in _lib.QsvProgramStats._fields_}
+        total = {f: 0 for f, _ in _lib.QsvProgramStats._fields_ if f != "reserved"}
         for st in prog:
             if isinstance(st, _Program):
                 for k, v in st.stats.items():
@@ -227,7 +233,7 @@ class Circuit:
         st = _lib.QsvProgramStats()
         check(lib.qsv_plan_stats(self.num_qubits, ops, len(basic), C.byref(opts),
                                  C.byref(st)))
-        return {f: getattr(st, f) for f, _ in _lib.QsvProgramStats._fields_}
+        return {f: getattr(st, f) for f, _ in _lib.QsvProgramStats._fields_ if f != "reserved"}
 
     def update_state(self, state, rng=None) -> None:
         """circuit.py:48-55: one generator (seed / Generator / None) shared by

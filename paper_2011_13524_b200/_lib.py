@@ -54,7 +54,7 @@ class QsvPlanOpts(C.Structure):
         ("fuse", C.c_int32),
         ("use_graph", C.c_int32),
         ("real_frames", C.c_int32),
-        ("reserved", C.c_int32),
+        ("jit", C.c_int32),
         ("outer_mask", C.c_uint64),
     ]
 
@@ -67,6 +67,8 @@ class QsvProgramStats(C.Structure):
         ("num_gate_kernels", C.c_int32),
         ("hbm_bytes", C.c_double),
         ("fp64_flops", C.c_double),
+        ("num_jit_passes", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -137,6 +139,7 @@ _SIGS = {
     "qsv_program_destroy": ([_P], _I),
     "qsv_plan_stats": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts),
                         C.POINTER(QsvProgramStats)], _I),
+    "qsv_jit_stats": ([C.POINTER(C.c_long)] * 3, _I),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -185,3 +188,11 @@ def device_count() -> int:
     if rc != QSV_OK:
         return 0
     return out.value
+
+
+def jit_stats() -> dict:
+    """Generated tile-pass kernels: NVRTC compiles, disk-cache and in-process
+    cache hits so far in this process."""
+    a, b, c = C.c_long(), C.c_long(), C.c_long()
+    check(lib.qsv_jit_stats(C.byref(a), C.byref(b), C.byref(c)))
+    return {"compiles": a.value, "disk_hits": b.value, "mem_hits": c.value}

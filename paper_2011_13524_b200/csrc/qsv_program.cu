@@ -36,6 +36,7 @@ struct qsv_program {
   cudaStream_t last_stream = 0;  // the payload is released in this stream's order
   uint64_t runs = 0;
   int device = -1;
+  bool jit_tried = false;  // generated pass kernels compiled / fetched
 };
 
 namespace {
@@ -97,6 +98,43 @@ int upload_payload(qsv_program* p, int dev) {
   p->payload_device = dev;
   p->last_stream = us;
   return QSV_OK;
+}
+
+// Compile (or fetch from the caches) the generated kernel of every tile pass
+// that has one; passes whose compilation fails keep the interpreter.
+int jit_prepare(qsv_program* p) {
+  if (p->jit_tried) return QSV_OK;
+  p->jit_tried = true;
+  std::vector<const std::string*> srcs;
+  std::vector<TilePlan*> tps;
+  for (TilePlan& tp : p->tiles)
+    if (!tp.jit_src.empty() && !tp.jit.kernel) {
+      srcs.push_back(&tp.jit_src);
+      tps.push_back(&tp);
+    }
+  if (srcs.empty()) return QSV_OK;
+  std::vector<JitKernel> ks;
+  std::string err;
+  const int rc = jit_kernels(srcs, ks, &err);
+  if (rc) return rc;
+  int ok = 0;
+  for (size_t i = 0; i < tps.size(); ++i) {
+    tps[i]->jit = ks[i];
+    if (ks[i].kernel) ++ok;
+  }
+  p->stats.num_jit_passes = ok;
+  if (!err.empty() && getenv("QSV_JIT_VERBOSE")) fprintf(stderr, "qsv jit: %s\n", err.c_str());
+  return QSV_OK;
+}
+
+bool jit_all_cached(const qsv_program* p) {
+  bool any = false;
+  for (const TilePlan& tp : p->tiles)
+    if (!tp.jit_src.empty()) {
+      any = true;
+      if (!jit_cached(tp.jit_src)) return false;
+    }
+  return any;
 }
 
 void drop_graph(qsv_program* p) {
@@ -182,7 +220,7 @@ int qsv_plan_stats(int n, const qsv_op* ops, int nops, const qsv_plan_opts* opts
     set_error("bad plan arguments");
     return QSV_EINVAL;
   }
-  qsv_plan_opts o{1, 0, 1, 1, 1};
+  qsv_plan_opts o{1, 0, 1, 1, 1, 1, 0};
   if (opts) o = *opts;
   std::vector<GateDesc> gates;
   int rc = convert_ops(n, ops, nops, gates);
@@ -206,7 +244,7 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
     set_error("bad program arguments");
     return QSV_EINVAL;
   }
-  qsv_plan_opts o{1, 0, 1, 1, 1};
+  qsv_plan_opts o{1, 0, 1, 1, 1, 1, 0};
   if (opts) o = *opts;
   std::vector<GateDesc> gates;
   int rc0 = convert_ops(n, ops, nops, gates);
@@ -232,6 +270,15 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
     return rc;
   }
   p->device = dev;
+  // jit 2: compile now; jit 1: now only if every pass is already loaded
+  // (structure seen before, e.g. a VQE recompile with new angles)
+  if (o.jit == 2 || (o.jit == 1 && jit_all_cached(p))) {
+    rc = jit_prepare(p);
+    if (rc) {
+      qsv_program_destroy(p);
+      return rc;
+    }
+  }
   *out = p;
   return QSV_OK;
 }
@@ -253,6 +300,14 @@ int qsv_program_run(qsv_program* p, qsv_state* st) {
   }
   if (p->payload_ready) QSV_TRY(cudaStreamWaitEvent(st->stream, p->payload_ready, 0));
   p->last_stream = st->stream;
+  // the second run compiles the generated pass kernels (a program that runs
+  // once never pays for NVRTC) -- before the graph capture, so the graph
+  // holds them
+  if (p->opts.jit && p->runs >= 1 && !p->jit_tried) {
+    const int rc = jit_prepare(p);
+    if (rc) return rc;
+    drop_graph(p);
+  }
   // the first run launches directly: a program that runs once (a recompile
   // after set_parameter) never pays for graph capture + instantiation
   if (!p->opts.use_graph || p->steps.empty() || p->runs++ == 0)
@@ -325,6 +380,10 @@ int qsv_program_run_fixed(qsv_program* p, qsv_state* st, uint64_t mask, uint64_t
   if (p->payload_device != st->device && !p->host_payload.empty()) {
     drop_graph(p);
     const int rc = upload_payload(p, st->device);
+    if (rc) return rc;
+  }
+  if (p->opts.jit && p->runs++ >= 1 && !p->jit_tried) {
+    const int rc = jit_prepare(p);
     if (rc) return rc;
   }
   if (p->payload_ready) QSV_TRY(cudaStreamWaitEvent(st->stream, p->payload_ready, 0));

@@ -2,9 +2,11 @@
 // qsv_tile_impl.cuh, compiled as qsv_tile_r4.cu / qsv_tile_r5.cu).
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "qsv_internal.cuh"
+#include "qsv_jit.cuh"
 #include "qsv_program.cuh"
 
 namespace qsv {
@@ -110,6 +112,14 @@ struct TilePlan {
   int ndata = 0;
   int num_gates = 0;
   double hbm_bytes = 0;
+  // runtime-compiled form (qsv_tile_jit.cuh / qsv_jit.cu): generated source,
+  // launch shape, payload passed as the kernel parameter; `jit.kernel` is
+  // set once compiled (until then the interpreter k_tile runs the pass)
+  std::string jit_src;
+  int jit_threads = 0;
+  size_t jit_smem = 0;
+  std::vector<Cplx> jit_data;
+  JitKernel jit;
 };
 
 // per-variant entry points (qsv_tile_r4.cu / qsv_tile_r5.cu)

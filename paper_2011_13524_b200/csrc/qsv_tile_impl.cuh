@@ -24,6 +24,8 @@
 #include <map>
 #include <set>
 #include <cstdlib>
+#include <stdexcept>
+#include <string>
 
 #include "qsv_tile.cuh"
 
@@ -1818,6 +1820,8 @@ void add_gate_step(int n, const GateDesc& g, std::vector<Step>& steps, std::vect
   stats->fp64_flops += gate_fp64_flops(n, g);
 }
 
+#include "qsv_tile_jit.cuh"
+
 }  // namespace
 
 bool tiles_enabled(int n, const qsv_plan_opts& opts) {
@@ -1902,6 +1906,27 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
     TilePlan tp;
     tp.variant = kRegBits;
     tp.L = L;
+    if (opts.jit && sizeof(JitParamHead) + sizeof(double2) * std::max<size_t>(1, e.data.size()) <=
+                        kJitMaxParamBytes) {
+      try {
+        JitSource js = jit_pass_source(e, L);
+        tp.jit_src = std::move(js.src);
+        tp.jit_threads = js.threads;
+        tp.jit_smem = js.smem;
+        tp.jit_data = e.data;
+        if (tp.jit_data.empty()) tp.jit_data.push_back(Cplx{0, 0});
+        if (const char* dir = getenv("QSV_JIT_DUMP")) {  // inspection: one file per pass
+          const std::string path =
+              std::string(dir) + "/pass_r" + std::to_string(kRegBits) + "_" + std::to_string(tiles.size()) + ".cu";
+          if (FILE* f = fopen(path.c_str(), "w")) {
+            fputs(tp.jit_src.c_str(), f);
+            fclose(f);
+          }
+        }
+      } catch (const std::exception&) {
+        tp.jit_src.clear();  // this pass stays on the interpreter
+      }
+    }
     if (mix) {
       for (const TileOp& op : e.ops) {
         const int cnt = __builtin_popcount((uint32_t)op.slots);
@@ -1968,6 +1993,49 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
       pos[np++] = q;
     }
   FixedBits tb = make_fixed(pos, np, fval & fmask);
+  const uint64_t ntiles_all = 1ULL << (n - np);
+  if (tp.jit.kernel) {
+    // generated kernel: same persistent work-counter scheme, payload in the
+    // kernel parameter (constant bank), no program staging in shared memory
+    static thread_local std::vector<char> pbuf;
+    pbuf.resize(sizeof(JitParamHead) + sizeof(double2) * tp.jit_data.size());
+    JitParamHead h;
+    memset(&h, 0, sizeof(h));
+    h.a = amps;
+    h.ntiles = ntiles_all;
+    h.ctr = ctr;
+    h.tb = tb;
+    int dev = 0, num_sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms) : num_sms;
+    // CTAs per SM: registers (64K per SM) and shared memory (227 KB) allow
+    int per_sm = 1;
+    if (tp.jit.regs > 0) {
+      const int regs = ((tp.jit.regs + 7) / 8) * 8;
+      per_sm = std::max(1, std::min(65536 / (regs * tp.jit_threads),
+                                    (int)((227u * 1024u) / (tp.jit_smem + 1024))));
+      per_sm = std::min(per_sm, 8);
+    }
+    if (max_ctas > 0) per_sm = 1;
+    unsigned grid;
+    if (ntiles_all <= (uint64_t)sms * per_sm) {
+      grid = (unsigned)ntiles_all;
+    } else {
+      const uint64_t ctas = (ntiles_all + kGroups - 1) / kGroups;
+      grid = (unsigned)std::min<uint64_t>(ctas, (uint64_t)sms * per_sm);
+      h.nostagger = ntiles_all <= (uint64_t)kGroups * grid;
+    }
+    if (ntiles_all <= (uint64_t)sms * per_sm) h.nostagger = 0;
+    memcpy(pbuf.data(), &h, sizeof(h));
+    memcpy(pbuf.data() + sizeof(h), tp.jit_data.data(), sizeof(double2) * tp.jit_data.size());
+    int rc = jit_set_smem(tp.jit, tp.jit_smem);
+    if (rc) return rc;
+    void* args[] = {pbuf.data()};
+    QSV_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(tp.jit.kernel), dim3(grid),
+                             dim3(tp.jit_threads), args, tp.jit_smem, s));
+    return QSV_OK;
+  }
   const size_t smem = kGroups * (sizeof(double2) << tp.L) + tp.nops * sizeof(TileOp) +
                       tp.ndata * sizeof(double2) + tp.nphases * sizeof(TilePhase);
   if (smem > kTileSmemLimit) {

@@ -1,0 +1,593 @@
+// Tile-pass code generator (included by qsv_tile_impl.cuh inside the variant
+// namespace; host code only).
+//
+// The interpreter k_tile reads every op of a pass from shared memory and
+// dispatches on it per tile: register slots, thread-bit layouts, control
+// patterns and table shapes are runtime values, so each op costs branches,
+// address arithmetic and spills (profiles/r1_tile_stalls_n28.md: op dispatch
+// ~20% of the stall samples, LDL/STL 4% of the instructions).  This generator
+// turns one encoded pass (the same phases and slot-space ops the interpreter
+// runs) into straight-line CUDA for that pass: every slot index, shared-memory
+// offset, thread-bit deposit and control mask is a literal, pairs excluded by
+// a register-slot control are simply not emitted, exact 1 / -1 table entries
+// become no-ops / sign flips, and the numeric payload (matrices, tables,
+// factors) is passed as a __grid_constant__ kernel parameter, so DFMA/DMUL
+// take it straight from the constant bank.  The code depends only on the
+// pass's structure and on which payload entries are exactly 0 / +-1, so a
+// VQE parameter update (new angles, same structure) hits the compile cache.
+// NVRTC compiles it to sm_100a SASS (qsv_jit.cu).
+
+struct JitSource {
+  std::string src;      // CUDA source of kernel "k_pass"
+  int threads = 0;      // CTA threads
+  int group_threads = 0;
+  size_t smem = 0;      // dynamic shared memory
+  int ndata = 0;        // double2 entries of the payload parameter
+};
+
+namespace jitgen {
+
+inline std::string hex64(uint64_t v) {
+  char b[32];
+  snprintf(b, sizeof(b), "0x%llxull", (unsigned long long)v);
+  return b;
+}
+inline std::string hex32(uint32_t v) {
+  char b[24];
+  snprintf(b, sizeof(b), "0x%xu", v);
+  return b;
+}
+
+// thread-local index of tid placed at the given local bits (literal shifts)
+inline std::string deposit(const std::vector<int>& pos, const char* var) {
+  std::string s = "(0u";
+  for (size_t j = 0; j < pos.size(); ++j) {
+    char b[96];
+    snprintf(b, sizeof(b), " | (((%s >> %zu) & 1u) << %d)", var, j, pos[j]);
+    s += b;
+  }
+  return s + ")";
+}
+
+inline uint32_t swz_host(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+
+inline bool is_val(const Cplx& c, double re, double im) { return c.re == re && c.im == im; }
+
+struct Gen {
+  const Encoded& e;
+  int L, R, R2, G;
+  std::string o;
+  explicit Gen(const Encoded& enc, int L_) : e(enc), L(L_), R(kRegBits), R2(kRegs) {
+    G = 1 << (L - kRegBits);
+  }
+  void line(const std::string& s) {
+    o += s;
+    o += '\n';
+  }
+  std::string d(uint32_t idx) const {  // payload entry as an expression
+    return "P.d[" + std::to_string(idx) + "]";
+  }
+  const Cplx& val(uint32_t idx) const { return e.data[idx]; }
+
+  // ---- register ops ----------------------------------------------------
+  // pairs (j, j | 1 << I) of slot I whose register-control part holds
+  template <typename F>
+  void pairs(int I, uint32_t rm, uint32_t rv, F body) {
+    for (int j = 0; j < R2; ++j) {
+      if ((j >> I) & 1) continue;
+      if (((uint32_t)j & rm) != rv) continue;
+      body(j, j | (1 << I));
+    }
+  }
+  void real1(int I, uint32_t rm, uint32_t rv, uint32_t D, bool swap) {
+    if (swap) {
+      pairs(I, rm, rv, [&](int j, int q) {
+        line("{ double2 t_ = v[" + std::to_string(j) + "]; v[" + std::to_string(j) + "] = v[" +
+             std::to_string(q) + "]; v[" + std::to_string(q) + "] = t_; }");
+      });
+      return;
+    }
+    const std::string ab = d(D), cd = d(D + 1);
+    const Cplx A = val(D), B = val(D + 1);
+    pairs(I, rm, rv, [&](int j, int q) {
+      const std::string x = "v[" + std::to_string(j) + "]", y = "v[" + std::to_string(q) + "]";
+      line("{ const double2 x_ = " + x + ", y_ = " + y + ";");
+      // [[a, b], [c, d]] with a = ab.x, b = ab.y, c = cd.x, d = cd.y
+      auto out = [&](const std::string& dst, double m0, const std::string& e0, double m1,
+                     const std::string& e1) {
+        for (const char* c : {".x", ".y"}) {
+          std::string expr;
+          if (m0 == 0.0 && m1 == 0.0) expr = "0.0";
+          else if (m0 == 0.0) expr = (m1 == 1.0 ? std::string("y_") + c
+                                      : m1 == -1.0 ? std::string("-y_") + c
+                                                   : e1 + " * y_" + c);
+          else if (m1 == 0.0) expr = (m0 == 1.0 ? std::string("x_") + c
+                                      : m0 == -1.0 ? std::string("-x_") + c
+                                                   : e0 + " * x_" + c);
+          else expr = "fma(" + e1 + ", y_" + c + ", " + e0 + " * x_" + c + ")";
+          line("  " + dst + c + " = " + expr + ";");
+        }
+      };
+      out(x, A.re, ab + ".x", A.im, ab + ".y");
+      out(y, B.re, cd + ".x", B.im, cd + ".y");
+      line("}");
+    });
+  }
+  void dense1(int I, uint32_t rm, uint32_t rv, uint32_t D) {
+    pairs(I, rm, rv, [&](int j, int q) {
+      const std::string x = "v[" + std::to_string(j) + "]", y = "v[" + std::to_string(q) + "]";
+      line("{ const double2 x_ = " + x + ", y_ = " + y + ";");
+      line("  " + x + " = cfma(" + d(D + 1) + ", y_, cmul(" + d(D) + ", x_));");
+      line("  " + y + " = cfma(" + d(D + 3) + ", y_, cmul(" + d(D + 2) + ", x_));");
+      line("}");
+    });
+  }
+  // v[j] *= T[j] for every slot, T = payload[D .. D + R2), exact +-1 skipped /
+  // folded into the sign mask `*neg`, real entries as two multiplies
+  void table_mul(uint32_t D, uint32_t* neg) {
+    for (int j = 0; j < R2; ++j) {
+      const Cplx t = val(D + j);
+      const std::string vj = "v[" + std::to_string(j) + "]";
+      if (is_val(t, 1, 0)) continue;
+      if (is_val(t, -1, 0)) {
+        *neg ^= 1u << j;
+        continue;
+      }
+      if (t.im == 0.0) {
+        line(vj + ".x *= " + d(D + j) + ".x; " + vj + ".y *= " + d(D + j) + ".x;");
+        continue;
+      }
+      line(vj + " = cmul(" + vj + ", " + d(D + j) + ");");
+    }
+  }
+  // runtime sign rules (FlushSign records at payload D..): bits ^= col where
+  // the thread / tile pattern holds
+  void sign_rules(uint32_t D, int m, const char* bits) {
+    for (int r = 0; r < m; ++r) {
+      FlushSign S;
+      memcpy(&S, &e.data[D + 2 * r], sizeof(S));
+      std::string cond;
+      if (S.lm) cond += "(lt & " + hex32(S.lm) + ") == " + hex32(S.lv);
+      if (S.gm) {
+        if (!cond.empty()) cond += " && ";
+        cond += "(base & " + hex64(S.gm) + ") == " + hex64(S.gv);
+      }
+      if (cond.empty()) line(std::string(bits) + " ^= " + hex32(S.col) + ";");
+      else line("if (" + cond + ") " + bits + " ^= " + hex32(S.col) + ";");
+    }
+  }
+  void apply_signs(const char* bits, uint32_t const_neg) {
+    // v[j] = -v[j] where bit j of (bits ^ const_neg) is set
+    for (int j = 0; j < R2; ++j) {
+      const std::string vj = "v[" + std::to_string(j) + "]";
+      if ((const_neg >> j) & 1u)
+        line("{ const int s_ = (int)(((~" + std::string(bits) + ") << " +
+             std::to_string(31 - j) + ") & 0x80000000u); " + vj + " = negs(" + vj +
+             ", s_); }");
+      else
+        line("{ const int s_ = (int)((" + std::string(bits) + " << " + std::to_string(31 - j) +
+             ") & 0x80000000u); " + vj + " = negs(" + vj + ", s_); }");
+    }
+  }
+
+  void op_flush(const TileOp& op) {
+    const uint32_t D = op.data;
+    const bool table = op.kind == T_FLUSH;
+    const uint32_t sgn0 = table ? 0u : op.lmask;
+    const uint32_t sD = table ? D + R2 : D;
+    line("{ uint32_t bits_ = " + hex32(sgn0) + ";");
+    sign_rules(sD, op.m, "bits_");
+    uint32_t neg = 0;
+    if (table) {
+      if (op.slots) {  // per-thread factors of non-register qubits
+        const uint32_t fD = sD + 2 * op.m;
+        line("  double2 C_ = make_double2(1.0, 0.0);");
+        for (int f = 0; f < op.slots; ++f) {
+          FlushFactor F;
+          memcpy(&F, &e.data[fD + 3 * f], sizeof(F));
+          const std::string bit =
+              F.pos >= 0 ? "((lt >> " + std::to_string(F.pos) + ") & 1u)"
+                         : "((base >> " + std::to_string(-F.pos - 1) + ") & 1ull)";
+          line("  C_ = cmul(C_, " + bit + " ? " + d(fD + 3 * f + 2) + " : " + d(fD + 3 * f + 1) +
+               ");");
+        }
+        for (int j = 0; j < R2; ++j)
+          line("  v[" + std::to_string(j) + "] = cmul(v[" + std::to_string(j) + "], C_);");
+      }
+      table_mul(D, &neg);
+    }
+    if (op.m > 0 || sgn0 != 0) {
+      apply_signs("bits_", neg);
+    } else if (neg) {
+      for (int j = 0; j < R2; ++j)
+        if ((neg >> j) & 1u)
+          line("v[" + std::to_string(j) + "].x = -v[" + std::to_string(j) + "].x; v[" +
+               std::to_string(j) + "].y = -v[" + std::to_string(j) + "].y;");
+    }
+    line("}");
+  }
+
+  void op_phases(const TileOp& op) {
+    line("{ double2 C_ = make_double2(1.0, 0.0);");
+    for (int i = 0; i < R; ++i)
+      if ((op.slots >> i) & 1) line("  double2 ph" + std::to_string(i) + "_ = make_double2(1.0, 0.0);");
+    for (int r = 0; r < op.m; ++r) {
+      FlushPhase F;
+      memcpy(&F, &e.data[op.data + 3 * r], sizeof(F));
+      std::string cond;
+      if (F.lm) cond += "(lt & " + hex32(F.lm) + ") == " + hex32(F.lv);
+      if (F.gm) {
+        if (!cond.empty()) cond += " && ";
+        cond += "(base & " + hex64(F.gm) + ") == " + hex64(F.gv);
+      }
+      const std::string tgt = F.slot < 0 ? "C_" : "ph" + std::to_string(F.slot) + "_";
+      const std::string stmt = tgt + " = cmul(" + tgt + ", " + d(op.data + 3 * r + 2) + ");";
+      line(cond.empty() ? "  " + stmt : "  if (" + cond + ") " + stmt);
+    }
+    if (op.flags & 1)
+      for (int j = 0; j < R2; ++j)
+        line("  v[" + std::to_string(j) + "] = cmul(v[" + std::to_string(j) + "], C_);");
+    for (int i = 0; i < R; ++i) {
+      if (!((op.slots >> i) & 1)) continue;
+      for (int j = 0; j < R2; ++j)
+        if ((j >> i) & 1)
+          line("  v[" + std::to_string(j) + "] = cmul(v[" + std::to_string(j) + "], ph" +
+               std::to_string(i) + "_);");
+    }
+    line("}");
+  }
+
+  void op_diag(const TileOp& op) {
+    const uint32_t rm = op.zl & 0xffffu, rv = op.zl >> 16;
+    int fixed_bits = 0;  // targets on thread / tile bits (runtime sub-index part)
+    std::string fsub = "0";
+    int slot[4] = {-1, -1, -1, -1};
+    for (int t = 0; t < op.m && t < 4; ++t) {
+      const int p = op.tpos[t];
+      if (p < 0) {
+        fsub += " | ((int)((base >> " + std::to_string(-p - 1) + ") & 1ull) << " +
+                std::to_string(t) + ")";
+        ++fixed_bits;
+      } else if (p >= 8) {
+        fsub += " | ((int)((lt >> " + std::to_string(p - 8) + ") & 1u) << " + std::to_string(t) +
+                ")";
+        ++fixed_bits;
+      } else {
+        slot[t] = p;
+      }
+    }
+    line("{ const int fs_ = " + fsub + ";");
+    for (int j = 0; j < R2; ++j) {
+      if (((uint32_t)j & rm) != rv) continue;
+      int sub = 0;
+      for (int t = 0; t < op.m && t < 4; ++t)
+        if (slot[t] >= 0) sub |= ((j >> slot[t]) & 1) << t;
+      const std::string vj = "v[" + std::to_string(j) + "]";
+      if (fixed_bits)
+        line("  " + vj + " = cmul(" + vj + ", P.d[" + std::to_string(op.data) + " + (fs_ | " +
+             std::to_string(sub) + ")]);");
+      else
+        line("  " + vj + " = cmul(" + vj + ", " + d(op.data + sub) + ");");
+    }
+    line("}");
+  }
+
+  void op_parity(const TileOp& op) {
+    const uint32_t rz = (uint32_t)op.m;
+    line("{ const int par_ = (__popcll(base & " + hex64(op.zg) + ") ^ __popc(lt & " +
+         hex32(op.zl) + ")) & 1;");
+    line("  const double2 fa_ = par_ ? " + d(op.data + 1) + " : " + d(op.data) + ";");
+    line("  const double2 fb_ = par_ ? " + d(op.data) + " : " + d(op.data + 1) + ";");
+    for (int j = 0; j < R2; ++j) {
+      const bool odd = __builtin_popcount((uint32_t)j & rz) & 1;
+      line("  v[" + std::to_string(j) + "] = cmul(v[" + std::to_string(j) + "], " +
+           (odd ? "fb_" : "fa_") + ");");
+    }
+    line("}");
+  }
+
+  void op_phase(const TileOp& op) {
+    const uint32_t rm = op.zl & 0xffffu, rv = op.zl >> 16;
+    for (int j = 0; j < R2; ++j) {
+      if (((uint32_t)j & rm) != rv) continue;
+      const std::string vj = "v[" + std::to_string(j) + "]";
+      if (op.flags & 2) line(vj + ".x = -" + vj + ".x; " + vj + ".y = -" + vj + ".y;");
+      else line(vj + " = cmul(" + vj + ", " + d(op.data) + ");");
+    }
+  }
+
+  // one register-phase op; thread / tile conditions wrap it
+  void reg_op(const TileOp& op) {
+    std::string cond;
+    if (op.gmask) cond = "(base & " + hex64(op.gmask) + ") == " + hex64(op.gval);
+    const bool tcond_kinds = op.kind == T_DENSE1 || op.kind == T_REAL1 || op.kind == T_PHASE ||
+                             op.kind == T_DIAG;
+    if (tcond_kinds && op.lmask) {
+      if (!cond.empty()) cond += " && ";
+      cond += "(lt & " + hex32(op.lmask) + ") == " + hex32(op.lval);
+    }
+    if (!cond.empty()) line("if (" + cond + ") {");
+    switch (op.kind) {
+      case T_DENSE1:
+      case T_REAL1: {
+        const int I = __builtin_ctz((uint32_t)op.slots);
+        const uint32_t rm = op.zl & 0xffffu, rv = op.zl >> 16;
+        if (op.kind == T_REAL1) real1(I, rm, rv, op.data, op.flags & 1);
+        else dense1(I, rm, rv, op.data);
+        break;
+      }
+      case T_REAL1X:
+      case T_DENSE1X: {
+        uint32_t D = op.data;
+        for (int I = 0; I < R; ++I) {
+          if (!((op.slots >> I) & 1)) continue;
+          if (op.kind == T_REAL1X) {
+            real1(I, 0, 0, D, false);
+            D += 2;
+          } else {
+            dense1(I, 0, 0, D);
+            D += 4;
+          }
+        }
+        break;
+      }
+      case T_FLUSH:
+      case T_SIGNS:
+        op_flush(op);
+        break;
+      case T_PHASES:
+        op_phases(op);
+        break;
+      case T_PHASE:
+        op_phase(op);
+        break;
+      case T_DIAG:
+        op_diag(op);
+        break;
+      case T_PARITY:
+        op_parity(op);
+        break;
+      default:
+        throw std::runtime_error("jit: unexpected register op");
+    }
+    if (!cond.empty()) line("}");
+  }
+
+  void reg_phase(const TilePhase& P) {
+    std::vector<int> thr;
+    for (int j = 0; j < L - R; ++j) thr.push_back(P.thrpos[j]);
+    line("{ // register phase");
+    line("const uint32_t lt = " + deposit(thr, "tid") + ";");
+    line("const uint32_t slt = swz(lt);");
+    line("double2 v[" + std::to_string(R2) + "];");
+    uint32_t srb[8];
+    for (int i = 0; i < R; ++i) srb[i] = swz_host(1u << P.regpos[i]);
+    std::vector<uint32_t> cj(R2);
+    for (int j = 0; j < R2; ++j) {
+      uint32_t ad = 0;
+      for (int i = 0; i < R; ++i)
+        if ((j >> i) & 1) ad ^= srb[i];
+      cj[j] = ad;
+      line("v[" + std::to_string(j) + "] = sm[slt ^ " + std::to_string(ad) + "u];");
+    }
+    for (int o = P.op_begin; o < P.op_end; ++o) reg_op(e.ops[o]);
+    for (int j = 0; j < R2; ++j)
+      line("sm[slt ^ " + std::to_string(cj[j]) + "u] = v[" + std::to_string(j) + "];");
+    line("}");
+    line("group_sync(group);");
+  }
+
+  void smem_dense(const TileOp& op) {
+    const int K = op.m;
+    const int DD = 1 << K;
+    std::vector<int> sorted(op.tpos, op.tpos + K);
+    std::sort(sorted.begin(), sorted.end());
+    const uint32_t ncos = 1u << (L - K);
+    line("for (uint32_t c_ = tid; c_ < " + std::to_string(ncos) + "u; c_ += " + std::to_string(G) +
+         "u) {");
+    line("  uint32_t l0 = c_;");
+    for (int j = 0; j < K; ++j)
+      line("  { const uint32_t lo_ = l0 & " + hex32((1u << sorted[j]) - 1u) +
+           "; l0 = ((l0 ^ lo_) << 1) | lo_; }");
+    if (op.lmask) line("  if ((l0 & " + hex32(op.lmask) + ") != " + hex32(op.lval) + ") continue;");
+    line("  const uint32_t s0 = swz(l0);");
+    std::vector<uint32_t> offs(DD);
+    for (int w = 0; w < DD; ++w) {
+      uint32_t l = 0;
+      for (int j = 0; j < K; ++j)
+        if ((w >> j) & 1) l |= 1u << op.tpos[j];
+      offs[w] = swz_host(l);
+      line("  const double2 in" + std::to_string(w) + " = sm[s0 ^ " + std::to_string(offs[w]) +
+           "u];");
+    }
+    for (int z = 0; z < DD; ++z) {
+      std::string acc = "cmul(" + d(op.data + z * DD) + ", in0)";
+      for (int w = 1; w < DD; ++w)
+        acc = "cfma(" + d(op.data + z * DD + w) + ", in" + std::to_string(w) + ", " + acc + ")";
+      line("  const double2 out" + std::to_string(z) + " = " + acc + ";");
+    }
+    for (int z = 0; z < DD; ++z)
+      line("  sm[s0 ^ " + std::to_string(offs[z]) + "u] = out" + std::to_string(z) + ";");
+    line("}");
+  }
+
+  void smem_pauli(const TileOp& op) {
+    const uint32_t xml = (uint32_t)op.slots;
+    const int pivot = 31 - __builtin_clz(xml);
+    line("{ const int gpar_ = __popcll(base & " + hex64(op.zg) + ") & 1;");
+    line("for (uint32_t p_ = tid; p_ < " + std::to_string(1u << (L - 1)) + "u; p_ += " +
+         std::to_string(G) + "u) {");
+    line("  const uint32_t lo_ = p_ & " + hex32((1u << pivot) - 1u) + ";");
+    line("  const uint32_t l = ((p_ ^ lo_) << 1) | lo_;");
+    line("  const uint32_t q = l ^ " + hex32(xml) + ";");
+    line("  const double2 x_ = sm[swz(l)], y_ = sm[swz(q)];");
+    line("  const int pl_ = (__popc(l & " + hex32(op.zl) + ") ^ gpar_) & 1;");
+    line("  const int pq_ = (__popc(q & " + hex32(op.zl) + ") ^ gpar_) & 1;");
+    line("  const double2 sy_ = pq_ ? make_double2(-y_.x, -y_.y) : y_;");
+    line("  const double2 sx_ = pl_ ? make_double2(-x_.x, -x_.y) : x_;");
+    line("  sm[swz(l)] = cfma(" + d(op.data + 1) + ", sy_, cmul(" + d(op.data) + ", x_));");
+    line("  sm[swz(q)] = cfma(" + d(op.data + 1) + ", sx_, cmul(" + d(op.data) + ", y_));");
+    line("}}");
+  }
+
+  void smem_phase(const TilePhase& P) {
+    for (int o = P.op_begin; o < P.op_end; ++o) {
+      const TileOp& op = e.ops[o];
+      line("{ // shared-memory op");
+      if (op.gmask) line("if ((base & " + hex64(op.gmask) + ") == " + hex64(op.gval) + ") {");
+      if (op.kind == S_PAULI) smem_pauli(op);
+      else smem_dense(op);
+      if (op.gmask) line("}");
+      line("}");
+      line("group_sync(group);");
+    }
+  }
+};
+
+}  // namespace jitgen
+
+// Fixed part of every generated kernel (device helpers + the persistent tile
+// loop); the pass body is spliced in at QSV_PASS_BODY.
+inline const char* jit_prelude() {
+  return R"JIT(
+typedef unsigned long long u64;
+typedef unsigned int uint32_t;
+#define QSV_MAX_FIXED 28
+struct FixedBits { int n; u64 lowmask[QSV_MAX_FIXED]; u64 value; };
+__device__ __forceinline__ u64 widen(u64 k, const FixedBits& f) {
+#pragma unroll 4
+  for (int i = 0; i < f.n; ++i) { const u64 lo = k & f.lowmask[i]; k = ((k ^ lo) << 1) | lo; }
+  return k | f.value;
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 negs(double2 v, int s) {
+  return make_double2(__hiloint2double(__double2hiint(v.x) ^ s, __double2loint(v.x)),
+                      __hiloint2double(__double2hiint(v.y) ^ s, __double2loint(v.y)));
+}
+__device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void st1(double2* p, double2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+)JIT";
+}
+
+inline JitSource jit_pass_source(const Encoded& e, int L) {
+  using namespace jitgen;
+  JitSource js;
+  if (L < kRegBits + 1 || L > kMaxTileQubits) throw std::runtime_error("jit: tile size");
+  Gen g(e, L);
+  const int G = g.G;
+  const int tidbits = L - kRegBits;
+  js.group_threads = G;
+  js.threads = kGroups * G;
+  js.smem = (size_t)kGroups * (sizeof(double2) << L);
+  js.ndata = std::max<int>(1, (int)e.data.size());
+  std::string& o = g.o;
+  o += jit_prelude();
+  o += "#define QSV_G " + std::to_string(G) + "\n";
+  o += "#define QSV_GROUPS " + std::to_string(kGroups) + "\n";
+  o += "struct __align__(16) PassParams { double2* a; u64 ntiles; u64* ctr; int nostagger; "
+       "int pad; FixedBits tb; double2 d[" + std::to_string(js.ndata) + "]; };\n";
+  o += "__device__ __forceinline__ void group_sync(int group) {\n"
+       "  asm volatile(\"bar.sync %0, %1;\" ::\"r\"(1 + group), \"n\"(QSV_G) : \"memory\"); }\n";
+  o += "extern \"C\" __global__ void __launch_bounds__(" + std::to_string(js.threads) +
+       ", 1) k_pass(const __grid_constant__ PassParams P) {\n";
+  o += R"JIT(
+  extern __shared__ double2 smem_all[];
+  __shared__ u64 s_next[QSV_GROUPS];
+  __shared__ int s_go_;
+  double2* __restrict__ a = P.a;
+  const int group = threadIdx.x / QSV_G;
+  const uint32_t tid = threadIdx.x % QSV_G;
+  double2* sm = smem_all + (size_t)group * (QSV_G * )JIT" +
+       std::to_string(kRegs) + R"JIT();
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+  volatile int* s_go = &s_go_;
+  if (threadIdx.x == 0) *s_go = (QSV_GROUPS < 2 || P.nostagger) ? QSV_GROUPS : 0;
+  __syncthreads();
+  if (group > 0) while (*s_go < group) __nanosleep(256);
+  bool first = true;
+)JIT";
+  // thread's low HBM offset: tid bit b -> global qubit spos[b]
+  {
+    std::string lo = "  const u64 lo_part = 0ull";
+    for (int b = 0; b < tidbits; ++b)
+      lo += " | ((u64)((tid >> " + std::to_string(b) + ") & 1u) << " +
+            std::to_string(e.pd.spos[b]) + ")";
+    o += lo + ";\n";
+  }
+  // copy index k (the bits above tidbits) -> global offset / smem slot
+  std::vector<uint64_t> hi(kRegs, 0);
+  std::vector<uint32_t> sk(kRegs, 0);
+  for (int k = 0; k < kRegs; ++k) {
+    for (int b = 0; b < kRegBits; ++b)
+      if (((k >> b) & 1) && tidbits + b < L) hi[k] |= 1ULL << e.pd.spos[tidbits + b];
+    sk[k] = swz_host((uint32_t)k * (uint32_t)G);
+  }
+  o += R"JIT(
+  if (tid == 0) s_next[group] = atomicAdd(P.ctr, 1ull);
+  group_sync(group);
+  u64 tile = s_next[group];
+  const int nph_total = )JIT" + std::to_string(std::max<size_t>(1, e.phases.size())) + R"JIT(;
+  while (tile < P.ntiles) {
+    u64 next = 0;
+    if (tid == 0) next = atomicAdd(P.ctr, 1ull);
+    const u64 base = widen(tile, P.tb);
+    {
+      const u64 gb = base | lo_part;
+      const uint32_t st = swz(tid);
+)JIT";
+  for (int k = 0; k < kRegs; ++k)
+    o += "      cp_async16(sbase + ((" + std::to_string(sk[k]) + "u ^ st) << 4), a + (gb | " +
+         hex64(hi[k]) + "));\n";
+  o += R"JIT(      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    group_sync(group);
+)JIT";
+  int ph_idx = 0;
+  const int nph = (int)e.phases.size();
+  for (const TilePhase& P : e.phases) {
+    // release group k once group 0 is k / kGroups of the way through its first tile
+    o += "    if (group == 0 && first && tid == 0 && " + std::to_string(ph_idx) +
+         " * QSV_GROUPS >= (*s_go + 1) * nph_total && *s_go < QSV_GROUPS - 1) *s_go = *s_go + 1;\n";
+    if (P.type == 0) g.reg_phase(P);
+    else g.smem_phase(P);
+    ++ph_idx;
+  }
+  (void)nph;
+  o += R"JIT(
+    {
+      const u64 gb = base | lo_part;
+      const uint32_t st = swz(tid);
+)JIT";
+  for (int k = 0; k < kRegs; ++k)
+    o += "      st1(a + (gb | " + hex64(hi[k]) + "), sm[" + std::to_string(sk[k]) + "u ^ st]);\n";
+  o += R"JIT(    }
+    if (tid == 0) s_next[group] = next;
+    group_sync(group);
+    if (group == 0 && first && tid == 0) *s_go = QSV_GROUPS;
+    first = false;
+    tile = s_next[group];
+  }
+  if (group == 0 && tid == 0) *s_go = QSV_GROUPS;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(P.ctr + 1, 1ull) == gridDim.x - 1) { P.ctr[0] = 0; P.ctr[1] = 0; __threadfence(); }
+  }
+}
+)JIT";
+  js.src = std::move(o);
+  return js;
+}
