@@ -39,56 +39,77 @@ def commutation_check(first: QuantumGate, second: QuantumGate) -> bool:
     return True
 
 
-def _support(g) -> frozenset:
-    return frozenset(g.touched_qubits())
+class _Entry:
+    """A gate with its support and mergeability computed once (the passes
+    below test them O(gates^2) times; the reference recomputes both on every
+    test)."""
+
+    __slots__ = ("gate", "support", "ok")
+
+    def __init__(self, gate):
+        self.gate = gate
+        self.support = frozenset(gate.touched_qubits())
+        self.ok = bool(gate.mergeable)
+
+
+def _fused(a: _Entry, b: _Entry) -> _Entry:
+    return _Entry(merge(a.gate, b.gate))
 
 
 def optimize_light(circuit) -> None:
-    """Merge neighbouring pairs whose supports nest, until nothing changes
-    (optimizer.py:56-70)."""
-    gates = circuit.gates
-    again = True
-    while again:
-        again = False
+    """Merge neighbouring pairs whose supports nest, until a sweep changes
+    nothing (optimizer.py:56-70).  A merge stays at position i, so the fused
+    gate is immediately tried against its new right neighbour."""
+    seq = [_Entry(g) for g in circuit.gates]
+    changed = True
+    while changed:
+        changed = False
         i = 0
-        while i + 1 < len(gates):
-            a, b = gates[i], gates[i + 1]
-            if a.mergeable and b.mergeable:
-                sa, sb = _support(a), _support(b)
-                if sa <= sb or sb <= sa:
-                    gates[i:i + 2] = [merge(a, b)]
-                    again = True
-                    continue  # retry at the same position
-            i += 1
+        while i + 1 < len(seq):
+            a, b = seq[i], seq[i + 1]
+            if a.ok and b.ok and (a.support <= b.support or b.support <= a.support):
+                seq[i:i + 2] = [_fused(a, b)]
+                changed = True
+            else:
+                i += 1
+    circuit.gates[:] = [e.gate for e in seq]
+
+
+def _partner(seq, i: int, block_size: int):
+    """First j > i that gate i can absorb: scanning right, a mergeable gate
+    whose union with i's support fits the block wins; a gate that does not
+    provably commute with gate i ends the scan (optimizer.py:90-103)."""
+    a = seq[i]
+    for j in range(i + 1, len(seq)):
+        b = seq[j]
+        if b.ok and len(a.support | b.support) <= block_size:
+            return j
+        if not commutation_check(a.gate, b.gate):
+            return None
+    return None
 
 
 def optimize_heavy(circuit, block_size: int) -> None:
-    """Slide a later gate left past gates that provably commute with gate i
-    and merge it into gate i when the union stays within ``block_size``
-    qubits (optimizer.py:73-107)."""
+    """Commutation-aware fusion within ``block_size`` qubits
+    (optimizer.py:73-107): gate j slides left to gate i past gates that
+    commute with gate i; the fused gate takes gate j's slot, so the gates in
+    between keep their order ahead of it, and gate i's position is retried."""
     if block_size < 1:
         raise ValueError("block size must be >= 1")
-    gates = circuit.gates
-    again = True
-    while again:
-        again = False
+    seq = [_Entry(g) for g in circuit.gates]
+    changed = True
+    while changed:
+        changed = False
         i = 0
-        while i < len(gates):
-            a = gates[i]
-            if not a.mergeable or len(_support(a)) > block_size:
+        while i < len(seq):
+            a = seq[i]
+            j = _partner(seq, i, block_size) if a.ok and len(a.support) <= block_size else None
+            if j is None:
                 i += 1
                 continue
-            fused = False
-            for j in range(i + 1, len(gates)):
-                b = gates[j]
-                if b.mergeable and len(_support(a) | _support(b)) <= block_size:
-                    m = merge(a, b)
-                    del gates[j]
-                    del gates[i]
-                    gates.insert(j - 1, m)
-                    again = fused = True
-                    break
-                if not commutation_check(a, b):
-                    break
-            if not fused:
-                i += 1
+            fused = _fused(a, seq[j])
+            del seq[j]
+            del seq[i]
+            seq.insert(j - 1, fused)
+            changed = True
+    circuit.gates[:] = [e.gate for e in seq]
