@@ -498,8 +498,14 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
   o += "#define QSV_GROUPS " + std::to_string(kGroups) + "\n";
   o += "struct __align__(16) PassParams { double2* a; u64 ntiles; u64* ctr; int nostagger; "
        "int pad; FixedBits tb; double2 d[" + std::to_string(js.ndata) + "]; };\n";
-  o += "__device__ __forceinline__ void group_sync(int group) {\n"
-       "  asm volatile(\"bar.sync %0, %1;\" ::\"r\"(1 + group), \"n\"(QSV_G) : \"memory\"); }\n";
+  // named barriers need whole warps; groups smaller than a warp (tiles of
+  // L < 5 + register bits) share one warp and synchronise on their lane mask
+  if (G >= 32)
+    o += "__device__ __forceinline__ void group_sync(int group) {\n"
+         "  asm volatile(\"bar.sync %0, %1;\" ::\"r\"(1 + group), \"n\"(QSV_G) : \"memory\"); }\n";
+  else
+    o += "__device__ __forceinline__ void group_sync(int group) {\n"
+         "  __syncwarp(((1u << QSV_G) - 1u) << (group * QSV_G)); }\n";
   o += "extern \"C\" __global__ void __launch_bounds__(" + std::to_string(js.threads) +
        ", 1) k_pass(const __grid_constant__ PassParams P) {\n";
   o += R"JIT(
@@ -513,7 +519,7 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
        std::to_string(kRegs) + R"JIT();
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
   volatile int* s_go = &s_go_;
-  if (threadIdx.x == 0) *s_go = (QSV_GROUPS < 2 || P.nostagger) ? QSV_GROUPS : 0;
+  if (threadIdx.x == 0) *s_go = (QSV_GROUPS < 2 || P.nostagger || QSV_G < 32) ? QSV_GROUPS : 0;
   __syncthreads();
   if (group > 0) while (*s_go < group) __nanosleep(256);
   bool first = true;
