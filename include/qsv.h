@@ -255,6 +255,18 @@ int qsv_plan_stats(int num_qubits, const qsv_op* ops, int nops, const qsv_plan_o
  * in-process cache (qsv_plan_opts.jit).  No GPU needed. */
 int qsv_jit_stats(long* compiles, long* disk_hits, long* mem_hits);
 
+/* Expectation-pass code generation without a device (inspection / tests):
+ * the pass layout qsv_expect would use for these terms (flip masks xms[t],
+ * sign masks zms[t] over qubits), and the CUDA source of pass `pass` copied
+ * into buf (NUL-terminated, truncated to cap).  *num_passes receives the pass
+ * count; returns QSV_EUNSUPPORTED when a flip mask does not fit a tile. */
+/* Expectation tile passes run so far in this process: through generated
+ * kernels (qsv_expect_jit.cu) and through the generic k_expect_tile. */
+int qsv_expect_path_stats(long* jit_passes, long* generic_passes);
+
+int qsv_expect_jit_source(int num_qubits, int nterms, const uint64_t* xms, const uint64_t* zms,
+                          int pass, char* buf, size_t cap, int* num_passes);
+
 /* --------------------------------------------------------------- sharding
  * Exchange primitives of the sharded engine (dist.py; no reference
  * counterpart -- the reference is single-process).  A shard that

@@ -140,6 +140,9 @@ _SIGS = {
     "qsv_plan_stats": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts),
                         C.POINTER(QsvProgramStats)], _I),
     "qsv_jit_stats": ([C.POINTER(C.c_long)] * 3, _I),
+    "qsv_expect_path_stats": ([C.POINTER(C.c_long)] * 2, _I),
+    "qsv_expect_jit_source": ([_I, _I, C.POINTER(_U64), C.POINTER(_U64), _I, C.c_char_p,
+                               C.c_size_t, _IP], _I),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -196,3 +199,25 @@ def jit_stats() -> dict:
     a, b, c = C.c_long(), C.c_long(), C.c_long()
     check(lib.qsv_jit_stats(C.byref(a), C.byref(b), C.byref(c)))
     return {"compiles": a.value, "disk_hits": b.value, "mem_hits": c.value}
+
+
+def expect_jit_sources(num_qubits: int, xms, zms) -> list:
+    """CUDA sources of the generated expectation passes qsv_expect would use
+    for terms with flip masks ``xms`` and sign masks ``zms`` (no GPU needed)."""
+    nt = len(xms)
+    xa, za = (_U64 * max(1, nt))(*xms), (_U64 * max(1, nt))(*zms)
+    npass = C.c_int()
+    check(lib.qsv_expect_jit_source(num_qubits, nt, xa, za, -1, None, 0, C.byref(npass)))
+    out = []
+    for p in range(npass.value):
+        buf = C.create_string_buffer(1 << 22)
+        check(lib.qsv_expect_jit_source(num_qubits, nt, xa, za, p, buf, len(buf), C.byref(npass)))
+        out.append(buf.value.decode())
+    return out
+
+
+def expect_path_stats() -> dict:
+    """Expectation tile passes run so far: generated kernels vs generic kernel."""
+    a, b = C.c_long(), C.c_long()
+    check(lib.qsv_expect_path_stats(C.byref(a), C.byref(b)))
+    return {"jit_passes": a.value, "generic_passes": b.value}

@@ -292,6 +292,18 @@ __global__ void __launch_bounds__(kXThreads)
 }
 
 // --------------------------------------------------------------- host side
+int launch_expect_tile_final(const double* partials, int nblocks, int nterms, double* out,
+                             cudaStream_t s) {
+  k_expect_tile_final<<<nterms, kXThreads, 0, s>>>(partials, nblocks, out);
+  QSV_CHECK_LAUNCH("k_expect_tile_final");
+  return QSV_OK;
+}
+
+void expect_generic_pass_done();
+int expect_tile_jit(const double2* a, int n, const std::vector<uint64_t>& xms,
+                    const std::vector<uint64_t>& zms, void* scratch, std::vector<double>& res,
+                    cudaStream_t s);
+
 struct XTermIn {
   uint64_t xm, zm;
   int index;  // caller's term index
@@ -361,6 +373,10 @@ size_t expect_tile_scratch_bytes() {
 int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
                 const std::vector<uint64_t>& zms, void* scratch, std::vector<double>& res,
                 cudaStream_t s) {
+  {  // generated pass kernels when compiled for this observable (qsv_expect_jit.cu)
+    const int rc = expect_tile_jit(a, n, xms, zms, scratch, res, s);
+    if (rc != QSV_EUNSUPPORTED) return rc;
+  }
   std::vector<XTermIn> terms;
   for (size_t i = 0; i < xms.size(); ++i) terms.push_back({xms[i], zms[i], (int)i});
   std::vector<std::pair<uint64_t, std::vector<int>>> passes;
@@ -459,6 +475,7 @@ int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
     QSV_CHECK_LAUNCH("k_expect_tile");
     k_expect_tile_final<<<P.nterms, kXThreads, 0, s>>>(partials, (int)grid, dout);
     QSV_CHECK_LAUNCH("k_expect_tile_final");
+    expect_generic_pass_done();
     orders.push_back(order);
   }
   return drain();

@@ -436,10 +436,14 @@ def test_program_stats_and_reuse():
     circ = workloads.generate_cnot_ring(12, seed=1)
     stats = circ.program_stats()
     assert stats["num_ops_in"] == circ.get_gate_count()
-    a, b = qs.QuantumState(12), qs.QuantumState(12)
-    circ.update_quantum_state(a)
-    circ.update_quantum_state(b)
-    assert np.array_equal(a.get_vector(), b.get_vector())
+    a, b, c = qs.QuantumState(12), qs.QuantumState(12), qs.QuantumState(12)
+    circ.update_quantum_state(a)  # first run: tile interpreter
+    circ.update_quantum_state(b)  # from the second run: generated pass kernels (jit=1)
+    circ.update_quantum_state(c)
+    # interpreter and generated code round differently (contraction order)
+    assert np.max(np.abs(a.get_vector() - b.get_vector())) <= 1e-14
+    # the same compiled program replayed is bit-reproducible
+    assert np.array_equal(b.get_vector(), c.get_vector())
 
 
 def test_graph_replay_on_reused_buffers():
