@@ -1213,6 +1213,35 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
   return rest;
 }
 
+// QSV_PDL=0: generated pass kernels launch without programmatic dependent
+// launch (A/B experiments)
+inline bool jit_pdl() {
+  static const int on = [] {
+    const char* e = getenv("QSV_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
+// QSV_ONE_FMA=0 keeps the plain real rotations (A/B experiments)
+inline bool one_fma_rotations() {
+  static const int on = [] {
+    const char* e = getenv("QSV_ONE_FMA");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
+// FP64 instructions per amplitude of a real 2x2 on a register slot: a
+// multiply and an FMA per output component, or one FMA when the matrix has a
+// unit diagonal / anti-diagonal (the one-FMA form of realify)
+inline double real_rot_ops(const std::vector<Cplx>& d) {
+  if (d.size() >= 2 && ((d[0].re == 1.0 && d[1].im == 1.0) || (d[0].im == 1.0 && d[1].re == 1.0)))
+    return 2.0;
+  return 4.0;
+}
+
+
 
 void emit_rlayer(Encoded& e, const std::vector<PhaseOp>& rl) {
   // uncontrolled 1-qubit ops are collected into slot-mask batches; a batch
@@ -1262,7 +1291,8 @@ void emit_rlayer(Encoded& e, const std::vector<PhaseOp>& rl) {
     if (x >= 0) {
       const PhaseOp& po = rl[x];
       emit_op(e, po.op, po.data);
-      e.fp64_ops_per_amp += (po.op.flags & 1) ? 0.0 : (po.op.kind == T_REAL1 ? 4.0 : 8.0);
+      e.fp64_ops_per_amp +=
+          (po.op.flags & 1) ? 0.0 : (po.op.kind == T_REAL1 ? real_rot_ops(po.data) : 8.0);
       continue;
     }
     const Batch& B = batches[-x - 1];
@@ -1283,7 +1313,8 @@ void emit_rlayer(Encoded& e, const std::vector<PhaseOp>& rl) {
         if ((B.slots >> i) & 1) data.insert(data.end(), B.mat[i].begin(), B.mat[i].end());
     }
     emit_op(e, op, data);
-    e.fp64_ops_per_amp += cnt * (B.real ? 4.0 : 8.0);
+    for (int i = 0; i < kRegBits; ++i)
+      if ((B.slots >> i) & 1) e.fp64_ops_per_amp += B.real ? real_rot_ops(B.mat[i]) : 8.0;
   }
 }
 
@@ -1757,6 +1788,35 @@ std::vector<GateDesc> realify(int n, const std::vector<GateDesc>& in) {
         push(canonicalize(desc_from_m2(q, U)));
         continue;
       }
+      // One-FMA form: R = D . M with D diagonal and M unit-diagonal
+      // ([[1, r1/r0], [r2/r3, 1]], D = diag(r0, r3)) or, when r0 = 0 (R is
+      // anti-diagonal), M = [[0, 1], [1, 0]] with D = diag(r1, r2).  D joins
+      // the pending diagonal diag(a) of the qubit (applied with the next gate
+      // on it or in a merged flush), so the rotation itself costs one FMA
+      // per output component instead of a multiply and an FMA.  The
+      // intermediate fl(x + t y) is later scaled by r0, so the result keeps
+      // a relative error of one rounding (no growth from a large t).  The
+      // structure (unit entries) does not depend on the angle, so generated
+      // pass kernels stay cached across parameter updates.
+      double D[2] = {1.0, 1.0};
+      if (one_fma_rotations()) {
+        if (Rm[0] != 0.0 && Rm[3] != 0.0) {
+          D[0] = Rm[0];
+          D[1] = Rm[3];
+          const double t1 = Rm[1] / Rm[0], t2 = Rm[2] / Rm[3];
+          Rm[0] = 1.0;
+          Rm[1] = t1;
+          Rm[2] = t2;
+          Rm[3] = 1.0;
+        } else if (Rm[1] != 0.0 && Rm[2] != 0.0) {
+          D[0] = Rm[1];
+          D[1] = Rm[2];
+          Rm[0] = 0.0;
+          Rm[1] = 1.0;
+          Rm[2] = 1.0;
+          Rm[3] = 0.0;
+        }
+      }
       // one gate carrying both factors, so the pass packer cannot separate
       // diag(b) from R (R diag(b) is what a standalone kernel applies)
       M2 RB;
@@ -1772,9 +1832,9 @@ std::vector<GateDesc> realify(int n, const std::vector<GateDesc>& in) {
         for (int k = 0; k < 4; ++k) gr.rf_r[k] = Rm[k];
       }
       push(canonicalize(gr));
-      p0[q] = a[0];
-      p1[q] = a[1];
-      has[q] = !(is_one_c(a[0]) && is_one_c(a[1]));
+      p0[q] = {a[0].re * D[0], a[0].im * D[0]};
+      p1[q] = {a[1].re * D[1], a[1].im * D[1]};
+      has[q] = !(is_one_c(p0[q]) && is_one_c(p1[q]));
       continue;
     }
     const uint64_t nd = nondiag_mask(g);
@@ -2032,8 +2092,17 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     int rc = jit_set_smem(tp.jit, tp.jit_smem);
     if (rc) return rc;
     void* args[] = {pbuf.data()};
-    QSV_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(tp.jit.kernel), dim3(grid),
-                             dim3(tp.jit_threads), args, tp.jit_smem, s));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tp.jit_threads);
+    cfg.dynamicSmemBytes = tp.jit_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = jit_pdl() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    QSV_TRY(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(tp.jit.kernel), args));
     return QSV_OK;
   }
   const size_t smem = kGroups * (sizeof(double2) << tp.L) + tp.nops * sizeof(TileOp) +

@@ -104,6 +104,8 @@ struct Gen {
           else if (m1 == 0.0) expr = (m0 == 1.0 ? std::string("x_") + c
                                       : m0 == -1.0 ? std::string("-x_") + c
                                                    : e0 + " * x_" + c);
+          else if (m0 == 1.0) expr = "fma(" + e1 + ", y_" + c + ", x_" + c + ")";
+          else if (m1 == 1.0) expr = "fma(" + e0 + ", x_" + c + ", y_" + c + ")";
           else expr = "fma(" + e1 + ", y_" + c + ", " + e0 + " * x_" + c + ")";
           line("  " + dst + c + " = " + expr + ";");
         }
@@ -519,6 +521,12 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
        std::to_string(kRegs) + R"JIT();
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
   volatile int* s_go = &s_go_;
+  // programmatic dependent launch: this grid may be scheduled while the
+  // previous pass drains; wait for its completion (and memory) before the
+  // first read of the state or the work counter, and let the next pass's
+  // CTAs queue behind this one as SMs free up
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) *s_go = (QSV_GROUPS < 2 || P.nostagger || QSV_G < 32) ? QSV_GROUPS : 0;
   __syncthreads();
   if (group > 0) while (*s_go < group) __nanosleep(256);

@@ -137,3 +137,35 @@ def test_argument_errors():
     c.add_gate(qg.H(1))
     with pytest.raises(ValueError):
         c.update_quantum_state(st)  # circuit and state sizes differ
+
+
+def _median_call_time(fn, calls=5000, batches=7):
+    import time
+    med = []
+    for _ in range(batches):
+        t0 = time.perf_counter()
+        for _ in range(calls):
+            fn()
+        med.append((time.perf_counter() - t0) / calls)
+    return sorted(med)[len(med) // 2]
+
+
+@pytest.mark.gpu
+def test_per_call_overhead_within_budget():
+    """Reference bindings/tests/test_bindings.py:581-590: the Qulacs-named
+    handle adds <= 2 us per gate call over the core gate's apply; and the
+    core call itself (cached ctypes arguments, one libqsv launch) stays in
+    the tens of microseconds at n=10."""
+    import paper_2011_13524_b200 as qs
+    from paper_2011_13524_b200 import gate as qg
+    st = qs.QuantumState(2)
+    g = qg.X(0)
+    core_g, core_s = g._core, st
+    bound = _median_call_time(lambda: g.update_quantum_state(st))
+    core = _median_call_time(lambda: core_g.apply(core_s))
+    assert bound - core <= 2e-6, (bound, core)
+    st10 = qs.QuantumState(10)
+    rx = qg.RX(3, 0.3)
+    t = _median_call_time(lambda: rx.update_quantum_state(st10), calls=2000)
+    st10.synchronize()
+    assert t <= 30e-6, t
