@@ -766,6 +766,25 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
     best = min(times)
     fpeak, fsrc = fp64_peak()
     achieved = stats.get("fp64_flops", 0.0) / best / 1e12
+    # both floors of the tile passes: FP64 work executed (planner count, one-FMA
+    # rotations included) at the sustained DFMA peak, and one HBM read + write
+    # of the state per pass at the measured copy bandwidth; the roofline is
+    # whichever is larger
+    hpeak, hsrc = measured_peaks()
+    fp64_floor = stats.get("fp64_flops", 0.0) / (fpeak * 1e12)
+    hbm_floor = stats.get("hbm_bytes", 0.0) / (hpeak * 1e9)
+    if fp64_floor >= hbm_floor:
+        roof = {"bound": "fp64", "achieved": achieved, "peak": fpeak, "unit": "TFLOP/s",
+                "frac": achieved / fpeak, "peak_source": fsrc}
+    else:
+        hach = stats.get("hbm_bytes", 0.0) / best / 1e9
+        roof = {"bound": "hbm", "achieved": hach, "peak": hpeak, "unit": "GB/s",
+                "frac": hach / hpeak, "peak_source": hsrc}
+    roof.update({"kernel": "k_pass (generated tile passes)",
+                 "floors_s": {"fp64": fp64_floor, "hbm": hbm_floor},
+                 "frac_of_max_floor": max(fp64_floor, hbm_floor) / best,
+                 "note": "FP64 flops counted by the planner (2 per FMA) / device time; "
+                         "HBM bytes = 32 B per amplitude per pass"})
     out = {"metric": "random-circuit sec/layer", "unit": "s/layer",
            "value": best / (depth + 1), "higher_is_better": False,
            "workload": f"cz-ladder n={n} depth={depth} seed=1 ({gates_in} gates), "
@@ -773,10 +792,7 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
            "circuit_s_best": best, "circuit_s_all": times, "plan_s": plan_s,
            "program": stats,
            "hbm_gbs_effective": stats.get("hbm_bytes", 0.0) / best / 1e9,
-           "roofline": {"bound": "fp64", "achieved": achieved, "peak": fpeak,
-                        "unit": "TFLOP/s", "frac": achieved / fpeak, "peak_source": fsrc,
-                        "kernel": "k_tile (tile passes)",
-                        "note": "FP64 flops counted by the planner (2 per FMA) / device time"},
+           "roofline": roof,
            "clocks": clk.summary()}
     del st
     # the headline curve: sec/layer vs qubits (same generator, same depth)
@@ -807,7 +823,8 @@ def run_random_circuit(args, dev, stream, qs, workloads, torch):
         s2 = qs.QuantumState(m, device=dev)
         s2.set_stream(stream.cuda_stream)
         s2.set_random_state_device(7)
-        c.update_quantum_state(s2)  # plan + first run
+        c.update_quantum_state(s2)  # plan + first run (pass interpreter)
+        c.update_quantum_state(s2)  # generated pass kernels compiled (NVRTC) + first use
         torch.cuda.synchronize(dev)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)

@@ -45,6 +45,7 @@ extern "C" {
 
 typedef struct qsv_state qsv_state;
 typedef struct qsv_program qsv_program;
+typedef struct qsv_comm qsv_comm;
 
 /* ------------------------------------------------------------ library */
 const char* qsv_last_error(void);
@@ -301,6 +302,36 @@ int qsv_slice_swap(qsv_state* st, void* peer_amps, const int* ls, int k, uint64_
  * of one waiting for the other's persistent CTAs. */
 int qsv_state_view(qsv_state* parent, uint64_t offset, int num_qubits, qsv_state** out);
 int qsv_set_sm_limit(qsv_state* st, int sms);
+
+/* ----------------------------------------------------------- communicator
+ * NCCL inside libqsv for the sharded engine (dist.py; the north star's
+ * "NCCL send/recv" exchange -- no reference counterpart, the reference is
+ * single-process).  NCCL is loaded on first use (dlopen libnccl.so.2).
+ * Rendezvous: rank 0 calls qsv_comm_unique_id and hands the
+ * QSV_COMM_ID_BYTES-byte id to every rank (dist.py broadcasts it), each rank
+ * calls qsv_comm_create with its rank and device.  All operations are
+ * enqueued on the given state's stream:
+ *  - qsv_comm_barrier: one-element all-reduce, a device-side barrier that
+ *    orders every rank's earlier shard work before later work (no host wait);
+ *  - qsv_comm_allreduce_sum: values[0..count) summed over ranks (count <= 64),
+ *    synchronous, results back in `values`;
+ *  - qsv_comm_slice_exchange: send the slice {x : bits ls of x == d_send} of
+ *    the shard to `peer` and overwrite the slice {x : bits ls == d_recv} with
+ *    the slice the peer sends (grouped ncclSend / ncclRecv through staging
+ *    buffers of at most chunk_bytes per direction; gather / scatter kernels
+ *    pack the strided slices).  Every rank of a pair must call it with the
+ *    other as peer; peer == own rank copies within the shard.
+ * qsv_comm_available: 1 when libnccl.so.2 can be loaded. */
+#define QSV_COMM_ID_BYTES 128
+int qsv_comm_available(void);
+int qsv_comm_unique_id(void* id_out);
+int qsv_comm_create(const void* id, int nranks, int rank, int device, qsv_comm** out);
+int qsv_comm_destroy(qsv_comm* comm);
+int qsv_comm_rank(const qsv_comm* comm, int* rank, int* nranks);
+int qsv_comm_barrier(qsv_comm* comm, qsv_state* st);
+int qsv_comm_allreduce_sum(qsv_comm* comm, qsv_state* st, double* values, int count);
+int qsv_comm_slice_exchange(qsv_comm* comm, qsv_state* st, int peer, const int* ls, int k,
+                            uint64_t d_send, uint64_t d_recv, uint64_t chunk_bytes);
 
 #ifdef __cplusplus
 }

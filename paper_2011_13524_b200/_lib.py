@@ -140,6 +140,14 @@ _SIGS = {
     "qsv_plan_stats": ([_I, C.POINTER(QsvOp), _I, C.POINTER(QsvPlanOpts),
                         C.POINTER(QsvProgramStats)], _I),
     "qsv_jit_stats": ([C.POINTER(C.c_long)] * 3, _I),
+    "qsv_comm_available": ([], _I),
+    "qsv_comm_unique_id": ([_P], _I),
+    "qsv_comm_create": ([_P, _I, _I, _I, C.POINTER(_P)], _I),
+    "qsv_comm_destroy": ([_P], _I),
+    "qsv_comm_rank": ([_P, _IP, _IP], _I),
+    "qsv_comm_barrier": ([_P, _P], _I),
+    "qsv_comm_allreduce_sum": ([_P, _P, _DP, _I], _I),
+    "qsv_comm_slice_exchange": ([_P, _P, _I, _IP, _I, _U64, _U64, _U64], _I),
     "qsv_expect_path_stats": ([C.POINTER(C.c_long)] * 2, _I),
     "qsv_expect_jit_source": ([_I, _I, C.POINTER(_U64), C.POINTER(_U64), _I, C.c_char_p,
                                C.c_size_t, _IP], _I),

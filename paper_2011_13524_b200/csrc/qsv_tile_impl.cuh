@@ -1213,12 +1213,14 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
   return rest;
 }
 
-// QSV_PDL=0: generated pass kernels launch without programmatic dependent
-// launch (A/B experiments)
+// QSV_PDL=1: generated pass kernels launch with programmatic dependent launch
+// (the next pass queued while this one drains).  Off by default: measured
+// slower on every small-state circuit (cnot-ring(14) 0.117 -> 0.138 ms,
+// cz-ladder(16) 0.180 -> 0.207 ms; profiles/r2_small_n_pdl.txt)
 inline bool jit_pdl() {
   static const int on = [] {
     const char* e = getenv("QSV_PDL");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   return on != 0;
 }

@@ -432,7 +432,7 @@ class ShardedQuantumState:
     def __init__(self, num_qubits, world=None, rank=None, owned=None, backend=None,
                  group=None, chunk_bytes=1 << 30, plan=None, exchange="auto",
                  overlap="auto", overlap_bits=2, overlap_sms=16, overlap_min_qubits=20,
-                 exchange_sms=0, reorder=True):
+                 exchange_sms=0, reorder=True, comm="auto"):
         import torch.distributed as dist
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
         if world is None:
@@ -481,6 +481,7 @@ class ShardedQuantumState:
         self._peer_ptr = {}
         self._peer_open = None
         self.exchange = self._setup_exchange(exchange)
+        self._qcomm = self._setup_comm(comm)
         self.set_zero_state()
 
     def _setup_exchange(self, mode):
@@ -521,6 +522,42 @@ class ShardedQuantumState:
             self._stream = torch.cuda.current_stream()
         return "p2p"
 
+    def _setup_comm(self, mode):
+        """libqsv's NCCL communicator (csrc/qsv_comm.cu) for the device
+        barrier, the all-reduce and the NCCL-mode slice exchange, when every
+        process drives one CUDA shard on its own GPU (NCCL does not allow two
+        ranks on one device: processes sharing a GPU keep torch.distributed
+        for these).  torch.distributed only carries the unique id from rank 0
+        (rendezvous).  ``comm``: "auto", "qsv" (required) or "torch"."""
+        if mode not in ("auto", "qsv", "torch"):
+            raise ValueError(f"unknown comm mode {mode!r}")
+        if mode == "torch" or self.dist is None or len(self.owned) == self.world:
+            return None
+        procs = self.dist.get_world_size(self.group)
+        ok = (len(self.owned) == 1 and procs == self.world
+              and all(isinstance(sh, CudaShard) for sh in self.shards.values())
+              and lib.qsv_comm_available() == 1)
+        dev = next(iter(self.shards.values())).device_id() if ok else None
+        info = [None] * procs
+        self.dist.all_gather_object(info, (ok, dev), group=self.group)
+        usable = all(o for o, _ in info) and len({d for _, d in info}) == procs
+        if not usable:
+            if mode == "qsv":
+                raise RuntimeError("qsv communicator needs one CUDA shard per process on "
+                                   "distinct GPUs and a loadable libnccl.so.2")
+            return None
+        me = self.dist.get_rank(self.group)
+        uid = C.create_string_buffer(128)
+        if me == 0:
+            check(lib.qsv_comm_unique_id(uid))
+        box = [uid.raw]
+        src = self.dist.get_global_rank(self.group, 0) if self.group is not None else 0
+        self.dist.broadcast_object_list(box, src=src, group=self.group)
+        h = C.c_void_p()
+        check(lib.qsv_comm_create(C.create_string_buffer(box[0], 128), procs, me, dev,
+                                  C.byref(h)))
+        return h
+
     def close(self):
         """Unmap the peers' shards after a final barrier (collective: every
         rank calls it).  Also a context manager."""
@@ -529,6 +566,13 @@ class ShardedQuantumState:
             for s in self.shards.values():
                 s.sync()
             self._unmap()
+        self._drop_comm()
+
+    def _drop_comm(self):
+        h = getattr(self, "_qcomm", None)
+        if h is not None:
+            self._qcomm = None
+            lib.qsv_comm_destroy(h)
 
     def _unmap(self):
         for ptr in self._peer_ptr.values():
@@ -548,12 +592,17 @@ class ShardedQuantumState:
         # no barrier here (not collective): just drop this process's mappings
         if getattr(self, "_peer_ptr", None):
             self._unmap()
+        self._drop_comm()
 
     def _device_barrier(self):
         """Order every rank's queued shard work before what follows, on the
         device where possible: a one-element all_reduce on the shard stream
         (NCCL) completes only after every rank's earlier kernels have run."""
         if self.dist is None or len(self.owned) == self.world:
+            return
+        if self._qcomm is not None:
+            sh = next(iter(self.shards.values()))
+            check(lib.qsv_comm_barrier(self._qcomm, sh.state._handle()))
             return
         if self.dist.get_backend(self.group) == "nccl":
             import torch
@@ -575,6 +624,12 @@ class ShardedQuantumState:
     def _allreduce(self, value: complex) -> complex:
         if self.dist is None or len(self.owned) == self.world:
             return value
+        if self._qcomm is not None:
+            sh = next(iter(self.shards.values()))
+            buf = (C.c_double * 2)(value.real, value.imag)
+            check(lib.qsv_comm_allreduce_sum(self._qcomm, sh.state._handle(),
+                                             C.cast(buf, C.c_void_p), 2))
+            return complex(buf[0], buf[1])
         import torch
         dev = "cpu"
         if self.dist.get_backend(self.group) == "nccl":
@@ -826,6 +881,15 @@ class ShardedQuantumState:
                 if r in done:
                     continue
                 partner = r ^ m
+                if partner not in self.shards and self._qcomm is not None:
+                    # grouped ncclSend / ncclRecv of the strided slice inside libqsv
+                    d = gbits(partner)
+                    arr = (C.c_int * k)(*ls)
+                    check(lib.qsv_comm_slice_exchange(self._qcomm, self.shards[r].state._handle(),
+                                                      partner, arr, k, d, d, self.chunk_bytes))
+                    done.add(r)
+                    self.stats["bytes_sent"] += 16 << (L - k)
+                    continue
                 mine = self._slice_view(r, ls, gbits(partner))
                 if partner in self.shards:
                     theirs = self._slice_view(partner, ls, gbits(r))

@@ -13,13 +13,15 @@ import torch  # noqa: E402
 import paper_2011_13524_b200 as qs  # noqa: E402
 from paper_2011_13524_b200 import workloads  # noqa: E402
 
-for n in (14, 16, 18, 20):
+NS = [int(v) for v in os.environ.get("NS", "14,16,18,20").split(",")]
+LS = [int(v) for v in os.environ.get("LS", "0,-1,8,9,10,11,12").split(",")]
+for n in NS:
     for fam in ("cnot-ring", "cz-ladder"):
         circ = (workloads.generate_cnot_ring(n, seed=1) if fam == "cnot-ring"
                 else workloads.generate_cz_ladder(n, 20, seed=1))
         st = qs.QuantumState(n)
         row = []
-        for L in (0, -1, 8, 9, 10, 11, 12):
+        for L in LS:
             if L == 0:
                 circ.set_plan_options(use_tiles=0)
             elif L == -1:
