@@ -15,6 +15,8 @@
 // pairs touch disjoint slices, so the 2^k - 1 rounds need no barrier between
 // them.
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "qsv_internal.cuh"
@@ -69,6 +71,49 @@ __global__ void __launch_bounds__(Threads) k_slice_swap(double2* __restrict__ a,
       }
     }
   }
+}
+
+// 32-byte variant: when the lowest slice bit is above bit 0, slice elements
+// 2i and 2i + 1 are adjacent amplitudes, so a thread moves the pair with one
+// 256-bit load / store on each side (half the memory instructions per byte,
+// the form of the HBM-bound gate kernels); pair range [p0, p1)
+template <int Threads>
+__global__ void __launch_bounds__(Threads) k_slice_swap2(double2* __restrict__ a,
+                                                         double2* __restrict__ b, SliceMap m,
+                                                         uint64_t p0, uint64_t p1) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = p0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; base < p1;
+       base += stride * kSwapPer) {
+    uint64_t ia[kSwapPer], ib[kSwapPer];
+    Amp2 va[kSwapPer], vb[kSwapPer];
+#pragma unroll
+    for (int i = 0; i < kSwapPer; ++i) {
+      const uint64_t j = base + i * stride;
+      const uint64_t x = spread(j << 1, m);
+      ia[i] = x | m.va;
+      ib[i] = x | m.vb;
+      if (j < p1) {
+        va[i] = ld2(a + ia[i]);
+        vb[i] = ld2(b + ib[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kSwapPer; ++i) {
+      if (base + i * stride < p1) {
+        st2(a + ia[i], vb[i]);
+        st2(b + ib[i], va[i]);
+      }
+    }
+  }
+}
+
+// QSV_SWAP_VEC=0 forces the 16-byte kernel (A/B of the exchange step)
+bool swap_vec2_enabled() {
+  static const int on = [] {
+    const char* e = getenv("QSV_SWAP_VEC");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
 }
 
 }  // namespace
@@ -154,6 +199,25 @@ int qsv_slice_swap(qsv_state* st, void* peer_amps, const int* ls, int k, uint64_
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st->device);
   double2* peer = static_cast<double2*>(peer_amps);
+  const bool vec2 = swap_vec2_enabled() && (k == 0 || m.pos[0] >= 1) && !(j0 & 1) && !(j1 & 1) &&
+                    !(reinterpret_cast<uintptr_t>(peer) & 31) &&
+                    !(reinterpret_cast<uintptr_t>(st->amps) & 31);
+  if (vec2) {
+    const uint64_t q0 = j0 >> 1, q1 = j1 >> 1;
+    const int threads = st->sm_limit > 0 ? kSwapFatThreads : kSwapThreads;
+    const uint64_t per_block = (uint64_t)threads * kSwapPer;
+    const uint64_t want = (q1 - q0 + per_block - 1) / per_block;
+    const uint64_t cap = st->sm_limit > 0 ? (uint64_t)std::min(st->sm_limit, sms) : (uint64_t)sms * 8;
+    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
+    if (st->sm_limit > 0)
+      k_slice_swap2<kSwapFatThreads><<<blocks, kSwapFatThreads, 0, st->stream>>>(st->amps, peer, m,
+                                                                                  q0, q1);
+    else
+      k_slice_swap2<kSwapThreads><<<blocks, kSwapThreads, 0, st->stream>>>(st->amps, peer, m, q0,
+                                                                          q1);
+    QSV_TRY(cudaGetLastError());
+    return QSV_OK;
+  }
   if (st->sm_limit > 0) {
     // overlapped with tile passes on another stream: at most sm_limit SMs,
     // one 1024-thread CTA each (the tile kernel's CTAs fill a whole SM, so

@@ -214,6 +214,16 @@ void emit_wht(EjGen& g, const std::string& base, int m) {
       }
 }
 
+// QSV_EXPECT_BULK=1: tiles move with cp.async.bulk + mbarrier (A/B; the
+// source differs, so the two variants are cached separately)
+bool ej_bulk() {
+  static const int on = [] {
+    const char* e = getenv("QSV_EXPECT_BULK");
+    return e ? atoi(e) : 0;
+  }();
+  return on != 0;
+}
+
 std::string ej_source(const EjPass& P) {
   EjGen g;
   g.line(R"JIT(typedef unsigned long long u64;
@@ -271,6 +281,55 @@ struct XParams { const double2* a; u64 ntiles; double* partials; FixedBits tb; }
     }
   }
   for (int t = 0; t < nt; ++t) g.line("  double acc" + I(t) + " = 0.0;");
+  if (ej_bulk()) {
+    // Blackwell bulk copies: each thread moves one 256-byte run (16
+    // amplitudes of qubits 0..3) with cp.async.bulk, completion counted by
+    // an mbarrier per buffer (tx bytes), instead of 16 cp.async of 16 bytes
+    {
+      std::string lr = "  const u64 lorun = 0ull";
+      for (int b = 0; b < 4; ++b)
+        lr += " | ((u64)((tid >> " + I(b) + ") & 1u) << " + I(P.spos[4 + b]) + ")";
+      for (int b = 0; b < 4; ++b)
+        lr += " | ((u64)((tid >> " + I(4 + b) + ") & 1u) << " + I(P.spos[8 + b]) + ")";
+      g.line(lr + ";");
+    }
+    g.line(R"JIT(  __shared__ __align__(8) u64 mbar[2];
+  const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(sbuf);
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+  // run tid: slot k = tid >> 4, first thread (tid & 15) << 4 -> smem element k*256 + (tid&15)*16
+  const uint32_t sofs = ((((tid >> 4) << 8) | ((tid & 15u) << 4)) << 4);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(mb0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(mb0 + 8) : "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  auto issue = [&](u64 t, int b) {
+    const double2* src = P.a + (widen(t, P.tb) | lorun);
+    const uint32_t mb = mb0 + 8u * (uint32_t)b;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 256;" ::"r"(mb) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];"
+                 ::"r"(sb0 + ((uint32_t)b << 16) + sofs), "l"(src), "r"(mb) : "memory");
+  };
+  auto wait = [&](int b, uint32_t parity) {
+    const uint32_t mb = mb0 + 8u * (uint32_t)b;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+  };
+  u64 tile = blockIdx.x;
+  int buf = 0;
+  uint32_t it = 0;
+  if (tile < P.ntiles) issue(tile, 0);
+  for (; tile < P.ntiles; tile += gridDim.x, ++it) {
+    buf = (int)(it & 1u);
+    wait(buf, (it >> 1) & 1u);
+    __syncthreads();
+    const u64 nxt = tile + gridDim.x;
+    if (nxt < P.ntiles) issue(nxt, buf ^ 1);)JIT");
+  } else {
   g.line(R"JIT(  const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(sbuf);
   u64 tile = blockIdx.x;
   int buf = 0;
@@ -292,8 +351,9 @@ struct XParams { const double2* a; u64 ntiles; double* partials; FixedBits tb; }
     g.line("      cp_async16(sbn + ((" + I(k * 256) + "u + tid) << 4), P.a + (gb | " +
            hex64(hi[k]) + "));");
   g.line(R"JIT(      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    const double2* sm = sbuf + (buf << 12);
+    })JIT");
+  }
+  g.line(R"JIT(    const double2* sm = sbuf + (buf << 12);
     const u64 base = widen(tile, P.tb);
     (void)base;
     double2 v[16];
