@@ -1213,6 +1213,32 @@ std::vector<PhaseOp> emit_flush(Encoded& e, const std::vector<PhaseOp>& dl, cons
   return rest;
 }
 
+// QSV_JIT_DIRECT_STORE=0: generated passes write tiles back through shared
+// memory even when the last phase could store from registers (A/B)
+inline bool jit_direct_store() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_DIRECT_STORE");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
+inline int max_pass_phases() {
+  static const int v = [] {
+    const char* e = getenv("QSV_MAX_PASS_PHASES");
+    return e ? std::max(1, atoi(e)) : 1 << 30;
+  }();
+  return v;
+}
+
+inline int jit_stagger_max_phases() {
+  static const int v = [] {
+    const char* e = getenv("QSV_STAGGER_MAX_PHASES");
+    return e ? atoi(e) : 1 << 30;
+  }();
+  return v;
+}
+
 // QSV_PDL=1: generated pass kernels launch with programmatic dependent launch
 // (the next pass queued while this one drains).  Off by default: measured
 // slower on every small-state circuit (cnot-ring(14) 0.117 -> 0.138 ms,
@@ -1944,11 +1970,20 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       continue;
     }
     std::vector<const GateDesc*> pg;
-    for (int k : ps.taken) {
-      pg.push_back(&gates[k]);
-      done[k] = 1;
-    }
+    for (int k : ps.taken) pg.push_back(&gates[k]);
     Encoded e = encode_pass(n, L, ps.S, pg);
+    // deep passes: cap the phase count (the generated code of a phase is
+    // ~10 KB of SASS; far beyond the instruction cache every tile refetches
+    // it).  A prefix of the taken gates is itself a valid pass: the rest stay
+    // pending and start the next pass (QSV_MAX_PASS_PHASES, A/B).
+    const int cap = max_pass_phases();
+    while ((int)e.phases.size() > cap && pg.size() > 1) {
+      const size_t keep = std::max<size_t>(1, pg.size() * (size_t)cap / e.phases.size());
+      pg.resize(std::min(pg.size() - 1, keep));
+      e = encode_pass(n, L, ps.S, pg);
+    }
+    ps.taken.resize(pg.size());
+    for (int k : ps.taken) done[k] = 1;
     if (getenv("QSV_PLAN_DUMP")) {
       fprintf(stderr, "pass %zu: %zu gates, %zu phases, %zu ops, %zu data, fp64 ops/amp %.1f\n",
               tiles.size(), pg.size(), e.phases.size(), e.ops.size(), e.data.size(),
@@ -2089,6 +2124,12 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
       h.nostagger = ntiles_all <= (uint64_t)kGroups * grid;
     }
     if (ntiles_all <= (uint64_t)sms * per_sm) h.nostagger = 0;
+    // deep passes: the generated code (~10 KB of SASS per phase) exceeds the
+    // instruction cache, so two groups half a tile apart stream two code
+    // regions; starting them together lets them share the fetched code
+    // (QSV_STAGGER_MAX_PHASES, A/B)
+    if (tp.nphases > jit_stagger_max_phases() && ntiles_all > (uint64_t)sms * per_sm)
+      h.nostagger = 1;
     memcpy(pbuf.data(), &h, sizeof(h));
     memcpy(pbuf.data() + sizeof(h), tp.jit_data.data(), sizeof(double2) * tp.jit_data.size());
     int rc = jit_set_smem(tp.jit, tp.jit_smem);

@@ -355,7 +355,12 @@ struct Gen {
     if (!cond.empty()) line("}");
   }
 
-  void reg_phase(const TilePhase& P) {
+  // `prefetch`: code issuing the next tile's copy-in.  With it this is the
+  // pass's last phase and its lanes cover local bits 0..3 (256-byte HBM
+  // runs): the tile buffer is free once the amplitudes are in registers, so
+  // the next tile streams in while this phase computes, and the results go
+  // from registers straight to HBM (no shared-memory write-back).
+  void reg_phase(const TilePhase& P, const std::string& prefetch = std::string()) {
     std::vector<int> thr;
     for (int j = 0; j < L - R; ++j) thr.push_back(P.thrpos[j]);
     line("{ // register phase");
@@ -372,7 +377,27 @@ struct Gen {
       cj[j] = ad;
       line("v[" + std::to_string(j) + "] = sm[slt ^ " + std::to_string(ad) + "u];");
     }
+    if (!prefetch.empty()) {
+      line("group_sync(group);");
+      line(prefetch);
+    }
     for (int o = P.op_begin; o < P.op_end; ++o) reg_op(e.ops[o]);
+    if (!prefetch.empty()) {
+      // global index of local index l: bit b of l -> qubit spos[b]
+      std::string gl = "const u64 gl_ = base";
+      for (int b = 0; b < L - R; ++b)
+        gl += " | ((u64)((tid >> " + std::to_string(b) + ") & 1u) << " +
+              std::to_string(e.pd.spos[P.thrpos[b]]) + ")";
+      line(gl + ";");
+      for (int j = 0; j < R2; ++j) {
+        uint64_t h = 0;
+        for (int i = 0; i < R; ++i)
+          if ((j >> i) & 1) h |= 1ULL << e.pd.spos[P.regpos[i]];
+        line("st1(a + (gl_ | " + hex64(h) + "), v[" + std::to_string(j) + "]);");
+      }
+      line("}");
+      return;
+    }
     for (int j = 0; j < R2; ++j)
       line("sm[slt ^ " + std::to_string(cj[j]) + "u] = v[" + std::to_string(j) + "];");
     line("}");
@@ -512,7 +537,7 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
        ", 1) k_pass(const __grid_constant__ PassParams P) {\n";
   o += R"JIT(
   extern __shared__ double2 smem_all[];
-  __shared__ u64 s_next[QSV_GROUPS];
+  __shared__ u64 s_next[QSV_GROUPS][2];
   __shared__ int s_go_;
   double2* __restrict__ a = P.a;
   const int group = threadIdx.x / QSV_G;
@@ -548,25 +573,33 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
       if (((k >> b) & 1) && tidbits + b < L) hi[k] |= 1ULL << e.pd.spos[tidbits + b];
     sk[k] = swz_host((uint32_t)k * (uint32_t)G);
   }
-  o += R"JIT(
-  if (tid == 0) s_next[group] = atomicAdd(P.ctr, 1ull);
-  group_sync(group);
-  u64 tile = s_next[group];
-  const int nph_total = )JIT" + std::to_string(std::max<size_t>(1, e.phases.size())) + R"JIT(;
-  while (tile < P.ntiles) {
-    u64 next = 0;
-    if (tid == 0) next = atomicAdd(P.ctr, 1ull);
-    const u64 base = widen(tile, P.tb);
-    {
-      const u64 gb = base | lo_part;
-      const uint32_t st = swz(tid);
-)JIT";
+  // copy-in of tile `t_` into this group's buffer (16-byte cp.async, swizzled slots)
+  std::string copy_in = "{ const u64 gb_ = widen(t_, P.tb) | lo_part; const uint32_t st_ = swz(tid);\n";
   for (int k = 0; k < kRegs; ++k)
-    o += "      cp_async16(sbase + ((" + std::to_string(sk[k]) + "u ^ st) << 4), a + (gb | " +
-         hex64(hi[k]) + "));\n";
-  o += R"JIT(      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    copy_in += "  cp_async16(sbase + ((" + std::to_string(sk[k]) + "u ^ st_) << 4), a + (gb_ | " +
+               hex64(hi[k]) + "));\n";
+  copy_in += "  asm volatile(\"cp.async.commit_group;\" ::: \"memory\"); }";
+  auto copy_of = [&](const std::string& t) {
+    return "{ const u64 t_ = " + t + "; if (t_ < P.ntiles) " + copy_in + " }";
+  };
+  // direct store from the last phase's registers when that phase's lanes hold
+  // local bits 0..3 (QSV_JIT_DIRECT_STORE=0 disables, A/B)
+  const TilePhase* lastp = e.phases.empty() ? nullptr : &e.phases.back();
+  bool direct = lastp && lastp->type == 0 && L - kRegBits >= 4 && jit_direct_store();
+  for (int b = 0; direct && b < 4; ++b) direct = lastp->thrpos[b] == b;
+  // the next tile is prefetched as soon as this tile's buffer is free
+  o += R"JIT(
+  if (tid == 0) s_next[group][0] = atomicAdd(P.ctr, 1ull);
+  group_sync(group);
+  u64 tile = s_next[group][0];
+  uint32_t it_ = 1;
+)JIT";
+  o += "  " + copy_of("tile") + "\n";
+  o += R"JIT(  const int nph_total = )JIT" + std::to_string(std::max<size_t>(1, e.phases.size())) + R"JIT(;
+  while (tile < P.ntiles) {
+    if (tid == 0) s_next[group][it_ & 1u] = atomicAdd(P.ctr, 1ull);
+    const u64 base = widen(tile, P.tb);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     group_sync(group);
 )JIT";
   int ph_idx = 0;
@@ -575,24 +608,28 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
     // release group k once group 0 is k / kGroups of the way through its first tile
     o += "    if (group == 0 && first && tid == 0 && " + std::to_string(ph_idx) +
          " * QSV_GROUPS >= (*s_go + 1) * nph_total && *s_go < QSV_GROUPS - 1) *s_go = *s_go + 1;\n";
-    if (P.type == 0) g.reg_phase(P);
+    const bool last = ph_idx == nph - 1;
+    if (P.type == 0 && last && direct)
+      g.reg_phase(P, "const u64 nxt_ = s_next[group][it_ & 1u]; " + copy_of("nxt_"));
+    else if (P.type == 0) g.reg_phase(P);
     else g.smem_phase(P);
     ++ph_idx;
   }
-  (void)nph;
-  o += R"JIT(
+  if (!direct) {
+    o += R"JIT(
     {
       const u64 gb = base | lo_part;
       const uint32_t st = swz(tid);
 )JIT";
-  for (int k = 0; k < kRegs; ++k)
-    o += "      st1(a + (gb | " + hex64(hi[k]) + "), sm[" + std::to_string(sk[k]) + "u ^ st]);\n";
-  o += R"JIT(    }
-    if (tid == 0) s_next[group] = next;
-    group_sync(group);
-    if (group == 0 && first && tid == 0) *s_go = QSV_GROUPS;
+    for (int k = 0; k < kRegs; ++k)
+      o += "      st1(a + (gb | " + hex64(hi[k]) + "), sm[" + std::to_string(sk[k]) + "u ^ st]);\n";
+    o += "    }\n    group_sync(group);\n";
+    o += "    " + copy_of("s_next[group][it_ & 1u]") + "\n";
+  }
+  o += R"JIT(    if (group == 0 && first && tid == 0) *s_go = QSV_GROUPS;
     first = false;
-    tile = s_next[group];
+    tile = s_next[group][it_ & 1u];
+    ++it_;
   }
   if (group == 0 && tid == 0) *s_go = QSV_GROUPS;
   __syncthreads();
