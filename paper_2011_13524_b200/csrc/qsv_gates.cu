@@ -388,6 +388,87 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Dense K = 5 on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).  A fused
+// 5-qubit block is a 32x32 complex matrix times 32-amplitude cosets, i.e. the
+// real GEMM [Or; Oi] = [[Mr, -Mi], [Mi, Mr]] [Ir; Ii] with a 64x64 A and one
+// column per coset.  A warp takes 8 cosets (one n = 8 column tile): each lane
+// (g = lane / 4, t = lane % 4) loads the 8 amplitudes w = t (mod 4) of coset
+// g -- exactly its B fragments for the 16 k-steps -- then runs 8 row tiles x 16
+// k-steps = 128 DMMA with the 8 row-tile accumulators interleaved (8
+// independent chains), and stores its D fragments: rows g, g+8, g+16, g+24
+// (real parts from row tiles 0..3, imaginary from 4..7) of cosets 2t, 2t+1.
+// A fragments come from shared memory pre-permuted into fragment order (one
+// conflict-free 256-byte LDS per DMMA).  Same FLOPs as k_dense5 (128 real
+// FMA per amplitude), on the DMMA pipe (measured 36.4 vs 31.7 TFLOP/s DFMA,
+// profiles/fp64_peak.json).  Reference: the zgemm path kernels.py:100-106.
+constexpr int kMmaThreads = 256;
+__global__ void __launch_bounds__(kMmaThreads)
+    k_dense5_mma(double2* __restrict__ a, FixedBits fb, const double2* __restrict__ mat,
+                 const uint64_t* __restrict__ offs, uint64_t ncos) {
+  __shared__ double sA[8 * 16 * 32];  // [row tile][k step][lane]
+  __shared__ uint64_t sO[32];
+  for (int i = threadIdx.x; i < 8 * 16 * 32; i += kMmaThreads) {
+    const int r = i >> 9, st = (i >> 5) & 15, ln = i & 31;
+    const int row = 8 * r + (ln >> 2), col = 4 * st + (ln & 3);  // into the 64x64 real A
+    const double2 m = mat[(row & 31) * 32 + (col & 31)];
+    // [[Mr, -Mi], [Mi, Mr]]
+    sA[i] = (row < 32) == (col < 32) ? m.x : (row < 32 ? -m.y : m.y);
+  }
+  if (threadIdx.x < 32) sO[threadIdx.x] = offs[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const uint64_t warps = (uint64_t)gridDim.x * (kMmaThreads / 32);
+  const uint64_t ntile = (ncos + 7) / 8;
+  for (uint64_t ct = (uint64_t)blockIdx.x * (kMmaThreads / 32) + (threadIdx.x >> 5); ct < ntile;
+       ct += warps) {
+    const uint64_t cin = ct * 8 + g;
+    double b[16];
+    if (cin < ncos) {
+      const uint64_t x0 = widen(cin, fb);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 v = ld1(a + (x0 | sO[4 * q + t]));
+        b[q] = v.x;
+        b[8 + q] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) b[q] = 0.0;
+    }
+    double d[8][2];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) d[r][0] = d[r][1] = 0.0;
+#pragma unroll
+    for (int st = 0; st < 16; ++st) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const double av = sA[((r << 4) | st) * 32 + lane];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(d[r][0]), "+d"(d[r][1])
+                     : "d"(av), "d"(b[st]));
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint64_t cout = ct * 8 + 2 * t + h;
+      if (cout >= ncos) continue;
+      const uint64_t x0 = widen(cout, fb);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        st1(a + (x0 | sO[8 * r + g]), make_double2(d[r][h], d[r + 4][h]));
+    }
+  }
+}
+
+// QSV_DENSE5_MMA=0 keeps the DFMA kernel (A/B)
+bool dense5_mma_enabled() {
+  static const int on = [] {
+    const char* e = getenv("QSV_DENSE5_MMA");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 // Sparse / permutation (kernels.py:141-152, 176-185): cosets staged in shared
 // memory like k_dense_smem, each output row summed over its CSR entries
 // (O(nnz) per coset instead of 4^K).  Payload: values, coset offsets,
@@ -932,6 +1013,15 @@ int launch_gate(double2* a, int n, const GateDesc& g0, const Cplx* dev_data, cud
   }
   const int D = 1 << m;
   const uint64_t* offs = reinterpret_cast<const uint64_t*>(dev_data + (size_t)D * D);
+  if (m == 5 && dense5_mma_enabled() && ncos >= 8) {
+    const uint64_t tiles = (ncos + 7) / 8;
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((tiles + kMmaThreads / 32 - 1) / (kMmaThreads / 32), 148ULL * 8));
+    k_dense5_mma<<<grid, kMmaThreads, 0, s>>>(a, fb, reinterpret_cast<const double2*>(dev_data),
+                                              offs, ncos);
+    QSV_CHECK_LAUNCH("k_dense5_mma");
+    return QSV_OK;
+  }
   if (m == 5) {
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((ncos + kThreads - 1) / kThreads, 148ULL * 8));
