@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstring>
 #include <atomic>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -84,7 +85,9 @@ struct EjPlan {
 
 std::mutex g_ej_mu;
 std::atomic<long> g_ej_jit_passes{0}, g_ej_generic_passes{0};
-std::unordered_map<std::string, EjPlan> g_ej_plans;
+// plans are shared_ptr so an evaluation keeps its plan alive while another
+// thread trims the cache; compile decisions are taken under g_ej_mu
+std::unordered_map<std::string, std::shared_ptr<EjPlan>> g_ej_plans;
 
 std::string hex64(uint64_t v) {
   char b[32];
@@ -533,28 +536,26 @@ int expect_tile_jit(const double2* a, int n, const std::vector<uint64_t>& xms,
   std::string key(reinterpret_cast<const char*>(&n), sizeof(n));
   key.append(reinterpret_cast<const char*>(xms.data()), xms.size() * sizeof(uint64_t));
   key.append(reinterpret_cast<const char*>(zms.data()), zms.size() * sizeof(uint64_t));
-  EjPlan* plan;
-  {
-    std::lock_guard<std::mutex> lk(g_ej_mu);
-    if (g_ej_plans.size() > 256) g_ej_plans.clear();
-    auto it = g_ej_plans.find(key);
-    if (it == g_ej_plans.end()) {
-      EjPlan p;
-      p.n = n;
-      if (!ej_pack(n, xms, zms, p.passes)) return QSV_EUNSUPPORTED;
-      for (EjPass& P : p.passes) P.src = ej_source(P);
-      if (const char* dir = getenv("QSV_JIT_DUMP")) {
-        for (size_t i = 0; i < p.passes.size(); ++i)
-          if (FILE* f = fopen((std::string(dir) + "/xpass_" + std::to_string(i) + ".cu").c_str(), "w")) {
-            fputs(p.passes[i].src.c_str(), f);
-            fclose(f);
-          }
-      }
-      it = g_ej_plans.emplace(key, std::move(p)).first;
+  std::shared_ptr<EjPlan> plan;
+  std::lock_guard<std::mutex> lk(g_ej_mu);
+  if (g_ej_plans.size() > 256) g_ej_plans.clear();
+  auto it = g_ej_plans.find(key);
+  if (it == g_ej_plans.end()) {
+    auto p = std::make_shared<EjPlan>();
+    p->n = n;
+    if (!ej_pack(n, xms, zms, p->passes)) return QSV_EUNSUPPORTED;
+    for (EjPass& P : p->passes) P.src = ej_source(P);
+    if (const char* dir = getenv("QSV_JIT_DUMP")) {
+      for (size_t i = 0; i < p->passes.size(); ++i)
+        if (FILE* f = fopen((std::string(dir) + "/xpass_" + std::to_string(i) + ".cu").c_str(), "w")) {
+          fputs(p->passes[i].src.c_str(), f);
+          fclose(f);
+        }
     }
-    plan = &it->second;
-    ++plan->evals;
+    it = g_ej_plans.emplace(key, std::move(p)).first;
   }
+  plan = it->second;
+  ++plan->evals;
   if (!plan->tried) {
     bool cached = true;
     for (const EjPass& P : plan->passes) cached = cached && jit_cached(P.src);
