@@ -912,10 +912,12 @@ struct PassSel {
 // a qubit with it and its active qubits fit in S (growing S up to L).
 PassSel select_pass(int n, int L, const std::vector<GateDesc>& gates,
                     const std::vector<uint64_t>& act, const std::vector<char>& ok,
-                    const std::vector<char>& done, size_t first, uint64_t outer) {
+                    const std::vector<char>& done, size_t first, uint64_t outer,
+                    uint64_t seed = 0) {
   PassSel ps;
   const int c = std::min(kLowQubits, n);
   ps.S = (c >= 64) ? ~0ULL : ((1ULL << c) - 1);
+  ps.S |= seed;
   uint64_t blocked = 0;
   const uint64_t all = (n >= 64) ? ~0ULL : ((1ULL << n) - 1);
   size_t budget = kTileProgramBudget;  // staged program must fit in shared memory
@@ -1221,6 +1223,16 @@ inline bool jit_direct_store() {
     return e ? atoi(e) : 1;
   }();
   return on != 0;
+}
+
+// QSV_PASS_SEARCH: 0 plain greedy, 1 multi-start (default), 2 multi-start
+// with one pass of lookahead (A/B)
+inline int pass_search() {
+  static const int mode = [] {
+    const char* e = getenv("QSV_PASS_SEARCH");
+    return e ? atoi(e) : 1;
+  }();
+  return mode;
 }
 
 inline int max_pass_phases() {
@@ -1957,6 +1969,56 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       continue;
     }
     PassSel ps = select_pass(n, L, gates, act, ok, done, first, opts.outer_mask);
+    if (pass_search()) {
+      // Multi-start: the greedy lets the first pending gates decide the tile
+      // set; also seed it with the active qubits of the first pending gate on
+      // each qubit and keep the pass that takes the most gates (for
+      // nearest-neighbour circuits the best window is often not the one at
+      // the lowest pending gate).  Mode 2 scores a candidate by its gates
+      // plus the best next pass after it.
+      auto seeds_of = [&](const std::vector<char>& dn, size_t from) {
+        std::vector<uint64_t> seeds;
+        uint64_t seen = 0;
+        for (size_t i = from; i < G && seen != ~0ULL; ++i) {
+          if (dn[i] || !ok[i]) continue;
+          const uint64_t A = act[i] & ~lowq;
+          if (!A || (A & seen) == A) continue;
+          seen |= A;
+          if (popc64(A | lowq) <= L && std::find(seeds.begin(), seeds.end(), A) == seeds.end())
+            seeds.push_back(A);
+          if ((int)seeds.size() >= 2 * n) break;
+        }
+        return seeds;
+      };
+      auto best_single = [&](const std::vector<char>& dn, size_t from) {
+        size_t best = select_pass(n, L, gates, act, ok, dn, from, opts.outer_mask).taken.size();
+        for (uint64_t sd : seeds_of(dn, from))
+          best = std::max(best,
+                          select_pass(n, L, gates, act, ok, dn, from, opts.outer_mask, sd).taken.size());
+        return best;
+      };
+      std::vector<PassSel> cands;
+      cands.push_back(ps);
+      for (uint64_t sd : seeds_of(done, first))
+        cands.push_back(select_pass(n, L, gates, act, ok, done, first, opts.outer_mask, sd));
+      size_t best_score = 0, best_i = 0;
+      std::vector<char> dn;
+      for (size_t c = 0; c < cands.size(); ++c) {
+        size_t score = cands[c].taken.size();
+        if (pass_search() >= 2 && score > 0) {
+          dn = done;
+          for (int k : cands[c].taken) dn[k] = 1;
+          size_t nf = first;
+          while (nf < G && dn[nf]) ++nf;
+          if (nf < G) score += best_single(dn, nf);
+        }
+        if (score > best_score) {
+          best_score = score;
+          best_i = c;
+        }
+      }
+      ps = std::move(cands[best_i]);
+    }
     if (popc64(ps.S) < L || (ps.S & opts.outer_mask)) {
       set_error("outer mask leaves too few tile qubits (%d qubits, tile %d)", n, L);
       return QSV_EINVAL;

@@ -56,6 +56,12 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
     const PlanMix mix = estimate_mix(pre);
     const int r5_score = mix.real_ops / 2 + 4 * mix.wide_dense;
     use5 = r5_score > 0 && r5_score >= mix.complex_ops;
+    // generated pass kernels (the steady state of a program run more than
+    // once): the 16-amplitude variant is as fast at n = 28..30 (cz-ladder(30)
+    // 272 vs 268 ms, (28) 64.1 vs 64.8 ms) and faster on small states
+    // (cz-ladder(14) 0.108 vs 0.149 ms, (18) 0.156 vs 0.206 ms, (22) 0.84 vs
+    // 0.98 ms; profiles/r2_variants_jit.txt): twice the warps per SM
+    if (opts.jit && mix.wide_dense == 0) use5 = false;
   }
   if (force == 4 && on4 != on5)
     return r4::plan_program(n, gates, opts, steps, tiles, payload, stats, nullptr, false);
