@@ -122,6 +122,11 @@ struct TilePlan {
   JitKernel jit;
 };
 
+// tile-set search mode of the planner for the current thread (-1: the
+// QSV_PASS_SEARCH default); plan_program (qsv_tile_select.cu) plans with
+// several modes and keeps the plan with the fewest passes
+inline thread_local int tl_pass_search = -1;
+
 // per-variant entry points (qsv_tile_r4.cu / qsv_tile_r5.cu)
 struct PlanMix {
   int real_ops = 0, complex_ops = 0;  // register 2x2 ops after encoding (+ narrow smem ops)

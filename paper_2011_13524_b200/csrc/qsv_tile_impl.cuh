@@ -1230,9 +1230,9 @@ inline bool jit_direct_store() {
 inline int pass_search() {
   static const int mode = [] {
     const char* e = getenv("QSV_PASS_SEARCH");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
-  return mode;
+  return tl_pass_search >= 0 ? tl_pass_search : mode;
 }
 
 inline int max_pass_phases() {

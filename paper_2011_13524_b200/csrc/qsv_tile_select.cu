@@ -118,6 +118,32 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
     }
     return have ? QSV_OK : best_rc;
   }
+  // Larger states: the tile-set search with one pass of lookahead usually
+  // packs the circuit into fewer passes, but not always (cz-ladder(28): 17
+  // passes vs 16 without the lookahead); each pass costs at least one HBM
+  // sweep, so plan both and keep the one with fewer passes (lookahead on a
+  // tie).  Measured: cz-ladder(30) 19 -> 18 passes, 253 -> 245 ms; VQE(24)
+  // 7 -> 5 passes, 1.32 -> 1.15 ms; cz-ladder(28) keeps 16 (54.7 ms).
+  if (!getenv("QSV_PASS_SEARCH") && opts.outer_mask == 0) {
+    std::vector<Step> st1;
+    std::vector<TilePlan> tp1;
+    std::vector<char> pl1;
+    qsv_program_stats ps1 = *stats;
+    tl_pass_search = 1;
+    const int rc1 = plan_with(opts, st1, tp1, pl1, &ps1);
+    tl_pass_search = 2;
+    const int rc2 = plan_with(opts, steps, tiles, payload, stats);
+    tl_pass_search = -1;
+    if (rc2 != QSV_OK) {
+      if (rc1 != QSV_OK) return rc2;
+      steps.swap(st1), tiles.swap(tp1), payload.swap(pl1), *stats = ps1;
+      return QSV_OK;
+    }
+    if (rc1 == QSV_OK && ps1.num_steps < stats->num_steps) {
+      steps.swap(st1), tiles.swap(tp1), payload.swap(pl1), *stats = ps1;
+    }
+    return QSV_OK;
+  }
   return plan_with(opts, steps, tiles, payload, stats);
 }
 
