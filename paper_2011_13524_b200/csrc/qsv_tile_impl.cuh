@@ -25,7 +25,9 @@
 #include <set>
 #include <cstdlib>
 #include <stdexcept>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "qsv_tile.cuh"
 
@@ -1225,6 +1227,10 @@ inline bool jit_direct_store() {
   return on != 0;
 }
 
+// recorded pass selections by gate-list structure (plan_program)
+inline std::mutex g_sel_mu;
+inline std::unordered_map<std::string, std::vector<PassSel>> g_sel_cache;
+
 // QSV_PASS_SEARCH: 0 plain greedy, 1 multi-start (default), 2 multi-start
 // with one pass of lookahead (A/B)
 inline int pass_search() {
@@ -1959,6 +1965,31 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
   for (size_t i = 0; i < G; ++i)
     ok[i] = active_qubits(gates[i], &act[i]) && popc64(act[i] | lowq) <= L &&
             !(act[i] & opts.outer_mask);
+  // Pass selections depend only on the gate list's structure (kinds, widths,
+  // qubits, active masks), not on angles: a ParametricCircuit recompiled
+  // after set_parameter replays the recorded selections instead of running
+  // the tile-set search again (the lookahead search costs a few ms).
+  std::string fp;
+  {
+    const uint64_t hdr[6] = {(uint64_t)n, (uint64_t)L, opts.outer_mask, (uint64_t)pass_search(),
+                             (uint64_t)max_pass_phases(), (uint64_t)G};
+    fp.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+    for (size_t i = 0; i < G; ++i) {
+      const GateDesc& g = gates[i];
+      const uint64_t rec[5] = {(uint64_t)g.kind | ((uint64_t)g.m << 8) | ((uint64_t)g.nc << 16),
+                               act[i], (uint64_t)ok[i], touched_mask(g),
+                               (uint64_t)(g.kind == QSV_OP_DENSE && g.m == 1)};
+      fp.append(reinterpret_cast<const char*>(rec), sizeof(rec));
+    }
+  }
+  std::vector<PassSel> replay, record;
+  size_t replay_at = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_sel_mu);
+    auto it = g_sel_cache.find(fp);
+    if (it != g_sel_cache.end()) replay = it->second;
+  }
+  const bool replaying = !replay.empty();
   size_t first = 0;
   while (true) {
     while (first < G && done[first]) ++first;
@@ -1968,7 +1999,11 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       done[first] = 1;
       continue;
     }
-    PassSel ps = select_pass(n, L, gates, act, ok, done, first, opts.outer_mask);
+    PassSel ps;
+    if (replaying && replay_at < replay.size()) {
+      ps = replay[replay_at++];
+    } else {
+    ps = select_pass(n, L, gates, act, ok, done, first, opts.outer_mask);
     if (pass_search()) {
       // Multi-start: the greedy lets the first pending gates decide the tile
       // set; also seed it with the active qubits of the first pending gate on
@@ -2019,6 +2054,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       }
       ps = std::move(cands[best_i]);
     }
+    }  // selection (searched or replayed)
     if (popc64(ps.S) < L || (ps.S & opts.outer_mask)) {
       set_error("outer mask leaves too few tile qubits (%d qubits, tile %d)", n, L);
       return QSV_EINVAL;
@@ -2029,6 +2065,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
       // program must run block by block: there every step is a tile pass)
       add_gate_step(n, gates[ps.taken[0]], steps, payload, stats);
       done[ps.taken[0]] = 1;
+      if (!replaying) record.push_back(ps);
       continue;
     }
     std::vector<const GateDesc*> pg;
@@ -2046,6 +2083,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
     }
     ps.taken.resize(pg.size());
     for (int k : ps.taken) done[k] = 1;
+    if (!replaying) record.push_back(ps);
     if (getenv("QSV_PLAN_DUMP")) {
       fprintf(stderr, "pass %zu: %zu gates, %zu phases, %zu ops, %zu data, fp64 ops/amp %.1f\n",
               tiles.size(), pg.size(), e.phases.size(), e.ops.size(), e.data.size(),
@@ -2123,6 +2161,11 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
     stats->num_tile_passes += 1;
     stats->num_steps += 1;
     stats->hbm_bytes += tp.hbm_bytes;
+  }
+  if (!replaying && !record.empty()) {
+    std::lock_guard<std::mutex> lk(g_sel_mu);
+    if (g_sel_cache.size() >= 64) g_sel_cache.clear();
+    g_sel_cache.emplace(std::move(fp), std::move(record));
   }
   return QSV_OK;
 }

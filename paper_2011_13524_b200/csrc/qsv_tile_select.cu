@@ -5,6 +5,9 @@
 // QSV_TILE_VARIANT=4|5 forces one (A/B experiments).
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
+#include <string>
+#include <unordered_map>
 
 #include "qsv_tile.cuh"
 
@@ -37,6 +40,9 @@ static PlanMix estimate_mix(const std::vector<GateDesc>& gates) {
   }
   return m;
 }
+
+static std::mutex g_mode_mu;
+static std::unordered_map<std::string, int> g_mode_cache;  // structure -> search mode
 
 int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts& opts,
                  std::vector<Step>& steps, std::vector<TilePlan>& tiles,
@@ -125,24 +131,58 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
   // tie).  Measured: cz-ladder(30) 19 -> 18 passes, 253 -> 245 ms; VQE(24)
   // 7 -> 5 passes, 1.32 -> 1.15 ms; cz-ladder(28) keeps 16 (54.7 ms).
   if (!getenv("QSV_PASS_SEARCH") && opts.outer_mask == 0) {
+    // the winning mode is remembered by gate-list structure, so a
+    // ParametricCircuit recompiled after set_parameter plans once
+    std::string fp;
+    {
+      const int32_t hdr[6] = {n, opts.tile_qubits, opts.fuse, opts.real_frames, opts.use_tiles,
+                              (int32_t)pre.size()};
+      fp.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+      for (const GateDesc& g : pre) {
+        const int32_t rec[3] = {g.kind | (g.m << 8) | (g.nc << 16), g.rf, 0};
+        fp.append(reinterpret_cast<const char*>(rec), sizeof(rec));
+        fp.append(reinterpret_cast<const char*>(g.targets), sizeof(int) * g.m);
+        fp.append(reinterpret_cast<const char*>(g.cq), sizeof(int) * g.nc);
+        fp.append(reinterpret_cast<const char*>(g.cv), sizeof(int) * g.nc);
+      }
+    }
+    {
+      std::lock_guard<std::mutex> lk(g_mode_mu);
+      auto it = g_mode_cache.find(fp);
+      if (it != g_mode_cache.end()) {
+        tl_pass_search = it->second;
+        const int rc = plan_with(opts, steps, tiles, payload, stats);
+        tl_pass_search = -1;
+        return rc;
+      }
+    }
+    // the multi-start plan is only counted (no kernel sources generated);
+    // it is planned again in full only when it wins
+    qsv_plan_opts count_only = opts;
+    count_only.jit = 0;
     std::vector<Step> st1;
     std::vector<TilePlan> tp1;
     std::vector<char> pl1;
     qsv_program_stats ps1 = *stats;
+    const qsv_program_stats init = *stats;
     tl_pass_search = 1;
-    const int rc1 = plan_with(opts, st1, tp1, pl1, &ps1);
+    const int rc1 = plan_with(count_only, st1, tp1, pl1, &ps1);
     tl_pass_search = 2;
-    const int rc2 = plan_with(opts, steps, tiles, payload, stats);
+    int rc = plan_with(opts, steps, tiles, payload, stats);
+    int mode = 2;
+    if (rc1 == QSV_OK && (rc != QSV_OK || ps1.num_steps < stats->num_steps)) {
+      steps.clear(), tiles.clear(), payload.clear();
+      *stats = init;
+      tl_pass_search = mode = 1;
+      rc = plan_with(opts, steps, tiles, payload, stats);
+    }
     tl_pass_search = -1;
-    if (rc2 != QSV_OK) {
-      if (rc1 != QSV_OK) return rc2;
-      steps.swap(st1), tiles.swap(tp1), payload.swap(pl1), *stats = ps1;
-      return QSV_OK;
+    if (rc == QSV_OK) {
+      std::lock_guard<std::mutex> lk(g_mode_mu);
+      if (g_mode_cache.size() >= 64) g_mode_cache.clear();
+      g_mode_cache.emplace(std::move(fp), mode);
     }
-    if (rc1 == QSV_OK && ps1.num_steps < stats->num_steps) {
-      steps.swap(st1), tiles.swap(tp1), payload.swap(pl1), *stats = ps1;
-    }
-    return QSV_OK;
+    return rc;
   }
   return plan_with(opts, steps, tiles, payload, stats);
 }
