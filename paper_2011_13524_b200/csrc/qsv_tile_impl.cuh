@@ -1249,6 +1249,15 @@ inline int max_pass_phases() {
   return v;
 }
 
+// QSV_JIT_WARP_LOCAL=0: every phase transition uses the group barrier (A/B)
+inline bool jit_warp_local() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_WARP_LOCAL");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 inline int jit_stagger_max_phases() {
   static const int v = [] {
     const char* e = getenv("QSV_STAGGER_MAX_PHASES");
@@ -1423,6 +1432,17 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
         local_of[q] = j++;
       }
   }
+  // 1-qubit dense gates by local target bit, in pass order (warp-bit choice)
+  std::vector<std::vector<size_t>> uses(L);
+  for (size_t i = 0; i < pg.size(); ++i)
+    if (pg[i]->kind == QSV_OP_DENSE && pg[i]->m == 1 && local_of[pg[i]->targets[0]] >= 0)
+      uses[local_of[pg[i]->targets[0]]].push_back(i);
+  size_t gi = 0;  // index of the gate being encoded
+  auto next_use = [&](int b) -> size_t {
+    auto it = std::lower_bound(uses[b].begin(), uses[b].end(), gi);
+    return it == uses[b].end() ? (size_t)-1 : *it;
+  };
+  std::vector<int> cur_warp;  // warp-index bit positions of the last register phase
   // current register phase: ops collected with their own data, scheduled at close
   bool open = false;
   uint32_t R = 0;
@@ -1454,10 +1474,35 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
       ph.regpos[i] = order[i];
       slot_of[order[i]] = i;
     }
+    // thread bits: lanes (tid bits 0..4) then warp-index bits.  The warp
+    // bits are kept from phase to phase while no register bit needs them, so
+    // a transition only permutes data inside each warp and the generated
+    // kernel synchronises it with __syncwarp instead of the group barrier;
+    // when they must change, the new warp bits are the non-register bits
+    // whose next 1-qubit use lies furthest ahead (they stay warp bits longest)
+    const int nwarp = std::max(0, (L - kRegBits) - 5);
+    bool keep = (int)cur_warp.size() == nwarp;
+    for (int b : cur_warp) keep = keep && !((Rall >> b) & 1u);
+    if (!keep) {
+      // local bits 0..3 (qubits 0..3, the 256-byte HBM runs) stay lane bits
+      // where possible: the direct store of a pass's last phase needs them
+      std::vector<int> cand;
+      for (int b = 0; b < L; ++b)
+        if (!((Rall >> b) & 1u)) cand.push_back(b);
+      std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) {
+        if ((x < kLowQubits) != (y < kLowQubits)) return y < kLowQubits;
+        const size_t nx = next_use(x), ny = next_use(y);
+        return nx != ny ? nx > ny : x > y;
+      });
+      cur_warp.assign(cand.begin(), cand.begin() + nwarp);
+    }
     std::vector<int> tb;
     for (int b = 0; b < L; ++b)
-      if (!((Rall >> b) & 1u)) tb.push_back(b);
+      if (!((Rall >> b) & 1u) &&
+          std::find(cur_warp.begin(), cur_warp.end(), b) == cur_warp.end())
+        tb.push_back(b);
     order_thread_bits(tb);
+    tb.insert(tb.end(), cur_warp.begin(), cur_warp.end());
     for (size_t k = 0; k < tb.size(); ++k) ph.thrpos[k] = tb[k];
     for (int v = 0; v < 16; ++v) {
       ph.thr_lo[v] = ph.thr_hi[v] = 0;
@@ -1555,8 +1600,9 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
     cur.push_back(po);
     d1bit.push_back(bit);
   };
-  for (const GateDesc* gp : pg) {
-    const GateDesc& g = *gp;
+  for (size_t gix = 0; gix < pg.size(); ++gix) {
+    gi = gix;
+    const GateDesc& g = *pg[gix];
     TileOp op;
     memset(&op, 0, sizeof(op));
     for (int c = 0; c < g.nc; ++c) {
@@ -1681,6 +1727,7 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
     e.phases.push_back(ph);
     e.fp64_ops_per_amp += 8.0;
   }
+  gi = pg.size();
   close(false);
   e.pd.nphases = (int)e.phases.size();
   if (const char* dbg = getenv("QSV_TILE_DEBUG")) e.pd.debug = atoi(dbg);

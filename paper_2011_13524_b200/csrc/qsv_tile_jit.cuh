@@ -360,7 +360,8 @@ struct Gen {
   // runs): the tile buffer is free once the amplitudes are in registers, so
   // the next tile streams in while this phase computes, and the results go
   // from registers straight to HBM (no shared-memory write-back).
-  void reg_phase(const TilePhase& P, const std::string& prefetch = std::string()) {
+  void reg_phase(const TilePhase& P, const std::string& prefetch = std::string(),
+                 bool warp_local_next = false) {
     std::vector<int> thr;
     for (int j = 0; j < L - R; ++j) thr.push_back(P.thrpos[j]);
     line("{ // register phase");
@@ -401,7 +402,9 @@ struct Gen {
     for (int j = 0; j < R2; ++j)
       line("sm[slt ^ " + std::to_string(cj[j]) + "u] = v[" + std::to_string(j) + "];");
     line("}");
-    line("group_sync(group);");
+    // the next register phase keeps this phase's warp bits: each warp reads
+    // back only what it wrote, so a warp barrier orders it
+    line(warp_local_next && G > 32 ? "__syncwarp();" : "group_sync(group);");
   }
 
   void smem_dense(const TileOp& op) {
@@ -609,9 +612,16 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
     o += "    if (group == 0 && first && tid == 0 && " + std::to_string(ph_idx) +
          " * QSV_GROUPS >= (*s_go + 1) * nph_total && *s_go < QSV_GROUPS - 1) *s_go = *s_go + 1;\n";
     const bool last = ph_idx == nph - 1;
+    // warp-local transition: the next phase is a register phase with the
+    // same (ordered) warp-index bit positions
+    bool wl = false;
+    if (!last && P.type == 0 && e.phases[ph_idx + 1].type == 0 && jit_warp_local()) {
+      wl = true;
+      for (int b = 5; b < tidbits; ++b) wl = wl && P.thrpos[b] == e.phases[ph_idx + 1].thrpos[b];
+    }
     if (P.type == 0 && last && direct)
       g.reg_phase(P, "const u64 nxt_ = s_next[group][it_ & 1u]; " + copy_of("nxt_"));
-    else if (P.type == 0) g.reg_phase(P);
+    else if (P.type == 0) g.reg_phase(P, std::string(), wl);
     else g.smem_phase(P);
     ++ph_idx;
   }
