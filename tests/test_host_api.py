@@ -201,3 +201,31 @@ def test_small_state_tile_size_choice():
         assert auto == per_l[expect_l], (n, auto, per_l)
     c = _core(workloads.generate_cz_ladder(24, 4, seed=1))
     assert c.plan_stats(use_tiles=1) == c.plan_stats(use_tiles=1, tile_qubits=12)
+
+
+def test_tile_set_search_pass_counts():
+    """The planner's tile-set search (multi-start + one pass of lookahead,
+    the fewer-pass plan kept; qsv_tile_impl.cuh select_pass / qsv_tile_select.cu)
+    packs the benchmark circuits into at most these many HBM sweeps (greedy:
+    cz-ladder(30) 22, VQE(24) 8)."""
+    for circ, most in ((workloads.generate_cz_ladder(30, 20, seed=1), 18),
+                       (workloads.generate_cz_ladder(28, 20, seed=1), 16),
+                       (workloads.vqe_ansatz(24), 5)):
+        st = _core(circ).plan_stats()
+        assert st["num_tile_passes"] <= most, st
+
+
+def test_parametric_replan_replays_the_same_plan():
+    """New angles keep the pass structure: the recorded pass selections are
+    replayed (structure-keyed cache) and give the plan a fresh search gives."""
+    import numpy as np
+    circ = workloads.vqe_ansatz(20)
+    first = _core(circ).plan_stats()
+    rng = np.random.default_rng(4)
+    for _ in range(3):
+        for k in range(circ.get_parameter_count()):
+            circ.set_parameter(k, float(rng.uniform(0, 2 * np.pi)))
+        again = _core(circ).plan_stats()
+        assert again["num_tile_passes"] == first["num_tile_passes"]
+        assert again["num_steps"] == first["num_steps"]
+        assert again["hbm_bytes"] == first["hbm_bytes"]
