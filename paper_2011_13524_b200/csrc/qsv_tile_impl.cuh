@@ -1258,6 +1258,16 @@ inline bool jit_warp_local() {
   return on != 0;
 }
 
+// QSV_JIT_NOHOIST=0: let the compiler hoist per-phase thread deposits out of
+// the tile loop (A/B)
+inline bool jit_nohoist() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_NOHOIST");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 inline int jit_stagger_max_phases() {
   static const int v = [] {
     const char* e = getenv("QSV_STAGGER_MAX_PHASES");

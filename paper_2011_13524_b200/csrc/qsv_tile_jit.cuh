@@ -365,7 +365,7 @@ struct Gen {
     std::vector<int> thr;
     for (int j = 0; j < L - R; ++j) thr.push_back(P.thrpos[j]);
     line("{ // register phase");
-    line("const uint32_t lt = " + deposit(thr, "tid") + ";");
+    line("const uint32_t lt = " + deposit(thr, "tidv") + ";");
     line("const uint32_t slt = swz(lt);");
     line("double2 v[" + std::to_string(R2) + "];");
     uint32_t srb[8];
@@ -525,6 +525,7 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
   std::string& o = g.o;
   o += jit_prelude();
   o += "#define QSV_G " + std::to_string(G) + "\n";
+  o += std::string("constexpr bool jit_nohoist = ") + (jit_nohoist() ? "true" : "false") + ";\n";
   o += "#define QSV_GROUPS " + std::to_string(kGroups) + "\n";
   o += "struct __align__(16) PassParams { double2* a; u64 ntiles; u64* ctr; int nostagger; "
        "int pad; FixedBits tb; double2 d[" + std::to_string(js.ndata) + "]; };\n";
@@ -601,6 +602,11 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
   o += R"JIT(  const int nph_total = )JIT" + std::to_string(std::max<size_t>(1, e.phases.size())) + R"JIT(;
   while (tile < P.ntiles) {
     if (tid == 0) s_next[group][it_ & 1u] = atomicAdd(P.ctr, 1ull);
+    // an opaque per-tile copy of tid: the phases' thread-bit deposits are
+    // recomputed in each tile (a few ALU ops) instead of being hoisted out of
+    // the tile loop, where dozens of them stay live and spill
+    uint32_t tidv = tid;
+    if (jit_nohoist) asm volatile("mov.u32 %0, %0;" : "+r"(tidv));
     const u64 base = widen(tile, P.tb);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     group_sync(group);
