@@ -67,7 +67,25 @@ struct Gen {
   std::string d(uint32_t idx) const {  // payload entry as an expression
     return "P.d[" + std::to_string(idx) + "]";
   }
-  const Cplx& val(uint32_t idx) const { return e.data[idx]; }
+  // What the generated text depends on besides the op / phase arrays: the
+  // class (0, 1, -1, other per real part) of every payload value the
+  // generator inspects, and the raw bytes of structural records (sign /
+  // factor / phase rules) stored in the payload.  Recorded so a later pass
+  // with the same arrays and the same recorded facts reuses the source
+  // (jit_pass_source) -- a VQE parameter update changes only other values.
+  mutable std::vector<std::pair<uint32_t, uint8_t>> sig_cls;
+  mutable std::vector<std::pair<uint32_t, uint32_t>> sig_raw;  // (first entry, entries)
+  static uint8_t cls1(double x) { return x == 0.0 ? 0 : x == 1.0 ? 1 : x == -1.0 ? 2 : 3; }
+  static uint8_t cls(const Cplx& c) { return (uint8_t)(cls1(c.re) | (cls1(c.im) << 2)); }
+  const Cplx& val(uint32_t idx) const {
+    sig_cls.push_back({idx, cls(e.data[idx])});
+    return e.data[idx];
+  }
+  template <typename T>
+  void rec(T* out, uint32_t idx, uint32_t structural_entries) const {
+    memcpy(out, &e.data[idx], sizeof(T));
+    sig_raw.push_back({idx, structural_entries});
+  }
 
   // ---- register ops ----------------------------------------------------
   // pairs (j, j | 1 << I) of slot I whose register-control part holds
@@ -147,7 +165,7 @@ struct Gen {
   void sign_rules(uint32_t D, int m, const char* bits) {
     for (int r = 0; r < m; ++r) {
       FlushSign S;
-      memcpy(&S, &e.data[D + 2 * r], sizeof(S));
+      rec(&S, D + 2 * r, 2);
       std::string cond;
       if (S.lm) cond += "(lt & " + hex32(S.lm) + ") == " + hex32(S.lv);
       if (S.gm) {
@@ -186,7 +204,7 @@ struct Gen {
         line("  double2 C_ = make_double2(1.0, 0.0);");
         for (int f = 0; f < op.slots; ++f) {
           FlushFactor F;
-          memcpy(&F, &e.data[fD + 3 * f], sizeof(F));
+          rec(&F, fD + 3 * f, 1);  // pos (the factors are read as P.d[...])
           const std::string bit =
               F.pos >= 0 ? "((lt >> " + std::to_string(F.pos) + ") & 1u)"
                          : "((base >> " + std::to_string(-F.pos - 1) + ") & 1ull)";
@@ -215,7 +233,7 @@ struct Gen {
       if ((op.slots >> i) & 1) line("  double2 ph" + std::to_string(i) + "_ = make_double2(1.0, 0.0);");
     for (int r = 0; r < op.m; ++r) {
       FlushPhase F;
-      memcpy(&F, &e.data[op.data + 3 * r], sizeof(F));
+      rec(&F, op.data + 3 * r, 2);  // masks and slot (f is read as P.d[...])
       std::string cond;
       if (F.lm) cond += "(lt & " + hex32(F.lm) + ") == " + hex32(F.lv);
       if (F.gm) {
@@ -511,7 +529,63 @@ __device__ __forceinline__ void st1(double2* p, double2 v) {
 )JIT";
 }
 
+inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::pair<uint32_t, uint8_t>>* scls,
+                                     std::vector<std::pair<uint32_t, uint32_t>>* sraw);
+
+// Generated source of a pass, reusing an earlier pass's text when the op /
+// phase arrays are identical and every payload fact the generator read
+// (value classes, structural record bytes) still holds.
+struct JitSrcEntry {
+  std::vector<std::pair<uint32_t, uint8_t>> cls;
+  std::vector<std::pair<uint32_t, uint32_t>> raw;
+  std::vector<Cplx> raw_bytes;  // the structural entries, concatenated
+  JitSource js;
+};
+inline std::mutex g_src_mu;
+inline std::unordered_map<std::string, std::vector<JitSrcEntry>> g_src_cache;
+
 inline JitSource jit_pass_source(const Encoded& e, int L) {
+  std::string key;
+  const int32_t hdr[3] = {L, kRegBits, (int32_t)e.data.size()};
+  key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+  key.append(reinterpret_cast<const char*>(&e.pd), sizeof(e.pd));
+  key.append(reinterpret_cast<const char*>(e.phases.data()), e.phases.size() * sizeof(TilePhase));
+  key.append(reinterpret_cast<const char*>(e.ops.data()), e.ops.size() * sizeof(TileOp));
+  static const bool enabled = [] {
+    const char* v = getenv("QSV_JIT_SRC_CACHE");
+    return !v || atoi(v) != 0;
+  }();
+  if (!enabled) return jit_pass_source_gen(e, L, nullptr, nullptr);
+  {
+    std::lock_guard<std::mutex> lk(g_src_mu);
+    auto it = g_src_cache.find(key);
+    if (it != g_src_cache.end())
+      for (const JitSrcEntry& en : it->second) {
+        bool same = true;
+        for (const auto& c : en.cls) same = same && jitgen::Gen::cls(e.data[c.first]) == c.second;
+        size_t at = 0;
+        for (const auto& r : en.raw) {
+          same = same && memcmp(&e.data[r.first], &en.raw_bytes[at], sizeof(Cplx) * r.second) == 0;
+          at += r.second;
+        }
+        if (same) return en.js;
+      }
+  }
+  JitSrcEntry en;
+  en.js = jit_pass_source_gen(e, L, &en.cls, &en.raw);
+  for (const auto& r : en.raw)
+    en.raw_bytes.insert(en.raw_bytes.end(), e.data.begin() + r.first,
+                        e.data.begin() + r.first + r.second);
+  JitSource js = en.js;
+  std::lock_guard<std::mutex> lk(g_src_mu);
+  if (g_src_cache.size() >= 512) g_src_cache.clear();
+  auto& v = g_src_cache[key];
+  if (v.size() < 8) v.push_back(std::move(en));
+  return js;
+}
+
+inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::pair<uint32_t, uint8_t>>* scls,
+                                     std::vector<std::pair<uint32_t, uint32_t>>* sraw) {
   using namespace jitgen;
   JitSource js;
   if (L < kRegBits + 1 || L > kMaxTileQubits) throw std::runtime_error("jit: tile size");
@@ -656,5 +730,7 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
 }
 )JIT";
   js.src = std::move(o);
+  if (scls) *scls = std::move(g.sig_cls);
+  if (sraw) *sraw = std::move(g.sig_raw);
   return js;
 }
