@@ -1268,6 +1268,25 @@ inline bool jit_nohoist() {
   return on != 0;
 }
 
+// QSV_JIT_DIRECT_LOAD=0: tiles always enter through cp.async copy-in (A/B)
+inline bool jit_direct_load() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_DIRECT_LOAD");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
+// QSV_JIT_DIRECT_ANY=0: direct stores only when the last phase's lanes hold
+// qubits 0..3 in order (fully coalesced), else through shared memory (A/B)
+inline bool jit_direct_any() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_DIRECT_ANY");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 inline int jit_stagger_max_phases() {
   static const int v = [] {
     const char* e = getenv("QSV_STAGGER_MAX_PHASES");

@@ -378,14 +378,39 @@ struct Gen {
   // runs): the tile buffer is free once the amplitudes are in registers, so
   // the next tile streams in while this phase computes, and the results go
   // from registers straight to HBM (no shared-memory write-back).
-  void reg_phase(const TilePhase& P, const std::string& prefetch = std::string(),
-                 bool warp_local_next = false) {
+  // global index of the thread's amplitudes in phase P: gl_ (thread bits)
+  // | h(j) (register slot bits), local bit b -> qubit spos[b]
+  std::string gl_decl(const TilePhase& P) const {
+    std::string gl = "const u64 gl_ = base";
+    for (int b = 0; b < L - R; ++b)
+      gl += " | ((u64)((tid >> " + std::to_string(b) + ") & 1u) << " +
+            std::to_string(e.pd.spos[P.thrpos[b]]) + ")";
+    return gl + ";";
+  }
+  uint64_t gl_slot(const TilePhase& P, int j) const {
+    uint64_t h = 0;
+    for (int i = 0; i < R; ++i)
+      if ((j >> i) & 1) h |= 1ULL << e.pd.spos[P.regpos[i]];
+    return h;
+  }
+
+  // One register phase.  load_global: the pass's first phase takes its
+  // amplitudes straight from HBM (no tile copy-in: cp.async writes shared
+  // memory at one wavefront per 32-byte sector, a quarter of a register
+  // store's rate, and the phase's own shared-memory read disappears too).
+  // store_global: the pass's last phase stores straight to HBM; `prefetch`
+  // then issues the next tile's copy-in once this phase's reads are done.
+  // The thread layouts keep qubits 0..3 on lane or register bits, so every
+  // warp's loads / stores cover whole 128-byte lines.
+  void reg_phase(const TilePhase& P, bool load_global, bool store_global,
+                 const std::string& prefetch, bool warp_local_next) {
     std::vector<int> thr;
     for (int j = 0; j < L - R; ++j) thr.push_back(P.thrpos[j]);
     line("{ // register phase");
     line("const uint32_t lt = " + deposit(thr, "tidv") + ";");
     line("const uint32_t slt = swz(lt);");
     line("double2 v[" + std::to_string(R2) + "];");
+    if (load_global || store_global) line(gl_decl(P));
     uint32_t srb[8];
     for (int i = 0; i < R; ++i) srb[i] = swz_host(1u << P.regpos[i]);
     std::vector<uint32_t> cj(R2);
@@ -394,26 +419,19 @@ struct Gen {
       for (int i = 0; i < R; ++i)
         if ((j >> i) & 1) ad ^= srb[i];
       cj[j] = ad;
-      line("v[" + std::to_string(j) + "] = sm[slt ^ " + std::to_string(ad) + "u];");
+      if (load_global)
+        line("v[" + std::to_string(j) + "] = ld1(a + (gl_ | " + hex64(gl_slot(P, j)) + "));");
+      else
+        line("v[" + std::to_string(j) + "] = sm[slt ^ " + std::to_string(ad) + "u];");
     }
-    if (!prefetch.empty()) {
+    if (store_global && !load_global && !prefetch.empty()) {
       line("group_sync(group);");
       line(prefetch);
     }
     for (int o = P.op_begin; o < P.op_end; ++o) reg_op(e.ops[o]);
-    if (!prefetch.empty()) {
-      // global index of local index l: bit b of l -> qubit spos[b]
-      std::string gl = "const u64 gl_ = base";
-      for (int b = 0; b < L - R; ++b)
-        gl += " | ((u64)((tid >> " + std::to_string(b) + ") & 1u) << " +
-              std::to_string(e.pd.spos[P.thrpos[b]]) + ")";
-      line(gl + ";");
-      for (int j = 0; j < R2; ++j) {
-        uint64_t h = 0;
-        for (int i = 0; i < R; ++i)
-          if ((j >> i) & 1) h |= 1ULL << e.pd.spos[P.regpos[i]];
-        line("st1(a + (gl_ | " + hex64(h) + "), v[" + std::to_string(j) + "]);");
-      }
+    if (store_global) {
+      for (int j = 0; j < R2; ++j)
+        line("st1(a + (gl_ | " + hex64(gl_slot(P, j)) + "), v[" + std::to_string(j) + "]);");
       line("}");
       return;
     }
@@ -522,6 +540,11 @@ __device__ __forceinline__ double2 negs(double2 v, int s) {
 __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ double2 ld1(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
 }
 __device__ __forceinline__ void st1(double2* p, double2 v) {
   asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
@@ -664,7 +687,18 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   // local bits 0..3 (QSV_JIT_DIRECT_STORE=0 disables, A/B)
   const TilePhase* lastp = e.phases.empty() ? nullptr : &e.phases.back();
   bool direct = lastp && lastp->type == 0 && L - kRegBits >= 4 && jit_direct_store();
-  for (int b = 0; direct && b < 4; ++b) direct = lastp->thrpos[b] == b;
+  if (direct && jit_direct_any()) {
+    // qubits 0..3 on lane or register bits (never warp bits, by the
+    // encoder's warp-bit choice): each warp's stores cover whole lines
+    for (int b = 0; direct && b < kLowQubits; ++b) {
+      bool ok = false;
+      for (int j = 0; j < 5 && j < L - kRegBits; ++j) ok = ok || lastp->thrpos[j] == b;
+      for (int i = 0; i < kRegBits; ++i) ok = ok || lastp->regpos[i] == b;
+      direct = ok;
+    }
+  } else {
+    for (int b = 0; direct && b < 4; ++b) direct = lastp->thrpos[b] == b;
+  }
   // the next tile is prefetched as soon as this tile's buffer is free
   o += R"JIT(
   if (tid == 0) s_next[group][0] = atomicAdd(P.ctr, 1ull);
@@ -672,7 +706,9 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   u64 tile = s_next[group][0];
   uint32_t it_ = 1;
 )JIT";
-  o += "  " + copy_of("tile") + "\n";
+  // first phase straight from HBM (no copy-in, no prefetch)
+  const bool direct_load = jit_direct_load() && !e.phases.empty() && e.phases[0].type == 0;
+  if (!direct_load) o += "  " + copy_of("tile") + "\n";
   o += R"JIT(  const int nph_total = )JIT" + std::to_string(std::max<size_t>(1, e.phases.size())) + R"JIT(;
   while (tile < P.ntiles) {
     if (tid == 0) s_next[group][it_ & 1u] = atomicAdd(P.ctr, 1ull);
@@ -699,9 +735,13 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
       wl = true;
       for (int b = 5; b < tidbits; ++b) wl = wl && P.thrpos[b] == e.phases[ph_idx + 1].thrpos[b];
     }
+    const bool first_ph = ph_idx == 0;
     if (P.type == 0 && last && direct)
-      g.reg_phase(P, "const u64 nxt_ = s_next[group][it_ & 1u]; " + copy_of("nxt_"));
-    else if (P.type == 0) g.reg_phase(P, std::string(), wl);
+      g.reg_phase(P, first_ph && direct_load, true,
+                  direct_load ? std::string()
+                              : "const u64 nxt_ = s_next[group][it_ & 1u]; " + copy_of("nxt_"),
+                  false);
+    else if (P.type == 0) g.reg_phase(P, first_ph && direct_load, false, std::string(), wl);
     else g.smem_phase(P);
     ++ph_idx;
   }
@@ -714,7 +754,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
     for (int k = 0; k < kRegs; ++k)
       o += "      st1(a + (gb | " + hex64(hi[k]) + "), sm[" + std::to_string(sk[k]) + "u ^ st]);\n";
     o += "    }\n    group_sync(group);\n";
-    o += "    " + copy_of("s_next[group][it_ & 1u]") + "\n";
+    if (!direct_load) o += "    " + copy_of("s_next[group][it_ & 1u]") + "\n";
   }
   o += R"JIT(    if (group == 0 && first && tid == 0) *s_go = QSV_GROUPS;
     first = false;
