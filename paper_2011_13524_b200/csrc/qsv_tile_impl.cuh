@@ -1277,12 +1277,13 @@ inline bool jit_direct_load() {
   return on != 0;
 }
 
-// QSV_JIT_DIRECT_ANY=0: direct stores only when the last phase's lanes hold
-// qubits 0..3 in order (fully coalesced), else through shared memory (A/B)
+// QSV_JIT_DIRECT_ANY=1: direct stores whenever qubits 0..3 sit on lane or
+// register bits; default: only when the last phase's lanes hold them in order
+// (fully coalesced; measured 1-2% faster on cz-ladder, equal on cnot-ring)
 inline bool jit_direct_any() {
   static const int on = [] {
     const char* e = getenv("QSV_JIT_DIRECT_ANY");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   return on != 0;
 }
