@@ -107,9 +107,11 @@ bool ej_pack(int n, const std::vector<uint64_t>& xms, const std::vector<uint64_t
              std::vector<EjPass>& passes) {
   if (n < kEjTileQubits) return false;
   const uint64_t low = 0xFULL;
+  // units: (flip mask, <= kEjMaxTerms of its terms); flip-free terms (Z
+  // products) fit any tile and are dealt out afterwards to balance the passes
   std::vector<uint64_t> masks;
   for (uint64_t m : xms)
-    if (std::find(masks.begin(), masks.end(), m) == masks.end()) masks.push_back(m);
+    if (m && std::find(masks.begin(), masks.end(), m) == masks.end()) masks.push_back(m);
   struct Unit {
     uint64_t xm;
     std::vector<int> terms;
@@ -128,22 +130,48 @@ bool ej_pack(int n, const std::vector<uint64_t>& xms, const std::vector<uint64_t
     }
     if (!u.terms.empty()) units.push_back(u);
   }
+  std::vector<int> diag;
+  for (size_t t = 0; t < xms.size(); ++t)
+    if (!xms[t]) diag.push_back((int)t);
+  // 1. flip units first-fit into tile sets of 12 qubits
+  struct Sel {
+    uint64_t S;
+    std::vector<int> members;  // unit indices
+    std::vector<int> dterms;   // flip-free terms dealt to this pass
+    int nterms;
+  };
+  std::vector<Sel> sel;
   std::vector<char> done(units.size(), 0);
   size_t left = units.size();
   while (left) {
-    uint64_t S = low;
-    int nterms = 0;
-    std::vector<int> members;
+    Sel P{low, {}, {}, 0};
     for (size_t i = 0; i < units.size(); ++i) {
       if (done[i]) continue;
-      if (__builtin_popcountll(S | units[i].xm) > kEjTileQubits) continue;
-      if (nterms + (int)units[i].terms.size() > kEjMaxTerms) continue;
-      S |= units[i].xm;
-      nterms += (int)units[i].terms.size();
+      if (__builtin_popcountll(P.S | units[i].xm) > kEjTileQubits) continue;
+      if (P.nterms + (int)units[i].terms.size() > kEjMaxTerms) continue;
+      P.S |= units[i].xm;
+      P.nterms += (int)units[i].terms.size();
       done[i] = 1;
       --left;
-      members.push_back((int)i);
+      P.members.push_back((int)i);
     }
+    sel.push_back(std::move(P));
+  }
+  // 2. flip-free terms to the passes with the fewest terms (registers: one
+  // accumulator per term), new passes only when every pass is full
+  for (int t : diag) {
+    Sel* best = nullptr;
+    for (Sel& P : sel)
+      if (P.nterms < kEjMaxTerms && (!best || P.nterms < best->nterms)) best = &P;
+    if (!best) {
+      sel.push_back(Sel{low, {}, {}, 0});
+      best = &sel.back();
+    }
+    best->dterms.push_back(t);
+    ++best->nterms;
+  }
+  for (Sel& Q : sel) {
+    uint64_t S = Q.S;
     // local layout: qubits 0..3 on bits 0..3; flip qubits on the slot bits
     // 8..11 first (most-used first), then bit 4, then the warp bits 5..7;
     // the lowest unused qubits fill what is left
@@ -151,7 +179,7 @@ bool ej_pack(int n, const std::vector<uint64_t>& xms, const std::vector<uint64_t
     for (int q = 4; q < n; ++q) {
       if (!((S >> q) & 1ULL)) continue;
       int cnt = 0;
-      for (int i : members) cnt += (int)((units[i].xm >> q) & 1ULL);
+      for (int i : Q.members) cnt += (int)((units[i].xm >> q) & 1ULL);
       use.push_back({-cnt, q});
     }
     std::sort(use.begin(), use.end());
@@ -168,11 +196,11 @@ bool ej_pack(int n, const std::vector<uint64_t>& xms, const std::vector<uint64_t
     int local_of[64];
     for (int q = 0; q < 64; ++q) local_of[q] = -1;
     for (int j = 0; j < kEjTileQubits; ++j) local_of[P.spos[j]] = j;
-    for (int i : members) {
+    auto add_terms = [&](uint64_t xm, const std::vector<int>& ts) {
       EjGroup* G = nullptr;
       uint32_t xl = 0;
       for (int q = 0; q < n; ++q)
-        if ((units[i].xm >> q) & 1ULL) xl |= 1u << local_of[q];
+        if ((xm >> q) & 1ULL) xl |= 1u << local_of[q];
       for (EjGroup& g : P.groups)
         if (g.xl == xl) G = &g;
       if (!G) {
@@ -180,7 +208,7 @@ bool ej_pack(int n, const std::vector<uint64_t>& xms, const std::vector<uint64_t
         G = &P.groups.back();
         G->xl = xl;
       }
-      for (int t : units[i].terms) {
+      for (int t : ts) {
         EjTerm T{t, 0, 0, false};
         for (int q = 0; q < n; ++q)
           if ((zms[t] >> q) & 1ULL) {
@@ -191,7 +219,9 @@ bool ej_pack(int n, const std::vector<uint64_t>& xms, const std::vector<uint64_t
         G->terms.push_back(T);
         ++P.nterms;
       }
-    }
+    };
+    if (!Q.dterms.empty()) add_terms(0, Q.dterms);
+    for (int i : Q.members) add_terms(units[i].xm, units[i].terms);
     passes.push_back(std::move(P));
   }
   return true;
@@ -219,6 +249,15 @@ void emit_wht(EjGen& g, const std::string& base, int m) {
 
 // QSV_EXPECT_BULK=1: tiles move with cp.async.bulk + mbarrier (A/B; the
 // source differs, so the two variants are cached separately)
+// QSV_EXPECT_REGLOAD=0: tiles always enter through cp.async (A/B)
+bool ej_regload() {
+  static const int on = [] {
+    const char* e = getenv("QSV_EXPECT_REGLOAD");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 bool ej_bulk() {
   static const int on = [] {
     const char* e = getenv("QSV_EXPECT_BULK");
@@ -284,7 +323,45 @@ struct XParams { const double2* a; u64 ntiles; double* partials; FixedBits tb; }
     }
   }
   for (int t = 0; t < nt; ++t) g.line("  double acc" + I(t) + " = 0.0;");
-  if (ej_bulk()) {
+  // register staging: each thread loads its 16 amplitudes of the next tile
+  // into registers while the current one is evaluated (64 more registers,
+  // so only for passes with at most 24 accumulators), and stores the tile to
+  // shared memory itself only when a group needs partner amplitudes from
+  // other threads -- a 128-bit register store costs a quarter of the
+  // shared-memory wavefronts of the cp.async copy-in (one per 32-byte sector)
+  bool need_smem = false;
+  for (const EjGroup& G : P.groups) need_smem = need_smem || (G.xl & 0xffu) != 0;
+  const bool regload = ej_regload() && !ej_bulk() && P.nterms <= 24;
+  if (regload) {
+    g.line("  u64 tile = blockIdx.x;");
+    g.line("  int buf = 0;");
+    g.line("  double2 nx[16];");
+    g.line("  if (tile < P.ntiles) {");
+    g.line("    const u64 gb = widen(tile, P.tb) | lo;");
+    for (int k = 0; k < 16; ++k)
+      g.line("    nx[" + I(k) + "] = __ldg(P.a + (gb | " + hex64(hi[k]) + "));");
+    g.line("  }");
+    g.line("  for (; tile < P.ntiles; tile += gridDim.x, buf ^= 1) {");
+    g.line("    double2 v[16];");
+    g.line("#pragma unroll");
+    g.line("    for (int k = 0; k < 16; ++k) v[k] = nx[k];");
+    g.line("    const u64 nxt = tile + gridDim.x;");
+    g.line("    if (nxt < P.ntiles) {");
+    g.line("      const u64 gb = widen(nxt, P.tb) | lo;");
+    for (int k = 0; k < 16; ++k)
+      g.line("      nx[" + I(k) + "] = __ldg(P.a + (gb | " + hex64(hi[k]) + "));");
+    g.line("    }");
+    g.line("    double2* smw = sbuf + (buf << 12);");
+    if (need_smem) {
+      g.line("#pragma unroll");
+      g.line("    for (int k = 0; k < 16; ++k) smw[(k << 8) + tid] = v[k];");
+      g.line("    __syncthreads();");
+    }
+    g.line("    const double2* sm = smw;");
+    g.line("    (void)sm;");
+    g.line("    const u64 base = widen(tile, P.tb);");
+    g.line("    (void)base;");
+  } else if (ej_bulk()) {
     // Blackwell bulk copies: each thread moves one 256-byte run (16
     // amplitudes of qubits 0..3) with cp.async.bulk, completion counted by
     // an mbarrier per buffer (tx bytes), instead of 16 cp.async of 16 bytes
@@ -356,6 +433,7 @@ struct XParams { const double2* a; u64 ntiles; double* partials; FixedBits tb; }
   g.line(R"JIT(      asm volatile("cp.async.commit_group;" ::: "memory");
     })JIT");
   }
+  if (!regload)
   g.line(R"JIT(    const double2* sm = sbuf + (buf << 12);
     const u64 base = widen(tile, P.tb);
     (void)base;
