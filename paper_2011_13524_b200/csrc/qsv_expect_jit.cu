@@ -249,11 +249,12 @@ void emit_wht(EjGen& g, const std::string& base, int m) {
 
 // QSV_EXPECT_BULK=1: tiles move with cp.async.bulk + mbarrier (A/B; the
 // source differs, so the two variants are cached separately)
-// QSV_EXPECT_REGLOAD=0: tiles always enter through cp.async (A/B)
+// QSV_EXPECT_REGLOAD=1: register-staged tile loads (A/B; measured slower:
+// TFIM n=28 2.75 -> 3.10 ms, profiles/r2_expect_bulk_ab.md), default cp.async
 bool ej_regload() {
   static const int on = [] {
     const char* e = getenv("QSV_EXPECT_REGLOAD");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   return on != 0;
 }
