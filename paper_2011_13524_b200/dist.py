@@ -35,6 +35,7 @@ gloo tests plug the oracle in (tests/test_dist_gloo.py).
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import math
 
@@ -224,6 +225,22 @@ def records_to_ops(records):
             op.control_qubits[j] = q
             op.control_values[j] = v
     return ops, keep
+
+
+# libqsv NCCL communicators by (process group, ranks, rank, device)
+_COMMS: dict = {}
+
+
+def _release_comms():
+    for h in _COMMS.values():
+        try:
+            lib.qsv_comm_destroy(h)
+        except Exception:  # noqa: BLE001  (interpreter teardown: best effort)
+            pass
+    _COMMS.clear()
+
+
+atexit.register(_release_comms)
 
 
 # --------------------------------------------------------------------- backends
@@ -547,6 +564,13 @@ class ShardedQuantumState:
                                    "distinct GPUs and a loadable libnccl.so.2")
             return None
         me = self.dist.get_rank(self.group)
+        # one communicator per (process group, device) for the process's
+        # lifetime: sharded states are constructed collectively, so every rank
+        # takes the same hit / miss here
+        key = (id(self.group), procs, me, dev)
+        h = _COMMS.get(key)
+        if h is not None:
+            return h
         uid = C.create_string_buffer(128)
         if me == 0:
             check(lib.qsv_comm_unique_id(uid))
@@ -556,6 +580,7 @@ class ShardedQuantumState:
         h = C.c_void_p()
         check(lib.qsv_comm_create(C.create_string_buffer(box[0], 128), procs, me, dev,
                                   C.byref(h)))
+        _COMMS[key] = h
         return h
 
     def close(self):
@@ -569,10 +594,9 @@ class ShardedQuantumState:
         self._drop_comm()
 
     def _drop_comm(self):
-        h = getattr(self, "_qcomm", None)
-        if h is not None:
-            self._qcomm = None
-            lib.qsv_comm_destroy(h)
+        # the communicator is shared by the process's sharded states and
+        # released at exit (_release_comms)
+        self._qcomm = None
 
     def _unmap(self):
         for ptr in self._peer_ptr.values():
