@@ -1298,6 +1298,16 @@ inline int jit_experiment() {
   return v;
 }
 
+// QSV_JIT_PARTIAL_BARRIERS=0: transitions that keep some warp positions still
+// synchronise the whole group (A/B)
+inline bool jit_partial_barriers() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_PARTIAL_BARRIERS");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 inline int jit_stagger_max_phases() {
   static const int v = [] {
     const char* e = getenv("QSV_STAGGER_MAX_PHASES");
@@ -1521,20 +1531,27 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
     // when they must change, the new warp bits are the non-register bits
     // whose next 1-qubit use lies furthest ahead (they stay warp bits longest)
     const int nwarp = std::max(0, (L - kRegBits) - 5);
-    bool keep = (int)cur_warp.size() == nwarp;
-    for (int b : cur_warp) keep = keep && !((Rall >> b) & 1u);
-    if (!keep) {
-      // local bits 0..3 (qubits 0..3, the 256-byte HBM runs) stay lane bits
-      // where possible: the direct store of a pass's last phase needs them
+    if ((int)cur_warp.size() != nwarp) cur_warp.assign(nwarp, -1);
+    // Only the warp positions whose bit became a register bit change, the
+    // others keep their bit at the same index: a transition then moves data
+    // only among the warps that differ in the changed positions, and the
+    // generated kernel synchronises just those (named barrier per subset).
+    // Replacements: local bits 0..3 (the 256-byte HBM runs) stay lane bits
+    // where possible (the direct loads / stores need them), then the bit
+    // whose next 1-qubit use lies furthest ahead.
+    {
       std::vector<int> cand;
       for (int b = 0; b < L; ++b)
-        if (!((Rall >> b) & 1u)) cand.push_back(b);
+        if (!((Rall >> b) & 1u) && std::find(cur_warp.begin(), cur_warp.end(), b) == cur_warp.end())
+          cand.push_back(b);
       std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) {
         if ((x < kLowQubits) != (y < kLowQubits)) return y < kLowQubits;
         const size_t nx = next_use(x), ny = next_use(y);
         return nx != ny ? nx > ny : x > y;
       });
-      cur_warp.assign(cand.begin(), cand.begin() + nwarp);
+      size_t ci = 0;
+      for (int& w : cur_warp)
+        if (w < 0 || ((Rall >> w) & 1u)) w = cand[ci++];
     }
     std::vector<int> tb;
     for (int b = 0; b < L; ++b)

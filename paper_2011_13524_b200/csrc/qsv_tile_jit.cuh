@@ -403,7 +403,8 @@ struct Gen {
   // The thread layouts keep qubits 0..3 on lane or register bits, so every
   // warp's loads / stores cover whole 128-byte lines.
   void reg_phase(const TilePhase& P, bool load_global, bool store_global,
-                 const std::string& prefetch, bool warp_local_next) {
+                 const std::string& prefetch, bool warp_local_next,
+                 const std::string& next_sync = std::string()) {
     std::vector<int> thr;
     for (int j = 0; j < L - R; ++j) thr.push_back(P.thrpos[j]);
     line("{ // register phase");
@@ -450,8 +451,9 @@ struct Gen {
     // back only what it wrote, so a warp barrier orders it
     // (QSV_JIT_EXPERIMENT=1: every transition a warp barrier -- wrong results,
     // a timing bound of the group barriers)
-    line((warp_local_next || jit_experiment() == 1) && G > 32 ? "__syncwarp();"
-                                                                : "group_sync(group);");
+    if ((warp_local_next || jit_experiment() == 1) && G > 32) line("__syncwarp();");
+    else if (!next_sync.empty()) line(next_sync);
+    else line("group_sync(group);");
   }
 
   void smem_dense(const TileOp& op) {
@@ -740,11 +742,26 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
          " * QSV_GROUPS >= (*s_go + 1) * nph_total && *s_go < QSV_GROUPS - 1) *s_go = *s_go + 1;\n";
     const bool last = ph_idx == nph - 1;
     // warp-local transition: the next phase is a register phase with the
-    // same (ordered) warp-index bit positions
+    // same (ordered) warp-index bit positions; a partial one (some positions
+    // kept) synchronises only the warps that trade data: those equal in the
+    // kept positions, with one named barrier per such subset
     bool wl = false;
+    std::string psync;
     if (!last && P.type == 0 && e.phases[ph_idx + 1].type == 0 && jit_warp_local()) {
-      wl = true;
-      for (int b = 5; b < tidbits; ++b) wl = wl && P.thrpos[b] == e.phases[ph_idx + 1].thrpos[b];
+      const TilePhase& Q = e.phases[ph_idx + 1];
+      std::vector<int> kept, changed;
+      for (int b = 5; b < tidbits; ++b) (P.thrpos[b] == Q.thrpos[b] ? kept : changed).push_back(b - 5);
+      wl = changed.empty();
+      const int nsub = 1 << kept.size();              // subsets per group
+      const int ids = 3 + kGroups * nsub;             // named barriers 3.. (0: CTA, 1..2: groups)
+      if (!wl && !kept.empty() && ids <= 16 && jit_partial_barriers()) {
+        std::string sub = "0u";
+        for (size_t k = 0; k < kept.size(); ++k)
+          sub += " | (((tid >> " + std::to_string(5 + kept[k]) + ") & 1u) << " + std::to_string(k) + ")";
+        psync = "asm volatile(\"bar.sync %0, %1;\" ::\"r\"(3u + (uint32_t)group * " +
+                std::to_string(nsub) + "u + (" + sub + ")), \"n\"(" +
+                std::to_string(32 << changed.size()) + ") : \"memory\");";
+      }
     }
     const bool first_ph = ph_idx == 0;
     if (P.type == 0 && last && direct)
@@ -752,7 +769,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
                   direct_load ? std::string()
                               : "const u64 nxt_ = s_next[group][it_ & 1u]; " + copy_of("nxt_"),
                   false);
-    else if (P.type == 0) g.reg_phase(P, first_ph && direct_load, false, std::string(), wl);
+    else if (P.type == 0) g.reg_phase(P, first_ph && direct_load, false, std::string(), wl, psync);
     else g.smem_phase(P);
     ++ph_idx;
   }
