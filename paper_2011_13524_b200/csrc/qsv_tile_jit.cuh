@@ -736,6 +736,24 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
 )JIT";
   int ph_idx = 0;
   const int nph = (int)e.phases.size();
+  // the most frequent kept-warp-position pattern among partial transitions
+  uint32_t part_pattern = 0;
+  {
+    std::map<uint32_t, int> freq;
+    for (int i = 0; i + 1 < nph; ++i) {
+      const TilePhase &A = e.phases[i], &B = e.phases[i + 1];
+      if (A.type != 0 || B.type != 0) continue;
+      uint32_t km = 0, all = 0;
+      for (int b = 5; b < tidbits; ++b) {
+        all |= 1u << (b - 5);
+        if (A.thrpos[b] == B.thrpos[b]) km |= 1u << (b - 5);
+      }
+      if (km && km != all) ++freq[km];
+    }
+    int best = 0;
+    for (auto& kv : freq)
+      if (kv.second > best) best = kv.second, part_pattern = kv.first;
+  }
   for (const TilePhase& P : e.phases) {
     // release group k once group 0 is k / kGroups of the way through its first tile
     o += "    if (group == 0 && first && tid == 0 && " + std::to_string(ph_idx) +
@@ -750,11 +768,19 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
     if (!last && P.type == 0 && e.phases[ph_idx + 1].type == 0 && jit_warp_local()) {
       const TilePhase& Q = e.phases[ph_idx + 1];
       std::vector<int> kept, changed;
-      for (int b = 5; b < tidbits; ++b) (P.thrpos[b] == Q.thrpos[b] ? kept : changed).push_back(b - 5);
+      uint32_t kmask = 0;
+      for (int b = 5; b < tidbits; ++b) {
+        (P.thrpos[b] == Q.thrpos[b] ? kept : changed).push_back(b - 5);
+        if (P.thrpos[b] == Q.thrpos[b]) kmask |= 1u << (b - 5);
+      }
       wl = changed.empty();
       const int nsub = 1 << kept.size();              // subsets per group
       const int ids = 3 + kGroups * nsub;             // named barriers 3.. (0: CTA, 1..2: groups)
-      if (!wl && !kept.empty() && ids <= 16 && jit_partial_barriers()) {
+      // one kept pattern per pass (the most frequent): its subsets are fixed
+      // sets of warps, so each named barrier id is always used by the same
+      // warps with the same count (two patterns would alias ids between warps
+      // that drift apart)
+      if (!wl && !kept.empty() && ids <= 16 && jit_partial_barriers() && kmask == part_pattern) {
         std::string sub = "0u";
         for (size_t k = 0; k < kept.size(); ++k)
           sub += " | (((tid >> " + std::to_string(5 + kept[k]) + ") & 1u) << " + std::to_string(k) + ")";
