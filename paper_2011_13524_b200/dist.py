@@ -254,6 +254,12 @@ class CudaShard:
         if stream_ptr is not None:
             self.state.set_stream(stream_ptr)
         plan.setdefault("use_graph", 0)
+        # shard programs are built per segment and run once: compile their
+        # generated pass kernels at creation (jit=2; the in-process and disk
+        # caches serve every later segment / step with the same structure)
+        # instead of the default "from the second run", which a run-once
+        # program never reaches
+        plan.setdefault("jit", 2)
         self._plan = default_plan_opts(**plan)
 
     def set_zero(self, one: bool):
