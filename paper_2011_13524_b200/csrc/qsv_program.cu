@@ -137,6 +137,19 @@ bool jit_all_cached(const qsv_program* p) {
   return any;
 }
 
+// every pass's structure was planned before in this process (a parametric
+// circuit recompiled with new angles, a shard segment seen before): worth
+// compiling at creation even for a program that will run only once
+bool jit_all_seen(const qsv_program* p) {
+  bool any = false;
+  for (const TilePlan& tp : p->tiles)
+    if (!tp.jit_src.empty()) {
+      any = true;
+      if (!tp.jit_seen) return false;
+    }
+  return any;
+}
+
 void drop_graph(qsv_program* p) {
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
   if (p->graph) cudaGraphDestroy(p->graph);
@@ -270,9 +283,10 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
     return rc;
   }
   p->device = dev;
-  // jit 2: compile now; jit 1: now only if every pass is already loaded
+  // jit 2: compile now; jit 1: now only if every pass is already loaded or
+  // its structure was planned before (a parametric recompile, a repeated segment)
   // (structure seen before, e.g. a VQE recompile with new angles)
-  if (o.jit == 2 || (o.jit == 1 && jit_all_cached(p))) {
+  if (o.jit == 2 || (o.jit == 1 && (jit_all_cached(p) || jit_all_seen(p)))) {
     rc = jit_prepare(p);
     if (rc) {
       qsv_program_destroy(p);

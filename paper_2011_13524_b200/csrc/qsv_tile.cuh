@@ -116,6 +116,7 @@ struct TilePlan {
   // launch shape, payload passed as the kernel parameter; `jit.kernel` is
   // set once compiled (until then the interpreter k_tile runs the pass)
   std::string jit_src;
+  bool jit_seen = false;  // the same pass structure was planned before in this process
   int jit_threads = 0;
   size_t jit_smem = 0;
   std::vector<Cplx> jit_data;

@@ -1819,6 +1819,22 @@ bool euler_real(const M2& U, Cplx a[2], Cplx b[2], double R[4]) {
     if (!(mag(U11) > eps)) return false;
     a1 = cm(ph(U11), cconj(b1));
   }
+  // phases up to sign, canonical (real part > 0, or = 0 with imaginary part
+  // > 0): the sign goes into the real matrix R instead, so a real U (e.g. an
+  // RY whose cosine turns negative) keeps unit phases and the pass structure
+  // (which factors are exactly 1) does not flip with the angle's sign --
+  // generated pass kernels stay cached across parameter updates
+  // (also snapped to exact +-1 / +-i within a few ulps: whether a factor is
+  // exactly 1 must not depend on rounding either)
+  auto canon = [](Cplx z) {
+    constexpr double tol = 1e-15;
+    if (std::fabs(z.im) <= tol && std::fabs(std::fabs(z.re) - 1.0) <= tol) z = {z.re < 0 ? -1.0 : 1.0, 0.0};
+    else if (std::fabs(z.re) <= tol && std::fabs(std::fabs(z.im) - 1.0) <= tol) z = {0.0, z.im < 0 ? -1.0 : 1.0};
+    return (z.re < 0 || (z.re == 0 && z.im < 0)) ? Cplx{-z.re, -z.im} : z;
+  };
+  a0 = canon(a0);
+  a1 = canon(a1);
+  b1 = canon(b1);
   const Cplx A[2] = {a0, a1}, B[2] = {{1, 0}, b1};
   for (int i = 0; i < 2; ++i)
     for (int j = 0; j < 2; ++j) {
@@ -2211,6 +2227,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
                         kJitMaxParamBytes) {
       try {
         JitSource js = jit_pass_source(e, L);
+        tp.jit_seen = js.seen;
         tp.jit_src = std::move(js.src);
         tp.jit_threads = js.threads;
         tp.jit_smem = js.smem;

@@ -23,6 +23,7 @@ struct JitSource {
   int group_threads = 0;
   size_t smem = 0;      // dynamic shared memory
   int ndata = 0;        // double2 entries of the payload parameter
+  bool seen = false;    // served from the source cache: this structure was planned before
 };
 
 namespace jitgen {
@@ -604,7 +605,11 @@ inline JitSource jit_pass_source(const Encoded& e, int L) {
           same = same && memcmp(&e.data[r.first], &en.raw_bytes[at], sizeof(Cplx) * r.second) == 0;
           at += r.second;
         }
-        if (same) return en.js;
+        if (same) {
+          JitSource js = en.js;
+          js.seen = true;
+          return js;
+        }
       }
   }
   JitSrcEntry en;
