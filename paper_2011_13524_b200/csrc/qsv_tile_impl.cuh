@@ -1288,16 +1288,6 @@ inline bool jit_direct_any() {
   return on != 0;
 }
 
-// QSV_JIT_EXPERIMENT (timing experiments only, results are wrong): 1 all
-// phase transitions with warp barriers, 2 transitions without shared memory
-inline int jit_experiment() {
-  static const int v = [] {
-    const char* e = getenv("QSV_JIT_EXPERIMENT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 // QSV_JIT_PARTIAL_BARRIERS=0: transitions that keep some warp positions still
 // synchronise the whole group (A/B)
 inline bool jit_partial_barriers() {

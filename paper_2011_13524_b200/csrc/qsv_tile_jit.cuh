@@ -423,9 +423,6 @@ struct Gen {
       cj[j] = ad;
       if (load_global)
         line("v[" + std::to_string(j) + "] = ld1(a + (gl_ | " + hex64(gl_slot(P, j)) + "));");
-      else if (jit_experiment() == 2)  // timing bound only: transitions without shared memory
-        line("v[" + std::to_string(j) + "] = make_double2(__int_as_float(lt) + " + std::to_string(j) +
-             ".0, 1.0);");
       else
         line("v[" + std::to_string(j) + "] = sm[slt ^ " + std::to_string(ad) + "u];");
     }
@@ -440,19 +437,12 @@ struct Gen {
       line("}");
       return;
     }
-    for (int j = 0; j < R2; ++j) {
-      if (jit_experiment() == 2)  // timing bound only: keep the value live without a store
-        line("if (__double_as_longlong(v[" + std::to_string(j) + "].x) == 0x7ff0deadll) sm[0] = v[" +
-             std::to_string(j) + "];");
-      else
-        line("sm[slt ^ " + std::to_string(cj[j]) + "u] = v[" + std::to_string(j) + "];");
-    }
+    for (int j = 0; j < R2; ++j)
+      line("sm[slt ^ " + std::to_string(cj[j]) + "u] = v[" + std::to_string(j) + "];");
     line("}");
     // the next register phase keeps this phase's warp bits: each warp reads
     // back only what it wrote, so a warp barrier orders it
-    // (QSV_JIT_EXPERIMENT=1: every transition a warp barrier -- wrong results,
-    // a timing bound of the group barriers)
-    if ((warp_local_next || jit_experiment() == 1) && G > 32) line("__syncwarp();");
+    if (warp_local_next && G > 32) line("__syncwarp();");
     else if (!next_sync.empty()) line(next_sync);
     else line("group_sync(group);");
   }
