@@ -1298,6 +1298,16 @@ inline bool jit_partial_barriers() {
   return on != 0;
 }
 
+// QSV_JIT_SHUFFLE=0: warp-local phase transitions go through shared memory
+// (A/B); on: lane <-> register bit swaps with warp shuffles
+inline bool jit_shuffle_transitions() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_SHUFFLE");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 inline int jit_stagger_max_phases() {
   static const int v = [] {
     const char* e = getenv("QSV_STAGGER_MAX_PHASES");
@@ -1483,6 +1493,7 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
     return it == uses[b].end() ? (size_t)-1 : *it;
   };
   std::vector<int> cur_warp;  // warp-index bit positions of the last register phase
+  std::vector<int> prev_warp, prev_lanes;  // the last register phase's warp / lane bits
   // current register phase: ops collected with their own data, scheduled at close
   bool open = false;
   uint32_t R = 0;
@@ -1548,7 +1559,31 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
       if (!((Rall >> b) & 1u) &&
           std::find(cur_warp.begin(), cur_warp.end(), b) == cur_warp.end())
         tb.push_back(b);
-    order_thread_bits(tb);
+    const int nlane = std::min<int>(5, (int)tb.size());
+    if (jit_shuffle_transitions() && cur_warp == prev_warp && (int)prev_lanes.size() == nlane &&
+        nlane == (int)tb.size()) {
+      // warp bits unchanged after a register phase: keep every lane bit that
+      // is still a thread bit at its lane position and put the new ones (the
+      // previous phase's register bits) in the freed positions, so the
+      // transition is a set of lane <-> register bit swaps the generated
+      // kernel does with warp shuffles (no shared memory, no barrier)
+      std::vector<int> lanes(nlane, -1), avail = tb;
+      for (int p = 0; p < nlane; ++p) {
+        auto it = std::find(avail.begin(), avail.end(), prev_lanes[p]);
+        if (it != avail.end()) {
+          lanes[p] = *it;
+          avail.erase(it);
+        }
+      }
+      size_t ai = 0;
+      for (int p = 0; p < nlane; ++p)
+        if (lanes[p] < 0) lanes[p] = avail[ai++];
+      tb = lanes;
+    } else {
+      order_thread_bits(tb);
+    }
+    prev_lanes.assign(tb.begin(), tb.begin() + nlane);
+    prev_warp = cur_warp;
     tb.insert(tb.end(), cur_warp.begin(), cur_warp.end());
     for (size_t k = 0; k < tb.size(); ++k) ph.thrpos[k] = tb[k];
     for (int v = 0; v < 16; ++v) {
@@ -1712,6 +1747,7 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
       ph.op_end = (int)e.ops.size();
       e.phases.push_back(ph);
       e.fp64_ops_per_amp += 4.0 * (double)(1 << g.m);
+      prev_lanes.clear();
       continue;
     }
     if (g.kind == QSV_OP_DIAG) {
@@ -1773,6 +1809,7 @@ Encoded encode_pass(int n, int L, uint64_t S, const std::vector<const GateDesc*>
     ph.op_end = (int)e.ops.size();
     e.phases.push_back(ph);
     e.fp64_ops_per_amp += 8.0;
+    prev_lanes.clear();
   }
   gi = pg.size();
   close(false);

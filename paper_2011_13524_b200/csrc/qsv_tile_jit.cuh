@@ -403,15 +403,80 @@ struct Gen {
   // then issues the next tile's copy-in once this phase's reads are done.
   // The thread layouts keep qubits 0..3 on lane or register bits, so every
   // warp's loads / stores cover whole 128-byte lines.
+  // P -> Q by warp shuffles: Q keeps P's warp bits and every lane position
+  // either keeps its bit or swaps it with one of P's register bits (the
+  // encoder aligns lanes for this).  Each swap of lane bit p with register
+  // slot s is a butterfly: the lane with bit p clear sends its slot-s=1
+  // value, the other its slot-s=0 value, and each keeps the received one in
+  // that place; then the slots are renamed to Q's order (free).
+  bool shuffle_ok(const TilePhase& P, const TilePhase& Q) const {
+    if (P.type != 0 || Q.type != 0 || G < 32 || L - R < 5) return false;
+    for (int b = 5; b < L - R; ++b)
+      if (P.thrpos[b] != Q.thrpos[b]) return false;
+    for (int p = 0; p < 5; ++p) {
+      if (P.thrpos[p] == Q.thrpos[p]) continue;
+      bool y_reg = false, x_reg = false;
+      for (int i = 0; i < R; ++i) {
+        y_reg = y_reg || P.regpos[i] == Q.thrpos[p];
+        x_reg = x_reg || Q.regpos[i] == P.thrpos[p];
+      }
+      if (!y_reg || !x_reg) return false;
+    }
+    return true;
+  }
+  void shuffle_to(const TilePhase& P, const TilePhase& Q) {
+    int cur[8];  // slot -> local bit it encodes
+    for (int i = 0; i < R; ++i) cur[i] = P.regpos[i];
+    line("{ // shuffle transition");
+    for (int p = 0; p < 5; ++p) {
+      if (P.thrpos[p] == Q.thrpos[p]) continue;
+      int sl = -1;
+      for (int i = 0; i < R; ++i)
+        if (cur[i] == Q.thrpos[p]) sl = i;
+      line("{ const bool b_ = (tid >> " + std::to_string(p) + ") & 1u;");
+      for (int j = 0; j < R2; ++j) {
+        if ((j >> sl) & 1) continue;
+        const std::string j0 = "v[" + std::to_string(j) + "]",
+                          j1 = "v[" + std::to_string(j | (1 << sl)) + "]";
+        line("  { const double2 s_ = b_ ? " + j0 + " : " + j1 + "; double2 r_;");
+        line("    r_.x = __shfl_xor_sync(0xffffffffu, s_.x, " + std::to_string(1 << p) + ");");
+        line("    r_.y = __shfl_xor_sync(0xffffffffu, s_.y, " + std::to_string(1 << p) + ");");
+        line("    if (b_) " + j0 + " = r_; else " + j1 + " = r_; }");
+      }
+      line("}");
+      cur[sl] = P.thrpos[p];
+    }
+    // rename slots to Q's order: Q slot i holds bit Q.regpos[i]
+    int sigma[8];
+    for (int i = 0; i < R; ++i)
+      for (int s2 = 0; s2 < R; ++s2)
+        if (cur[s2] == Q.regpos[i]) sigma[i] = s2;
+    bool ident = true;
+    for (int i = 0; i < R; ++i) ident = ident && sigma[i] == i;
+    if (!ident) {
+      std::string t = "const double2 t_[" + std::to_string(R2) + "] = {";
+      for (int jq = 0; jq < R2; ++jq) {
+        int jc = 0;
+        for (int i = 0; i < R; ++i)
+          if ((jq >> i) & 1) jc |= 1 << sigma[i];
+        t += (jq ? ", v[" : "v[") + std::to_string(jc) + "]";
+      }
+      line(t + "};");
+      for (int jq = 0; jq < R2; ++jq)
+        line("v[" + std::to_string(jq) + "] = t_[" + std::to_string(jq) + "];");
+    }
+    line("}");
+  }
+
   void reg_phase(const TilePhase& P, bool load_global, bool store_global,
                  const std::string& prefetch, bool warp_local_next,
-                 const std::string& next_sync = std::string()) {
+                 const std::string& next_sync = std::string(), bool from_regs = false,
+                 const TilePhase* next_shuffle = nullptr) {
     std::vector<int> thr;
     for (int j = 0; j < L - R; ++j) thr.push_back(P.thrpos[j]);
     line("{ // register phase");
     line("const uint32_t lt = " + deposit(thr, "tidv") + ";");
     line("const uint32_t slt = swz(lt);");
-    line("double2 v[" + std::to_string(R2) + "];");
     if (load_global || store_global) line(gl_decl(P));
     uint32_t srb[8];
     for (int i = 0; i < R; ++i) srb[i] = swz_host(1u << P.regpos[i]);
@@ -421,6 +486,7 @@ struct Gen {
       for (int i = 0; i < R; ++i)
         if ((j >> i) & 1) ad ^= srb[i];
       cj[j] = ad;
+      if (from_regs) continue;  // arrived by a shuffle transition
       if (load_global)
         line("v[" + std::to_string(j) + "] = ld1(a + (gl_ | " + hex64(gl_slot(P, j)) + "));");
       else
@@ -434,6 +500,11 @@ struct Gen {
     if (store_global) {
       for (int j = 0; j < R2; ++j)
         line("st1(a + (gl_ | " + hex64(gl_slot(P, j)) + "), v[" + std::to_string(j) + "]);");
+      line("}");
+      return;
+    }
+    if (next_shuffle) {
+      shuffle_to(P, *next_shuffle);
       line("}");
       return;
     }
@@ -630,6 +701,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   std::string& o = g.o;
   o += jit_prelude();
   o += "#define QSV_G " + std::to_string(G) + "\n";
+  o += "#define QSV_R2 " + std::to_string(kRegs) + "\n";
   o += std::string("constexpr bool jit_nohoist = ") + (jit_nohoist() ? "true" : "false") + ";\n";
   o += "#define QSV_GROUPS " + std::to_string(kGroups) + "\n";
   o += "struct __align__(16) PassParams { double2* a; u64 ntiles; u64* ctr; int nostagger; "
@@ -726,10 +798,12 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
     uint32_t tidv = tid;
     if (jit_nohoist) asm volatile("mov.u32 %0, %0;" : "+r"(tidv));
     const u64 base = widen(tile, P.tb);
+    double2 v[QSV_R2];  // the thread's amplitudes, live across shuffle transitions
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     group_sync(group);
 )JIT";
   int ph_idx = 0;
+  bool shuffled_in = false;
   const int nph = (int)e.phases.size();
   // the most frequent kept-warp-position pattern among partial transitions
   uint32_t part_pattern = 0;
@@ -785,13 +859,19 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
       }
     }
     const bool first_ph = ph_idx == 0;
+    // entry by shuffles (the previous phase ended with them) / exit by shuffles
+    const bool from_regs = ph_idx > 0 && shuffled_in;
+    const TilePhase* shuf = (!last && jit_shuffle_transitions() &&
+                             g.shuffle_ok(P, e.phases[ph_idx + 1])) ? &e.phases[ph_idx + 1] : nullptr;
     if (P.type == 0 && last && direct)
       g.reg_phase(P, first_ph && direct_load, true,
                   direct_load ? std::string()
                               : "const u64 nxt_ = s_next[group][it_ & 1u]; " + copy_of("nxt_"),
-                  false);
-    else if (P.type == 0) g.reg_phase(P, first_ph && direct_load, false, std::string(), wl, psync);
+                  false, std::string(), from_regs);
+    else if (P.type == 0)
+      g.reg_phase(P, first_ph && direct_load, false, std::string(), wl, psync, from_regs, shuf);
     else g.smem_phase(P);
+    shuffled_in = shuf != nullptr;
     ++ph_idx;
   }
   if (!direct) {
