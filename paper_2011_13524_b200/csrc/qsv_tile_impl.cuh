@@ -1298,12 +1298,15 @@ inline bool jit_partial_barriers() {
   return on != 0;
 }
 
-// QSV_JIT_SHUFFLE=0: warp-local phase transitions go through shared memory
-// (A/B); on: lane <-> register bit swaps with warp shuffles
+// QSV_JIT_SHUFFLE=1: warp-local phase transitions as lane <-> register bit
+// swaps with warp shuffles (and lanes aligned by the encoder for them).  Off
+// by default: measured slower (cz-ladder(30) 222.7 -> 233.1 ms, cnot-ring(30)
+// 303.6 -> 310.8 ms) -- four 32-bit shuffles plus selects per moved amplitude
+// cost more issue slots than the 128-bit shared-memory round trip they save
 inline bool jit_shuffle_transitions() {
   static const int on = [] {
     const char* e = getenv("QSV_JIT_SHUFFLE");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   return on != 0;
 }
