@@ -1268,6 +1268,26 @@ inline bool jit_nohoist() {
   return on != 0;
 }
 
+// QSV_JIT_ADDR_SPLIT=0: slot addresses as sm[slt ^ c] (one LOP3 + LEA per
+// LDS/STS) instead of per-phase base pointers with immediate offsets (A/B)
+inline bool jit_addr_split() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_ADDR_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
+// QSV_JIT_SIGN_FOLD=0: flush signs as (bits << k) & 0x80000000 then two
+// xors, instead of the mask folded into each xor (A/B)
+inline bool jit_sign_fold() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_SIGN_FOLD");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 // QSV_JIT_DIRECT_LOAD=0: tiles always enter through cp.async copy-in (A/B)
 inline bool jit_direct_load() {
   static const int on = [] {

@@ -163,7 +163,10 @@ struct Gen {
   }
   // runtime sign rules (FlushSign records at payload D..): bits ^= col where
   // the thread / tile pattern holds
-  void sign_rules(uint32_t D, int m, const char* bits) {
+  // returns the bits some thread may see set (the others are the static
+  // xor of sgn0 and the unconditional rules, tracked in *stat)
+  uint32_t sign_rules(uint32_t D, int m, const char* bits, uint32_t* stat = nullptr) {
+    uint32_t dyn = 0;
     for (int r = 0; r < m; ++r) {
       FlushSign S;
       rec(&S, D + 2 * r, 2);
@@ -173,12 +176,33 @@ struct Gen {
         if (!cond.empty()) cond += " && ";
         cond += "(base & " + hex64(S.gm) + ") == " + hex64(S.gv);
       }
-      if (cond.empty()) line(std::string(bits) + " ^= " + hex32(S.col) + ";");
-      else line("if (" + cond + ") " + bits + " ^= " + hex32(S.col) + ";");
+      if (cond.empty()) {
+        line(std::string(bits) + " ^= " + hex32(S.col) + ";");
+        if (stat) *stat ^= S.col;
+      } else {
+        line("if (" + cond + ") " + bits + " ^= " + hex32(S.col) + ";");
+        dyn |= S.col;
+      }
+    }
+    return dyn;
+  }
+  void apply_signs(const char* bits, uint32_t const_neg, uint32_t dyn, uint32_t stat) {
+    // v[j] = -v[j] where bit j of (bits ^ const_neg) is set: one shift and
+    // one three-input LOP3 per component ((t & 0x80000000) ^ hi, the mask
+    // folded into the xor); bits no thread sees change are static negations
+    for (int j = 0; j < R2; ++j) {
+      const std::string vj = "v[" + std::to_string(j) + "]";
+      if (!((dyn >> j) & 1u)) {
+        if (((stat ^ const_neg) >> j) & 1u)
+          line(vj + ".x = -" + vj + ".x; " + vj + ".y = -" + vj + ".y;");
+        continue;
+      }
+      const std::string t = "(" + std::string(bits) + " << " + std::to_string(31 - j) + ")";
+      line(vj + " = negm" + (((const_neg >> j) & 1u) ? "<true>" : "") + "(" + vj + ", " + t +
+           ");");
     }
   }
-  void apply_signs(const char* bits, uint32_t const_neg) {
-    // v[j] = -v[j] where bit j of (bits ^ const_neg) is set
+  void apply_signs_old(const char* bits, uint32_t const_neg) {
     for (int j = 0; j < R2; ++j) {
       const std::string vj = "v[" + std::to_string(j) + "]";
       if ((const_neg >> j) & 1u)
@@ -197,7 +221,8 @@ struct Gen {
     const uint32_t sgn0 = table ? 0u : op.lmask;
     const uint32_t sD = table ? D + R2 : D;
     line("{ uint32_t bits_ = " + hex32(sgn0) + ";");
-    sign_rules(sD, op.m, "bits_");
+    uint32_t stat = sgn0;
+    const uint32_t dyn = sign_rules(sD, op.m, "bits_", &stat);
     uint32_t neg = 0;
     if (table) {
       if (op.slots) {  // per-thread factors of non-register qubits
@@ -218,7 +243,8 @@ struct Gen {
       table_mul(D, &neg);
     }
     if (op.m > 0 || sgn0 != 0) {
-      apply_signs("bits_", neg);
+      if (jit_sign_fold()) apply_signs("bits_", neg, dyn, stat);
+      else apply_signs_old("bits_", neg);
     } else if (neg) {
       for (int j = 0; j < R2; ++j)
         if ((neg >> j) & 1u)
@@ -486,11 +512,34 @@ struct Gen {
       for (int i = 0; i < R; ++i)
         if ((j >> i) & 1) ad ^= srb[i];
       cj[j] = ad;
+    }
+    // Slot addresses without per-access integer work: swz only rewrites bits
+    // 0..2, and the thread and register parts of a local index are disjoint
+    // bit sets, so slt ^ c = (slt_hi + c_hi) | (slt_lo ^ c_lo): one base
+    // pointer per distinct c_lo (at most 8, set up once per phase), c_hi an
+    // immediate offset of the LDS / STS
+    std::string sref[64];
+    if (!jit_addr_split()) {
+      for (int j = 0; j < R2; ++j) sref[j] = "sm[slt ^ " + std::to_string(cj[j]) + "u]";
+    } else {
+      bool used[8] = {false};
+      for (int j = 0; j < R2; ++j) used[cj[j] & 7u] = true;
+      line("const uint32_t shi_ = slt & ~7u, slo_ = slt & 7u;");
+      for (int k = 0; k < 8; ++k)
+        if (used[k])
+          line("double2* const b" + std::to_string(k) + "_ = sm + (shi_ | (slo_ ^ " +
+               std::to_string(k) + "u));");
+      for (int j = 0; j < R2; ++j)
+        sref[j] = "b" + std::to_string(cj[j] & 7u) + "_[" + std::to_string(cj[j] & ~7u) + "]";
+    }
+    for (int j = 0; j < R2; ++j) {
+      const uint32_t ad = cj[j];
+      (void)ad;
       if (from_regs) continue;  // arrived by a shuffle transition
       if (load_global)
         line("v[" + std::to_string(j) + "] = ld1(a + (gl_ | " + hex64(gl_slot(P, j)) + "));");
       else
-        line("v[" + std::to_string(j) + "] = sm[slt ^ " + std::to_string(ad) + "u];");
+        line("v[" + std::to_string(j) + "] = " + sref[j] + ";");
     }
     if (store_global && !load_global && !prefetch.empty()) {
       line("group_sync(group);");
@@ -508,8 +557,7 @@ struct Gen {
       line("}");
       return;
     }
-    for (int j = 0; j < R2; ++j)
-      line("sm[slt ^ " + std::to_string(cj[j]) + "u] = v[" + std::to_string(j) + "];");
+    for (int j = 0; j < R2; ++j) line(sref[j] + " = v[" + std::to_string(j) + "];");
     line("}");
     // the next register phase keeps this phase's warp bits: each warp reads
     // back only what it wrote, so a warp barrier orders it
@@ -611,6 +659,20 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
 __device__ __forceinline__ double2 negs(double2 v, int s) {
   return make_double2(__hiloint2double(__double2hiint(v.x) ^ s, __double2loint(v.x)),
                       __hiloint2double(__double2hiint(v.y) ^ s, __double2loint(v.y)));
+}
+template <bool Inv>
+__device__ __forceinline__ uint32_t xsgn(uint32_t hi, uint32_t t) {
+  uint32_t r;  // ((Inv ? ~t : t) & 0x80000000) ^ hi in one LOP3 (the compiler
+               // would CSE the masked sign and spend a second instruction)
+  if (Inv) asm("lop3.b32 %0, %1, 0x80000000, %2, 0xa6;" : "=r"(r) : "r"(t), "r"(hi));
+  else asm("lop3.b32 %0, %1, 0x80000000, %2, 0x6a;" : "=r"(r) : "r"(t), "r"(hi));
+  return r;
+}
+template <bool Inv = false>
+__device__ __forceinline__ double2 negm(double2 v, uint32_t t) {
+  return make_double2(
+      __hiloint2double((int)xsgn<Inv>((uint32_t)__double2hiint(v.x), t), __double2loint(v.x)),
+      __hiloint2double((int)xsgn<Inv>((uint32_t)__double2hiint(v.y), t), __double2loint(v.y)));
 }
 __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
