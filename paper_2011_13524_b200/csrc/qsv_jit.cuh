@@ -31,7 +31,7 @@ struct JitParamHead {
   unsigned long long ntiles;
   unsigned long long* ctr;
   int nostagger;
-  int pad;
+  int stat;  // one tile per CTA (group 0 takes tile blockIdx.x), no work counter
   FixedBits tb;
 };
 static_assert(sizeof(JitParamHead) % 16 == 0, "payload must start 16-byte aligned");

@@ -1288,6 +1288,16 @@ inline bool jit_sign_fold() {
   return on != 0;
 }
 
+// QSV_JIT_STATIC=0: passes with no more tiles than resident CTAs still pull
+// tiles from the work counter (A/B)
+inline bool jit_static_tiles() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_STATIC");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 // QSV_JIT_DIRECT_LOAD=0: tiles always enter through cp.async copy-in (A/B)
 inline bool jit_direct_load() {
   static const int on = [] {
@@ -2392,7 +2402,10 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     }
     if (max_ctas > 0) per_sm = 1;
     unsigned grid;
-    if (ntiles_all <= (uint64_t)sms * per_sm) {
+    if (ntiles_all <= (uint64_t)sms * per_sm && jit_static_tiles()) {
+      grid = (unsigned)ntiles_all;
+      h.stat = 1;
+    } else if (ntiles_all <= (uint64_t)sms * per_sm) {
       grid = (unsigned)ntiles_all;
     } else {
       const uint64_t ctas = (ntiles_all + kGroups - 1) / kGroups;

@@ -767,7 +767,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   o += std::string("constexpr bool jit_nohoist = ") + (jit_nohoist() ? "true" : "false") + ";\n";
   o += "#define QSV_GROUPS " + std::to_string(kGroups) + "\n";
   o += "struct __align__(16) PassParams { double2* a; u64 ntiles; u64* ctr; int nostagger; "
-       "int pad; FixedBits tb; double2 d[" + std::to_string(js.ndata) + "]; };\n";
+       "int stat; FixedBits tb; double2 d[" + std::to_string(js.ndata) + "]; };\n";
   // named barriers need whole warps; groups smaller than a warp (tiles of
   // L < 5 + register bits) share one warp and synchronise on their lane mask
   if (G >= 32)
@@ -795,7 +795,8 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   // CTAs queue behind this one as SMs free up
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  if (threadIdx.x == 0) *s_go = (QSV_GROUPS < 2 || P.nostagger || QSV_G < 32) ? QSV_GROUPS : 0;
+  if (threadIdx.x == 0)
+    *s_go = (QSV_GROUPS < 2 || P.nostagger || P.stat || QSV_G < 32) ? QSV_GROUPS : 0;
   __syncthreads();
   if (group > 0) while (*s_go < group) __nanosleep(256);
   bool first = true;
@@ -843,9 +844,16 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   }
   // the next tile is prefetched as soon as this tile's buffer is free
   o += R"JIT(
-  if (tid == 0) s_next[group][0] = atomicAdd(P.ctr, 1ull);
-  group_sync(group);
-  u64 tile = s_next[group][0];
+  // static assignment (grid = tiles): no work-counter round trips (about a
+  // microsecond each at the head and tail of a small pass)
+  u64 tile;
+  if (P.stat) {
+    tile = group == 0 ? (u64)blockIdx.x : P.ntiles;
+  } else {
+    if (tid == 0) s_next[group][0] = atomicAdd(P.ctr, 1ull);
+    group_sync(group);
+    tile = s_next[group][0];
+  }
   uint32_t it_ = 1;
 )JIT";
   // first phase straight from HBM (no copy-in, no prefetch)
@@ -853,7 +861,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   if (!direct_load) o += "  " + copy_of("tile") + "\n";
   o += R"JIT(  const int nph_total = )JIT" + std::to_string(std::max<size_t>(1, e.phases.size())) + R"JIT(;
   while (tile < P.ntiles) {
-    if (tid == 0) s_next[group][it_ & 1u] = atomicAdd(P.ctr, 1ull);
+    if (tid == 0) s_next[group][it_ & 1u] = P.stat ? P.ntiles : atomicAdd(P.ctr, 1ull);
     // an opaque per-tile copy of tid: the phases' thread-bit deposits are
     // recomputed in each tile (a few ALU ops) instead of being hoisted out of
     // the tile loop, where dozens of them stay live and spill
@@ -952,6 +960,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
     tile = s_next[group][it_ & 1u];
     ++it_;
   }
+  if (P.stat) return;
   if (group == 0 && tid == 0) *s_go = QSV_GROUPS;
   __syncthreads();
   if (threadIdx.x == 0) {
