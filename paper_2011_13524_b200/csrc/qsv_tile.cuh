@@ -146,6 +146,7 @@ struct PlanMix {
                        cudaStream_t s, int max_ctas, unsigned long long* ctr,               \
                        uint64_t fmask, uint64_t fval);                                      \
   }
+QSV_TILE_DECLARE(r3)
 QSV_TILE_DECLARE(r4)
 QSV_TILE_DECLARE(r5)
 #undef QSV_TILE_DECLARE

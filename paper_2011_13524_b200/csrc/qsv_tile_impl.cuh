@@ -2446,13 +2446,23 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
   }
   static int attr_dev = -1;
   static int num_sms = 148;
+  static int dyn_limit = kTileSmemLimit;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
+    // the dynamic window is what the static shared memory leaves of 227 KB
+    cudaFuncAttributes fa;
+    QSV_TRY(cudaFuncGetAttributes(&fa, k_tile));
+    dyn_limit = std::min<int>(kTileSmemLimit, 227 * 1024 - (int)fa.sharedSizeBytes);
     QSV_TRY(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kTileSmemLimit));
+                                 dyn_limit));
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     attr_dev = dev;
+  }
+  if ((int)smem > dyn_limit) {
+    set_error("tile pass program (%d ops, %d phases) does not fit in shared memory", tp.nops,
+              tp.nphases);
+    return QSV_EUNSUPPORTED;
   }
   const uint64_t ntiles = 1ULL << (n - np);
   const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms) : num_sms;

@@ -3,6 +3,7 @@
 // batches, otherwise the 16-amplitude kernel (r4); one plan per program.  Measured (profiles/variant_ab.py, time_fused.py):
 // cz-ladder r5, cnot-ring / QV / QFT / heavy(2..4) r4, heavy(5) r5 (2x).
 // QSV_TILE_VARIANT=4|5 forces one (A/B experiments).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -58,8 +59,22 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
   // fusion and real frames once (identical in both variants), then one plan
   std::vector<GateDesc> pre = r5::preprocess(n, gates, opts);
   bool use5 = force == 5;
+  // the 8-amplitude kernel (r3) takes tiles of at most 11 qubits
+  bool use3 = force == 3 && on4 && n >= 12;
+  int l3 = 0;  // its tile size when chosen here
   if (!force) {
     const PlanMix mix = estimate_mix(pre);
+    // small states under generated kernels: a pass is a chain of dependent
+    // phases on 32..256 tiles, one warp per scheduler; twice the threads per
+    // tile halve each thread's chain (cnot-ring(16) 0.118 -> 0.101 ms,
+    // cz-ladder(16) 0.104 -> 0.092, (14) 0.091 -> 0.077, cnot-ring(18) 0.151
+    // -> 0.134; from n = 20 the 16-amplitude kernel with 12-qubit tiles is
+    // faster, profiles/r2_small_n_r3.md)
+    if (opts.jit && opts.tile_qubits == 0 && opts.outer_mask == 0 && n >= 12 && n <= 18 &&
+        on4 && on5 && mix.wide_dense == 0 && !getenv("QSV_FIXED_TILE")) {
+      use3 = true;
+      l3 = n <= 16 ? 10 : 11;
+    }
     const int r5_score = mix.real_ops / 2 + 4 * mix.wide_dense;
     use5 = r5_score > 0 && r5_score >= mix.complex_ops;
     // generated pass kernels (the steady state of a program run more than
@@ -73,6 +88,12 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
     return r4::plan_program(n, gates, opts, steps, tiles, payload, stats, nullptr, false);
   auto plan_with = [&](const qsv_plan_opts& o, std::vector<Step>& st, std::vector<TilePlan>& tp,
                        std::vector<char>& pl, qsv_program_stats* ps) {
+    if (use3) {
+      qsv_plan_opts o3 = o;
+      if (o3.tile_qubits == 0) o3.tile_qubits = l3 ? l3 : 11;
+      o3.tile_qubits = std::min(o3.tile_qubits, 11);
+      return r3::plan_program(n, pre, o3, st, tp, pl, ps, nullptr, true);
+    }
     return use5 ? r5::plan_program(n, pre, o, st, tp, pl, ps, nullptr, true)
                 : r4::plan_program(n, pre, o, st, tp, pl, ps, nullptr, true);
   };
@@ -85,14 +106,14 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
   // profiles/time_small_n.py: it picks the measured best or within 1% of it
   // in all eight cases).
   if (opts.tile_qubits == 0 && opts.outer_mask == 0 && n <= 20 && n >= 11 && on4 && on5 &&
-      !getenv("QSV_FIXED_TILE")) {
+      !l3 && !getenv("QSV_FIXED_TILE")) {
     constexpr double kPass = 15.2e-3, kAmpPhase = 2.95e-7;  // ms
     constexpr double kGroupsPerGpu = 296.0;                 // 2 tile groups x 148 SMs
     double best_cost = 0;
     int best_rc = QSV_OK;
     bool have = false;
     const qsv_program_stats init = *stats;
-    for (int L = 10; L <= 12; ++L) {
+    for (int L = 10; L <= (use3 ? 11 : 12); ++L) {
       qsv_plan_opts o = opts;
       o.tile_qubits = L;
       std::vector<Step> st;
@@ -190,6 +211,8 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
 int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_payload,
                      cudaStream_t s, int max_ctas, unsigned long long* ctr, uint64_t fmask,
                      uint64_t fval) {
+  if (tp.variant == 3)
+    return r3::launch_tile_pass(amps, n, tp, dev_payload, s, max_ctas, ctr, fmask, fval);
   return tp.variant == 5
              ? r5::launch_tile_pass(amps, n, tp, dev_payload, s, max_ctas, ctr, fmask, fval)
              : r4::launch_tile_pass(amps, n, tp, dev_payload, s, max_ctas, ctr, fmask, fval);

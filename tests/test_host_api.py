@@ -191,14 +191,25 @@ def _core(circ):
     return circ._core if hasattr(circ, "_core") else circ
 
 
-def test_small_state_tile_size_choice():
+def test_small_state_tile_size_choice(monkeypatch):
     """n <= 20: the planner keeps the cheapest of the L = 10/11/12 plans
-    (qsv_tile_select.cu); larger states and explicit tile sizes are unchanged."""
+    (qsv_tile_select.cu); under generated kernels n = 12..18 take the
+    8-amplitude kernel with 10-qubit (n <= 16) or 11-qubit tiles; larger
+    states and explicit tile sizes are unchanged."""
     for n, expect_l in ((16, 11), (20, 12)):
         c = _core(workloads.generate_cnot_ring(n, seed=1))
-        auto = c.plan_stats(use_tiles=1)
-        per_l = {L: c.plan_stats(use_tiles=1, tile_qubits=L) for L in (10, 11, 12)}
+        auto = c.plan_stats(use_tiles=1, jit=0)
+        per_l = {L: c.plan_stats(use_tiles=1, tile_qubits=L, jit=0) for L in (10, 11, 12)}
         assert auto == per_l[expect_l], (n, auto, per_l)
+    assert (_core(workloads.generate_cnot_ring(20, seed=1)).plan_stats(use_tiles=1, jit=1)
+            ["num_steps"] == 21)
+    for n, l3 in ((14, 10), (16, 10), (18, 11)):
+        c = _core(workloads.generate_cnot_ring(n, seed=1))
+        auto = c.plan_stats(use_tiles=1, jit=1)
+        monkeypatch.setenv("QSV_TILE_VARIANT", "3")
+        forced = c.plan_stats(use_tiles=1, tile_qubits=l3, jit=1)
+        monkeypatch.delenv("QSV_TILE_VARIANT")
+        assert auto == forced, (n, auto, forced)
     c = _core(workloads.generate_cz_ladder(24, 4, seed=1))
     assert c.plan_stats(use_tiles=1) == c.plan_stats(use_tiles=1, tile_qubits=12)
 
