@@ -1298,6 +1298,19 @@ inline bool jit_static_tiles() {
   return on != 0;
 }
 
+// QSV_JIT_LATE_SYNC=1: the tile's group barrier and the next-tile index
+// publication move from the top of the tile loop to the first shared-memory
+// store, after the HBM loads.  Off: mixed (cnot-ring(30) 315.7 -> 307.8 ms,
+// cz-ladder(30) 223.5 -> 225.1 ms, (28) 49.8 -> 50.7 ms;
+// profiles/r2_late_sync_ab.md)
+inline bool jit_late_sync() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_LATE_SYNC");
+    return e ? atoi(e) : 0;
+  }();
+  return on != 0;
+}
+
 // QSV_JIT_DIRECT_LOAD=0: tiles always enter through cp.async copy-in (A/B)
 inline bool jit_direct_load() {
   static const int on = [] {

@@ -58,6 +58,9 @@ struct Gen {
   const Encoded& e;
   int L, R, R2, G;
   std::string o;
+  // emitted once, right before the tile's first shared-memory store (the
+  // group barrier that protects the tile buffer, moved past the loads)
+  std::string pre_store;
   explicit Gen(const Encoded& enc, int L_) : e(enc), L(L_), R(kRegBits), R2(kRegs) {
     G = 1 << (L - kRegBits);
   }
@@ -557,6 +560,10 @@ struct Gen {
       line("}");
       return;
     }
+    if (!pre_store.empty()) {
+      line(pre_store);
+      pre_store.clear();
+    }
     for (int j = 0; j < R2; ++j) line(sref[j] + " = v[" + std::to_string(j) + "];");
     line("}");
     // the next register phase keeps this phase's warp bits: each warp reads
@@ -859,9 +866,21 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   // first phase straight from HBM (no copy-in, no prefetch)
   const bool direct_load = jit_direct_load() && !e.phases.empty() && e.phases[0].type == 0;
   if (!direct_load) o += "  " + copy_of("tile") + "\n";
+  // late sync (direct loads): the next tile's index stays in a register of
+  // thread 0 and the group barrier that guards the tile buffer moves to the
+  // first shared-memory store, so neither the work-counter round trip nor
+  // the barrier delays this tile's HBM loads
+  const bool late_sync = direct_load && jit_late_sync();
   o += R"JIT(  const int nph_total = )JIT" + std::to_string(std::max<size_t>(1, e.phases.size())) + R"JIT(;
   while (tile < P.ntiles) {
-    if (tid == 0) s_next[group][it_ & 1u] = P.stat ? P.ntiles : atomicAdd(P.ctr, 1ull);
+)JIT";
+  if (late_sync) {
+    o += "    u64 nxt_ = P.ntiles;\n    if (tid == 0 && !P.stat) nxt_ = atomicAdd(P.ctr, 1ull);\n";
+    g.pre_store = "if (tid == 0) s_next[group][it_ & 1u] = nxt_;\ngroup_sync(group);";
+  } else {
+    o += "    if (tid == 0) s_next[group][it_ & 1u] = P.stat ? P.ntiles : atomicAdd(P.ctr, 1ull);\n";
+  }
+  o += R"JIT(
     // an opaque per-tile copy of tid: the phases' thread-bit deposits are
     // recomputed in each tile (a few ALU ops) instead of being hoisted out of
     // the tile loop, where dozens of them stay live and spill
@@ -869,9 +888,9 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
     if (jit_nohoist) asm volatile("mov.u32 %0, %0;" : "+r"(tidv));
     const u64 base = widen(tile, P.tb);
     double2 v[QSV_R2];  // the thread's amplitudes, live across shuffle transitions
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    group_sync(group);
 )JIT";
+  if (!late_sync)
+    o += "    asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n    group_sync(group);\n";
   int ph_idx = 0;
   bool shuffled_in = false;
   const int nph = (int)e.phases.size();
@@ -954,6 +973,10 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
       o += "      st1(a + (gb | " + hex64(hi[k]) + "), sm[" + std::to_string(sk[k]) + "u ^ st]);\n";
     o += "    }\n    group_sync(group);\n";
     if (!direct_load) o += "    " + copy_of("s_next[group][it_ & 1u]") + "\n";
+  }
+  if (!g.pre_store.empty()) {  // no shared-memory store in this pass
+    o += g.pre_store + "\n";
+    g.pre_store.clear();
   }
   o += R"JIT(    if (group == 0 && first && tid == 0) *s_go = QSV_GROUPS;
     first = false;
