@@ -1366,6 +1366,16 @@ inline int jit_stagger_max_phases() {
 // (the next pass queued while this one drains).  Off by default: measured
 // slower on every small-state circuit (cnot-ring(14) 0.117 -> 0.138 ms,
 // cz-ladder(16) 0.180 -> 0.207 ms; profiles/r2_small_n_pdl.txt)
+// QSV_PDL_LATE=1 (with QSV_PDL=1): trigger the dependent launch after each
+// CTA's last tile instead of at kernel start (A/B)
+inline bool jit_pdl_late() {
+  static const int on = [] {
+    const char* e = getenv("QSV_PDL_LATE");
+    return e ? atoi(e) : 0;
+  }();
+  return on != 0;
+}
+
 inline bool jit_pdl() {
   static const int on = [] {
     const char* e = getenv("QSV_PDL");

@@ -773,6 +773,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   o += "#define QSV_R2 " + std::to_string(kRegs) + "\n";
   o += std::string("constexpr bool jit_nohoist = ") + (jit_nohoist() ? "true" : "false") + ";\n";
   o += "#define QSV_GROUPS " + std::to_string(kGroups) + "\n";
+  o += std::string("#define QSV_PDL_LATE ") + (jit_pdl_late() ? "1" : "0") + "\n";
   o += "struct __align__(16) PassParams { double2* a; u64 ntiles; u64* ctr; int nostagger; "
        "int stat; FixedBits tb; double2 d[" + std::to_string(js.ndata) + "]; };\n";
   // named barriers need whole warps; groups smaller than a warp (tiles of
@@ -801,7 +802,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   // first read of the state or the work counter, and let the next pass's
   // CTAs queue behind this one as SMs free up
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
+  if (!QSV_PDL_LATE) asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0)
     *s_go = (QSV_GROUPS < 2 || P.nostagger || P.stat || QSV_G < 32) ? QSV_GROUPS : 0;
   __syncthreads();
@@ -983,6 +984,9 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
     tile = s_next[group][it_ & 1u];
     ++it_;
   }
+  // late trigger: the next pass's CTAs are scheduled once this CTA's tiles
+  // are stored (they wait in griddepcontrol.wait for the whole grid anyway)
+  if (QSV_PDL_LATE) asm volatile("griddepcontrol.launch_dependents;");
   if (P.stat) return;
   if (group == 0 && tid == 0) *s_go = QSV_GROUPS;
   __syncthreads();
