@@ -218,9 +218,11 @@ def test_planner_fuzz():
         seed = int(rng.integers(1 << 30))
         circ = random_circuit(n, ng, seed, max_k=int(rng.integers(2, 5))) if case % 2 \
             else layered_circuit(n, int(rng.integers(2, 8)), seed)
+        if case % 5 == 4:
+            L = 0  # the planner's own choice (n = 12..18: 8-amplitude kernel)
         opts = dict(tile_qubits=L, real_frames=int(rng.integers(2)), fuse=int(rng.integers(2)),
                     use_graph=int(rng.integers(2)))
-        variant = ("", "4", "5")[int(rng.integers(3))]
+        variant = ("", "3", "4", "5")[int(rng.integers(4))]  # r3 caps tiles at 11 qubits
         if variant:
             os.environ["QSV_TILE_VARIANT"] = variant
         try:
