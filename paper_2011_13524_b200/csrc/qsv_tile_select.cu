@@ -73,7 +73,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
     if (opts.jit && opts.tile_qubits == 0 && opts.outer_mask == 0 && n >= 12 && n <= 18 &&
         on4 && on5 && mix.wide_dense == 0 && !getenv("QSV_FIXED_TILE")) {
       use3 = true;
-      l3 = n <= 16 ? 10 : 11;
+      l3 = n <= 17 ? 10 : 11;  // n = 17: 0.112 vs 0.124 ms (cnot-ring); n = 18 equal
     }
     const int r5_score = mix.real_ops / 2 + 4 * mix.wide_dense;
     use5 = r5_score > 0 && r5_score >= mix.complex_ops;
@@ -105,8 +105,11 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
   // n = 14..20 with the few-tile grid policy of launch_tile_pass,
   // profiles/time_small_n.py: it picks the measured best or within 1% of it
   // in all eight cases).
+  // (generated kernels from n = 19: 12-qubit tiles measured best at n = 19..22 -- cnot-ring(19)
+  // 0.190 vs 0.240 ms for the model's L = 11, profiles/r2_mid_n.md -- so the model only
+  // serves the interpreter)
   if (opts.tile_qubits == 0 && opts.outer_mask == 0 && n <= 20 && n >= 11 && on4 && on5 &&
-      !l3 && !getenv("QSV_FIXED_TILE")) {
+      !l3 && !(opts.jit && n >= 19) && !getenv("QSV_FIXED_TILE")) {
     constexpr double kPass = 15.2e-3, kAmpPhase = 2.95e-7;  // ms
     constexpr double kGroupsPerGpu = 296.0;                 // 2 tile groups x 148 SMs
     double best_cost = 0;
