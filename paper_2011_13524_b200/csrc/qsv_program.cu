@@ -286,7 +286,9 @@ int qsv_program_create(int n, const qsv_op* ops, int nops, const qsv_plan_opts* 
   // jit 2: compile now; jit 1: now only if every pass is already loaded or
   // its structure was planned before (a parametric recompile, a repeated segment)
   // (structure seen before, e.g. a VQE recompile with new angles)
-  if (o.jit == 2 || (o.jit == 1 && (jit_all_cached(p) || jit_all_seen(p)))) {
+  bool need_jit = false;  // passes the interpreter cannot run
+  for (const TilePlan& tp : p->tiles) need_jit = need_jit || tp.jit_only;
+  if (o.jit == 2 || need_jit || (o.jit == 1 && (jit_all_cached(p) || jit_all_seen(p)))) {
     rc = jit_prepare(p);
     if (rc) {
       qsv_program_destroy(p);

@@ -118,6 +118,8 @@ struct TilePlan {
   std::string jit_src;
   bool jit_seen = false;  // the same pass structure was planned before in this process
   int jit_threads = 0;
+  int jit_groups = 0;     // tile groups per CTA of the generated kernel
+  bool jit_only = false;  // the interpreter cannot run this pass (more than 8 thread bits)
   size_t jit_smem = 0;
   std::vector<Cplx> jit_data;
   JitKernel jit;

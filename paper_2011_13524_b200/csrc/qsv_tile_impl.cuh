@@ -2306,6 +2306,13 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
     TilePlan tp;
     tp.variant = kRegBits;
     tp.L = L;
+    // the interpreter's thread-base tables hold 8 thread bits
+    tp.jit_only = L - kRegBits > 8;
+    if (tp.jit_only && !opts.jit) {
+      set_error("tile of %d qubits with %d amplitudes per thread needs generated kernels", L,
+                kRegs);
+      return QSV_EUNSUPPORTED;
+    }
     if (opts.jit && sizeof(JitParamHead) + sizeof(double2) * std::max<size_t>(1, e.data.size()) <=
                         kJitMaxParamBytes) {
       try {
@@ -2313,6 +2320,7 @@ int plan_program(int n, const std::vector<GateDesc>& gates_in, const qsv_plan_op
         tp.jit_seen = js.seen;
         tp.jit_src = std::move(js.src);
         tp.jit_threads = js.threads;
+        tp.jit_groups = js.groups;
         tp.jit_smem = js.smem;
         tp.jit_data = e.data;
         if (tp.jit_data.empty()) tp.jit_data.push_back(Cplx{0, 0});
@@ -2431,9 +2439,10 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     } else if (ntiles_all <= (uint64_t)sms * per_sm) {
       grid = (unsigned)ntiles_all;
     } else {
-      const uint64_t ctas = (ntiles_all + kGroups - 1) / kGroups;
+      const int groups = tp.jit_groups > 0 ? tp.jit_groups : kGroups;
+      const uint64_t ctas = (ntiles_all + groups - 1) / groups;
       grid = (unsigned)std::min<uint64_t>(ctas, (uint64_t)sms * per_sm);
-      h.nostagger = ntiles_all <= (uint64_t)kGroups * grid;
+      h.nostagger = ntiles_all <= (uint64_t)groups * grid;
     }
     if (ntiles_all <= (uint64_t)sms * per_sm) h.nostagger = 0;
     // deep passes: the generated code (~10 KB of SASS per phase) exceeds the
@@ -2459,6 +2468,10 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     cfg.numAttrs = 1;
     QSV_TRY(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(tp.jit.kernel), args));
     return QSV_OK;
+  }
+  if (tp.jit_only) {
+    set_error("tile pass needs its generated kernel (NVRTC compile failed or not prepared)");
+    return QSV_EUNSUPPORTED;
   }
   const size_t smem = kGroups * (sizeof(double2) << tp.L) + tp.nops * sizeof(TileOp) +
                       tp.ndata * sizeof(double2) + tp.nphases * sizeof(TilePhase);

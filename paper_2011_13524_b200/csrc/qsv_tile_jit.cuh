@@ -21,6 +21,7 @@ struct JitSource {
   std::string src;      // CUDA source of kernel "k_pass"
   int threads = 0;      // CTA threads
   int group_threads = 0;
+  int groups = 0;       // tile groups per CTA
   size_t smem = 0;      // dynamic shared memory
   int ndata = 0;        // double2 entries of the payload parameter
   bool seen = false;    // served from the source cache: this structure was planned before
@@ -764,15 +765,19 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   const int G = g.G;
   const int tidbits = L - kRegBits;
   js.group_threads = G;
-  js.threads = kGroups * G;
-  js.smem = (size_t)kGroups * (sizeof(double2) << L);
+  // one group per CTA when a group alone is 512 threads (8 amplitudes per
+  // thread on 12-qubit tiles): two would not fit the register file
+  const int groups = G >= 512 ? 1 : kGroups;
+  js.groups = groups;
+  js.threads = groups * G;
+  js.smem = (size_t)groups * (sizeof(double2) << L);
   js.ndata = std::max<int>(1, (int)e.data.size());
   std::string& o = g.o;
   o += jit_prelude();
   o += "#define QSV_G " + std::to_string(G) + "\n";
   o += "#define QSV_R2 " + std::to_string(kRegs) + "\n";
   o += std::string("constexpr bool jit_nohoist = ") + (jit_nohoist() ? "true" : "false") + ";\n";
-  o += "#define QSV_GROUPS " + std::to_string(kGroups) + "\n";
+  o += "#define QSV_GROUPS " + std::to_string(groups) + "\n";
   o += std::string("#define QSV_PDL_LATE ") + (jit_pdl_late() ? "1" : "0") + "\n";
   o += "struct __align__(16) PassParams { double2* a; u64 ntiles; u64* ctr; int nostagger; "
        "int stat; FixedBits tb; double2 d[" + std::to_string(js.ndata) + "]; };\n";
@@ -934,7 +939,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
       }
       wl = changed.empty();
       const int nsub = 1 << kept.size();              // subsets per group
-      const int ids = 3 + kGroups * nsub;             // named barriers 3.. (0: CTA, 1..2: groups)
+      const int ids = 3 + groups * nsub;              // named barriers 3.. (0: CTA, 1..2: groups)
       // one kept pattern per pass (the most frequent): its subsets are fixed
       // sets of warps, so each named barrier id is always used by the same
       // warps with the same count (two patterns would alias ids between warps

@@ -91,7 +91,8 @@ int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts&
     if (use3) {
       qsv_plan_opts o3 = o;
       if (o3.tile_qubits == 0) o3.tile_qubits = l3 ? l3 : 11;
-      o3.tile_qubits = std::min(o3.tile_qubits, 11);
+      // 12-qubit tiles (512 threads, one group per CTA) only as generated kernels
+      o3.tile_qubits = std::min(o3.tile_qubits, o.jit ? 12 : 11);
       return r3::plan_program(n, pre, o3, st, tp, pl, ps, nullptr, true);
     }
     return use5 ? r5::plan_program(n, pre, o, st, tp, pl, ps, nullptr, true)
