@@ -1231,8 +1231,10 @@ inline bool jit_direct_store() {
 inline std::mutex g_sel_mu;
 inline std::unordered_map<std::string, std::vector<PassSel>> g_sel_cache;
 
-// QSV_PASS_SEARCH: 0 plain greedy, 1 multi-start (default), 2 multi-start
-// with one pass of lookahead (A/B)
+// QSV_PASS_SEARCH: 0 plain greedy, 1 multi-start, 2 multi-start with one
+// pass of lookahead.  Unset: plan_program (qsv_tile_select.cu) plans modes 1
+// and 2 and keeps the plan with fewer passes; this default only serves
+// callers that plan once.
 inline int pass_search() {
   static const int mode = [] {
     const char* e = getenv("QSV_PASS_SEARCH");
