@@ -12,6 +12,7 @@ rotation angle changes.
 from __future__ import annotations
 
 import ctypes as C
+import struct
 
 import numpy as np
 
@@ -22,6 +23,8 @@ from ._lib import check, lib
 
 
 _OP_SIZE = C.sizeof(_lib.QsvOp)
+_ANGLE_OFF = _lib.QsvOp.angle.offset
+_put_angle = struct.Struct("<d").pack_into  # angle field of a packed qsv_op
 
 
 class _OpsCache:
@@ -38,10 +41,10 @@ class _OpsCache:
         self.rot = [(i, g) for i, g in enumerate(gates) if isinstance(g, PauliRotationGate)]
 
     def ops(self):
-        ops = (_lib.QsvOp * max(1, len(self.gates))).from_buffer_copy(self.blob)
+        blob = bytearray(self.blob)
         for i, g in self.rot:
-            ops[i].angle = g.angle
-        return ops
+            _put_angle(blob, i * _OP_SIZE + _ANGLE_OFF, g.angle)
+        return (_lib.QsvOp * max(1, len(self.gates))).from_buffer(blob)
 
 
 def fill_ops(gates, cache_owner=None):
@@ -58,8 +61,10 @@ def fill_ops(gates, cache_owner=None):
 def _fill_ops_uncached(gates):
     """qsv_op array for a gate list.  Each gate's op is built once and cached
     on the gate (with the arrays it points to); only angles are re-read."""
-    ops = (_lib.QsvOp * max(1, len(gates)))()
-    base = C.addressof(ops)
+    # packed into one buffer (slice copies + struct stores: a ctypes element
+    # proxy per gate cost several microseconds each on 600-gate circuits)
+    parts = []
+    rot = []
     for i, g in enumerate(gates):
         cached = getattr(g, "_op_cache", None)
         if cached is None:
@@ -68,10 +73,13 @@ def _fill_ops_uncached(gates):
             g.fill_op(tmp, keep)
             cached = (bytes(tmp), keep)
             g._op_cache = cached
-        C.memmove(base + i * _OP_SIZE, cached[0], _OP_SIZE)
+        parts.append(cached[0])
         if isinstance(g, PauliRotationGate):
-            ops[i].angle = g.angle
-    return ops
+            rot.append((i, g.angle))
+    blob = bytearray(b"".join(parts) if parts else bytes(_OP_SIZE))
+    for i, angle in rot:
+        _put_angle(blob, i * _OP_SIZE + _ANGLE_OFF, angle)
+    return (_lib.QsvOp * max(1, len(gates))).from_buffer(blob)
 
 
 class _Program:
