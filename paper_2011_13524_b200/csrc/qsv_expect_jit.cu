@@ -51,6 +51,7 @@ namespace qsv {
 constexpr int kEjTileQubits = 12;
 constexpr int kEjThreads = 256;
 constexpr int kEjMaxTermsStride = 44;  // partials stride (k_expect_tile_final)
+constexpr int kEjLanes = 3;            // passes in flight at once (forked streams)
 int launch_expect_tile_final(const double* partials, int nblocks, int nterms, double* out,
                              cudaStream_t s);
 
@@ -602,6 +603,44 @@ int jit_mode() {
 
 using namespace ej;
 
+// QSV_EXPECT_STREAMS: passes of one evaluation in flight at once (1: all on
+// the caller's stream, the pre-overlap behaviour)
+int ej_lanes() {
+  static const int v = [] {
+    const char* e = getenv("QSV_EXPECT_STREAMS");
+    const int k = e ? atoi(e) : kEjLanes;
+    return std::max(1, std::min(k, kEjLanes));
+  }();
+  return v;
+}
+
+// per-device auxiliary streams and fork / join events of the pass lanes
+struct EjLaneSet {
+  cudaStream_t streams[kEjLanes] = {};
+  cudaEvent_t fork = nullptr, join[kEjLanes] = {};
+};
+EjLaneSet* ej_lane_set(int dev) {
+  static EjLaneSet sets[64];
+  static bool made[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  EjLaneSet& L = sets[dev];
+  if (!made[dev]) {
+    for (int k = 1; k < kEjLanes; ++k) {
+      if (cudaStreamCreateWithFlags(&L.streams[k], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&L.join[k], cudaEventDisableTiming) != cudaSuccess)
+        return nullptr;
+    }
+    if (cudaEventCreateWithFlags(&L.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    made[dev] = true;
+  }
+  return &L;
+}
+
+size_t expect_jit_scratch_bytes() {
+  return sizeof(double) * ((size_t)kEjLanes * 2 * 296 * kEjMaxTermsStride +
+                           2 * (size_t)kEjMaxTermsStride * 32);
+}
+
 // Evaluate every term's S_t through generated pass kernels.  Returns
 // QSV_EUNSUPPORTED when the generated path is off or not (yet) compiled for
 // this observable -- the caller then runs the generic k_expect_tile.  Mode
@@ -664,36 +703,67 @@ int expect_tile_jit(const double2* a, int n, const std::vector<uint64_t>& xms,
   }
   const uint64_t ntiles = 1ULL << (n - kEjTileQubits);
   const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)std::min(num_sms, 296));
-  // scratch (expect_tile_scratch_bytes()): partials of one pass, then up to
-  // kEjBatch passes' results, copied back with one synchronisation per batch
+  // scratch (expect_jit_scratch_bytes()): partials of kEjLanes passes, then
+  // up to kEjBatch passes' results, copied back with one synchronisation per
+  // batch.  The passes only read the state and write their own partials, so
+  // they run on kEjLanes forked streams (pass p on lane p mod kEjLanes, its
+  // reduction after it on the same lane): one pass's ramp and tail overlap
+  // the next pass's sweep instead of idling HBM between kernels.
   constexpr size_t kEjBatch = 32;
   double* partials = reinterpret_cast<double*>(scratch);
-  double* dout = partials + 2 * (size_t)296 * kEjMaxTermsStride;
+  double* dout = partials + kEjLanes * 2 * (size_t)296 * kEjMaxTermsStride;
   const size_t smem = 2 * sizeof(double2) * (1u << kEjTileQubits);
   res.assign(2 * xms.size(), 0.0);
   std::vector<double> hout;
+  const int lanes = std::min<int>(ej_lanes(), (int)plan->passes.size());
+  cudaStream_t ls[kEjLanes];
+  for (int k = 0; k < kEjLanes; ++k) ls[k] = s;
+  EjLaneSet* L = nullptr;
+  if (lanes > 1) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    L = ej_lane_set(dev);
+    if (!L) return QSV_EUNSUPPORTED;
+    QSV_TRY(cudaEventRecord(L->fork, s));
+    for (int k = 1; k < lanes; ++k) {
+      ls[k] = L->streams[k];
+      QSV_TRY(cudaStreamWaitEvent(ls[k], L->fork, 0));
+    }
+  }
   for (size_t p0 = 0; p0 < plan->passes.size(); p0 += kEjBatch) {
     const size_t p1 = std::min(plan->passes.size(), p0 + kEjBatch);
     for (size_t p = p0; p < p1; ++p) {
       const EjPass& P = plan->passes[p];
+      const int lane = lanes > 1 ? (int)(p % lanes) : 0;
+      double* part = partials + lane * 2 * (size_t)296 * kEjMaxTermsStride;
       EjParams prm;
       memset(&prm, 0, sizeof(prm));
       prm.a = a;
       prm.ntiles = ntiles;
-      prm.partials = partials;
+      prm.partials = part;
       prm.tb = make_fixed(P.spos, kEjTileQubits, 0);
       QSV_TRY_RC(jit_set_smem(P.k, smem));
       void* args[] = {&prm};
       QSV_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(P.k.kernel), dim3(grid),
-                               dim3(kEjThreads), args, smem, s));
-      QSV_TRY_RC(launch_expect_tile_final(partials, (int)grid, P.nterms,
-                                          dout + 2 * kEjMaxTermsStride * (p - p0), s));
+                               dim3(kEjThreads), args, smem, ls[lane]));
+      QSV_TRY_RC(launch_expect_tile_final(part, (int)grid, P.nterms,
+                                          dout + 2 * kEjMaxTermsStride * (p - p0), ls[lane]));
       ++g_ej_jit_passes;
+    }
+    if (L) {  // join the lanes into s before the copy back
+      for (int k = 1; k < lanes; ++k) {
+        QSV_TRY(cudaEventRecord(L->join[k], ls[k]));
+        QSV_TRY(cudaStreamWaitEvent(s, L->join[k], 0));
+      }
     }
     hout.resize(2 * kEjMaxTermsStride * (p1 - p0));
     QSV_TRY(cudaMemcpyAsync(hout.data(), dout, hout.size() * sizeof(double),
                             cudaMemcpyDeviceToHost, s));
     QSV_TRY(cudaStreamSynchronize(s));
+    if (L && p1 < plan->passes.size()) {  // next batch: fork again
+      QSV_TRY(cudaEventRecord(L->fork, s));
+      for (int k = 1; k < lanes; ++k) QSV_TRY(cudaStreamWaitEvent(ls[k], L->fork, 0));
+    }
     for (size_t p = p0; p < p1; ++p) {
       int t = 0;
       for (const EjGroup& G : plan->passes[p].groups)

@@ -365,9 +365,12 @@ static bool pack_passes(int n, const std::vector<XTermIn>& terms,
 // + 2 * kXMaxTerms doubles.
 constexpr int kXBatch = 32;  // passes launched back to back before one synchronisation
 
+size_t expect_jit_scratch_bytes();  // qsv_expect_jit.cu (generated passes' layout)
+
 size_t expect_tile_scratch_bytes() {
-  return ((sizeof(XPass) * kXBatch + 255) / 256) * 256 +
-         sizeof(double) * (2 * (size_t)296 * kXMaxTerms + 2 * kXMaxTerms * kXBatch);
+  const size_t generic = ((sizeof(XPass) * kXBatch + 255) / 256) * 256 +
+                         sizeof(double) * (2 * (size_t)296 * kXMaxTerms + 2 * kXMaxTerms * kXBatch);
+  return std::max(generic, expect_jit_scratch_bytes());
 }
 
 int expect_tile(const double2* a, int n, const std::vector<uint64_t>& xms,
