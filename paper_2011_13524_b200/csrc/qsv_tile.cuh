@@ -120,6 +120,7 @@ struct TilePlan {
   int jit_threads = 0;
   int jit_groups = 0;     // tile groups per CTA of the generated kernel
   bool jit_only = false;  // the interpreter cannot run this pass (more than 8 thread bits)
+  bool pdl = false;       // launch with programmatic dependent launch (shallow programs)
   size_t jit_smem = 0;
   std::vector<Cplx> jit_data;
   JitKernel jit;

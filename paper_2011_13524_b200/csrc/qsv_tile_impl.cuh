@@ -1378,13 +1378,16 @@ inline bool jit_pdl_late() {
   return on != 0;
 }
 
-inline bool jit_pdl() {
-  static const int on = [] {
+// 0 never, 1 always, -1 (unset) per program: the planner marks programs of
+// shallow passes (TilePlan.pdl, qsv_tile_select.cu)
+inline int jit_pdl_mode() {
+  static const int v = [] {
     const char* e = getenv("QSV_PDL");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : -1;
   }();
-  return on != 0;
+  return v;
 }
+inline bool jit_pdl() { return jit_pdl_mode() == 1; }
 
 // QSV_ONE_FMA=0 keeps the plain real rotations (A/B experiments)
 inline bool one_fma_rotations() {
@@ -2465,7 +2468,8 @@ int launch_tile_pass(double2* amps, int n, const TilePlan& tp, const void* dev_p
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = jit_pdl() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed =
+        (jit_pdl_mode() == 1 || (jit_pdl_mode() < 0 && tp.pdl)) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     QSV_TRY(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(tp.jit.kernel), args));

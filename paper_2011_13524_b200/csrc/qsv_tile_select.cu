@@ -45,9 +45,35 @@ static PlanMix estimate_mix(const std::vector<GateDesc>& gates) {
 static std::mutex g_mode_mu;
 static std::unordered_map<std::string, int> g_mode_cache;  // structure -> search mode
 
+static int plan_program_impl(int n, const std::vector<GateDesc>& gates,
+                             const qsv_plan_opts& opts, std::vector<Step>& steps,
+                             std::vector<TilePlan>& tiles, std::vector<char>& payload,
+                             qsv_program_stats* stats);
+
+// Programmatic dependent launch per program: on small states it hides the
+// kernel boundary when every pass is shallow (cnot-ring(16) 0.100 -> 0.095 ms,
+// (17) 0.112 -> 0.111, (18) 0.134 -> 0.132) but costs deep passes up to 15%
+// (cz-ladder(12..18): the next pass's CTAs take SM slots while the current
+// pass still runs; profiles/r2_pdl_late_ab.md) and measured 6% slower on
+// cnot-ring(19) (r4 tiles, one CTA on 128 of 148 SMs), so it is used for the
+// small-state programs (n <= 18) whose passes have at most kPdlMaxPhases
+// phases (profiles/r2_pdl_auto_ab.md).
 int plan_program(int n, const std::vector<GateDesc>& gates, const qsv_plan_opts& opts,
                  std::vector<Step>& steps, std::vector<TilePlan>& tiles,
                  std::vector<char>& payload, qsv_program_stats* stats) {
+  const int rc = plan_program_impl(n, gates, opts, steps, tiles, payload, stats);
+  if (rc != QSV_OK) return rc;
+  constexpr int kPdlMaxPhases = 8;
+  bool shallow = n <= 18 && !tiles.empty();
+  for (const TilePlan& tp : tiles) shallow = shallow && tp.nphases <= kPdlMaxPhases;
+  for (TilePlan& tp : tiles) tp.pdl = shallow;
+  return QSV_OK;
+}
+
+static int plan_program_impl(int n, const std::vector<GateDesc>& gates,
+                             const qsv_plan_opts& opts, std::vector<Step>& steps,
+                             std::vector<TilePlan>& tiles, std::vector<char>& payload,
+                             qsv_program_stats* stats) {
   if (!steps.empty() || !tiles.empty() || !payload.empty()) {
     set_error("internal: plan_program expects empty outputs");
     return QSV_EINVAL;
