@@ -129,7 +129,7 @@ def test_unfit_flip_mask_is_unsupported():
 # ------------------------------------------------------------------ GPU
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", ["tfim14", "tfim20", "tfim24", "random16", "random18y",
-                                  "chunked13"])
+                                  "chunked13", "many18"])
 def test_generated_expectation_matches_oracle(case):
     import paper_2011_13524_b200 as qs
     from paper_2011_13524_b200 import workloads
@@ -143,6 +143,8 @@ def test_generated_expectation_matches_oracle(case):
     else:
         if case == "random16":
             n, terms = 16, random_terms(16, 60, 5)
+        elif case == "many18":  # 43 passes: two copy-back batches, three stream lanes
+            n, terms = 18, random_terms(18, 400, 7, max_len=10)
         elif case == "random18y":
             n = 18
             terms = random_terms(18, 40, 6, max_len=6)
