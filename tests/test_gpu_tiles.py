@@ -210,7 +210,7 @@ def test_planner_fuzz():
     """Random circuits (every gate kind, random widths) under random plan
     options and forced kernel variants, against the C oracle."""
     import os
-    rng = np.random.default_rng(2024)
+    rng = np.random.default_rng(int(os.environ.get("QSV_FUZZ_SEED", "2024")))
     for case in range(int(os.environ.get("QSV_FUZZ_CASES", "40"))):
         n = int(rng.integers(6, 19))
         L = int(rng.integers(6, 13))
