@@ -1313,6 +1313,18 @@ inline bool jit_late_sync() {
   return on != 0;
 }
 
+// QSV_JIT_LATE_WAIT=1: passes with statically assigned tiles wait for their
+// predecessor (PDL) at the first HBM load instead of kernel start.  Off:
+// mixed (cnot-ring(18) 0.133 -> 0.120 ms, (16) 0.095 -> 0.092, but (17)
+// 0.110 -> 0.125; profiles/r2_late_wait_ab.md)
+inline bool jit_late_wait() {
+  static const int on = [] {
+    const char* e = getenv("QSV_JIT_LATE_WAIT");
+    return e ? atoi(e) : 0;
+  }();
+  return on != 0;
+}
+
 // QSV_JIT_DIRECT_LOAD=0: tiles always enter through cp.async copy-in (A/B)
 inline bool jit_direct_load() {
   static const int on = [] {

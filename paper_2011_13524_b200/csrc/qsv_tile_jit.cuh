@@ -51,6 +51,10 @@ inline std::string deposit(const std::vector<int>& pos, const char* var) {
   return s + ")";
 }
 
+inline void replace_first(std::string& s, const std::string& from, const std::string& to) {
+  const size_t at = s.find(from);
+  if (at != std::string::npos) s.replace(at, from.size(), to);
+}
 inline uint32_t swz_host(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
 
 inline bool is_val(const Cplx& c, double re, double im) { return c.re == re && c.im == im; }
@@ -62,6 +66,7 @@ struct Gen {
   // emitted once, right before the tile's first shared-memory store (the
   // group barrier that protects the tile buffer, moved past the loads)
   std::string pre_store;
+  bool late_wait = false;  // static tiles wait for the previous pass at their first load
   explicit Gen(const Encoded& enc, int L_) : e(enc), L(L_), R(kRegBits), R2(kRegs) {
     G = 1 << (L - kRegBits);
   }
@@ -540,6 +545,8 @@ struct Gen {
       const uint32_t ad = cj[j];
       (void)ad;
       if (from_regs) continue;  // arrived by a shuffle transition
+      if (load_global && j == 0 && late_wait)
+        line("if (P.stat) asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");");
       if (load_global)
         line("v[" + std::to_string(j) + "] = ld1(a + (gl_ | " + hex64(gl_slot(P, j)) + "));");
       else
@@ -806,7 +813,7 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
   // previous pass drains; wait for its completion (and memory) before the
   // first read of the state or the work counter, and let the next pass's
   // CTAs queue behind this one as SMs free up
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // QSV_WAIT_AT_START
   if (!QSV_PDL_LATE) asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0)
     *s_go = (QSV_GROUPS < 2 || P.nostagger || P.stat || QSV_G < 32) ? QSV_GROUPS : 0;
@@ -871,6 +878,13 @@ inline JitSource jit_pass_source_gen(const Encoded& e, int L, std::vector<std::p
 )JIT";
   // first phase straight from HBM (no copy-in, no prefetch)
   const bool direct_load = jit_direct_load() && !e.phases.empty() && e.phases[0].type == 0;
+  // statically assigned tiles that load straight from HBM read no global
+  // memory before their first loads: wait for the previous pass there, so
+  // the prologue (tile index, thread deposits, addresses) overlaps its tail
+  if (direct_load && jit_late_wait())
+    replace_first(o, "asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");  // QSV_WAIT_AT_START",
+                  "if (!P.stat) asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");");
+  g.late_wait = direct_load && jit_late_wait();
   if (!direct_load) o += "  " + copy_of("tile") + "\n";
   // late sync (direct loads): the next tile's index stays in a register of
   // thread 0 and the group barrier that guards the tile buffer moves to the
